@@ -1,0 +1,396 @@
+"""ET-BFS benchmark on B200 — prints ONE JSON line (the driver's contract).
+
+Metric (BASELINE.json): harmonic-mean GTEPS over 64 roots, plus the fraction of
+the HBM TEPS roofline. Workload: Kronecker R-MAT scale 22 / edgefactor 16
+(BASELINE configs[1], the largest config quoted on one GPU that the same run can
+also time the reference on), generator seed 1, 64 roots from select_roots(seed
+1), ET mode mh=-1 with TEET (the reference's BenchConfig defaults,
+proj/include/etbfs/bench.hpp:30-45). Synthetic inputs produced by the
+reference's own generator algorithm stand in for the paper's Graph500 inputs.
+
+A "step" is one pass of the hot path over the 64 roots: per root, the
+start-side walk + one persistent kernel that runs the whole core DO-BFS and the
+edge-tree replay, results left in HBM. Per-root times come from CUDA events on
+the launching stream; L2 is flushed (a 2x-L2 memset) between roots outside the
+timed events.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--scale S] [--edgefactor E]
+                  [--mh M] [--impl ours|reference] [--no-cpu-baseline]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "harmonic-mean GTEPS over 64 roots at 1/2/4/8 B200; % of HBM TEPS roofline"
+NROOTS = 64
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def harmonic_gteps(te, seconds):
+    te = np.asarray(te, np.float64)
+    s = np.asarray(seconds, np.float64)
+    g = te / s / 1e9
+    return float(len(g) / np.sum(1.0 / g)), g
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during timing."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9:
+                    rows.append(f)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def b_alg(nc, ecore, ntree):
+    """algorithmic bytes per BFS (relaid space, u32 core ids)."""
+    return 4 * ecore + 8 * (nc + 1) + 8 * nc + 16 * ntree
+
+
+# --------------------------------------------------------------------- ours --
+def run_ours(args):
+    import paper_2009_07463_b200 as eb
+    from paper_2009_07463_b200 import etbfs as E
+
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    E.lib().etb_set_device(local)
+
+    t0 = time.perf_counter()
+    g = eb.generate_graph(scale=args.scale, edgefactor=args.edgefactor, seed=1)
+    t_csr = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    cg = eb.relayout_csr(g, mh=args.mh)
+    t_layout = time.perf_counter() - t1
+    preprocessing_s = time.perf_counter() - t0
+
+    # Roots: select_roots(original, 64, seed 1) (bench.cpp:217-242) in original ids.
+    roots = select_roots_from_degrees(g.degrees(), NROOTS, 1)
+    starts = cg.old2new[roots.astype(np.int64)]
+    if world > 1:
+        # replicas: rank r takes every world-th root (independent graph copies)
+        sel = np.arange(NROOTS) % world == rank
+        roots, starts = roots[sel], starts[sel]
+
+    te = np.empty(len(starts), np.uint64)
+    for i, s in enumerate(starts):
+        E.bfs_device(cg, int(s))
+        te[i] = E.result_traversed_edges(cg)
+
+    pol = eb.HybridPolicy()
+    reps = np.tile(starts, args.steps)
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        ms, kms = E.time_roots(cg, reps, warmup=args.warmup * len(starts), flush_l2=True,
+                               policy=pol)
+    if world > 1:
+        dist.barrier()
+    clocks = clk.summary()
+    sec = ms / 1e3
+    te_rep = np.tile(te, args.steps).astype(np.float64)
+    hm, per = harmonic_gteps(te_rep, sec)
+    giant = te_rep == te_rep.max()
+    hm_giant, _ = harmonic_gteps(te_rep[giant], sec[giant])
+    step_ms = float(ms.sum() / args.steps)
+    value = hm
+    if world > 1:
+        import torch
+        t = torch.tensor([step_ms, hm], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        mn = t.clone()
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+        step_ms = float(mx[0])
+        value = float(mn[1]) * world  # replicas: slowest rank's HM times the rank count
+
+    # Roofline of the dominant (only) kernel: algorithmic bytes / kernel time.
+    peak, peak_src = measured_peak_hbm()
+    balg = b_alg(cg.core_vertex_count, cg.restricted_edge_count, cg.tree_vertex_count)
+    kern_s = float(np.mean(kms)) / 1e3
+    achieved = balg / kern_s / 1e9
+    roof_gteps = peak * 1e9 / (balg / float(te.max())) / 1e9
+
+    # e2e: the reference-facing call with HOST output buffers (D2H inside the timing).
+    n = cg.vertex_count
+    depth_h = np.empty(n, np.int32)
+    parent_h = np.empty(n, np.uint64)
+    E.lib().etb_host_register(depth_h.ctypes.data, depth_h.nbytes)
+    E.lib().etb_host_register(parent_h.ctypes.data, parent_h.nbytes)
+    e2e_t = []
+    for s in starts:
+        c0 = time.perf_counter()
+        eb.etbfs._check(E.lib().etb_bfs(cg.handle, int(s), None, depth_h.ctypes.data,
+                                        parent_h.ctypes.data, None))
+        e2e_t.append(time.perf_counter() - c0)
+    E.lib().etb_host_unregister(depth_h.ctypes.data)
+    E.lib().etb_host_unregister(parent_h.ctypes.data)
+    e2e_hm, _ = harmonic_gteps(te.astype(np.float64), np.array(e2e_t))
+    if world > 1:
+        e2e_hm *= world
+
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-seed1",
+                   "scale": args.scale, "edgefactor": args.edgefactor, "roots": NROOTS,
+                   "root_seed": 1, "mh": args.mh, "replay": "teet", "alpha": 14.0, "beta": 24.0,
+                   "parallelism": "replicas" if world > 1 else "1gpu",
+                   "l2": "flushed between roots (2x L2 memset outside the timed events)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_source": peak_src, "algorithmic_bytes_per_bfs": int(balg),
+                     "bytes_per_te": round(balg / float(te.max()), 3),
+                     "roofline_gteps": round(roof_gteps, 1),
+                     "frac_of_roofline_gteps": round(hm_giant / roof_gteps, 4)},
+        "e2e": {"value": round(e2e_hm, 3), "unit": "GTEPS",
+                "h2d_bytes_per_step": 8 * len(starts),
+                "d2h_bytes_per_step": 12 * n * len(starts),
+                "api": "etb_bfs (C-ABI, host depth i32 + parent u64 outputs, pinned)"},
+        "gpu_launches": int(len(reps)),
+        "clocks": clocks,
+        "detail": {"mean_gteps": round(float(per.mean()), 3), "min_gteps": round(float(per.min()), 3),
+                   "max_gteps": round(float(per.max()), 3),
+                   "hm_gteps_giant_component": round(hm_giant, 3),
+                   "kernel_ms_mean": round(float(np.mean(kms)), 4),
+                   "call_ms_mean": round(float(np.mean(ms)), 4),
+                   "traversed_edges": int(te.max()),
+                   "core_vertices": int(cg.core_vertex_count),
+                   "tree_vertices": int(cg.tree_vertex_count),
+                   "core_directed_edges": int(cg.restricted_edge_count),
+                   "preprocessing_s": round(preprocessing_s, 3),
+                   "generate_build_csr_s": round(t_csr, 3), "classify_relayout_s": round(t_layout, 3)},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, roots[: args.cpu_roots])
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def select_roots_from_degrees(deg, count, seed):
+    """select_roots (bench.cpp:217-242) from a degree array (original ids)."""
+    n = len(deg)
+    eligible = int(np.count_nonzero(deg))
+    taken = np.zeros(n, bool)
+    out, distinct = [], 0
+    state = seed
+    M = 0xFFFFFFFFFFFFFFFF
+    while len(out) < count:
+        state = (state + 0x9E3779B97F4A7C15) & M
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        z ^= z >> 31
+        v = z % n
+        if deg[v] == 0:
+            continue
+        if taken[v] and distinct < eligible:
+            continue
+        if not taken[v]:
+            taken[v] = True
+            distinct += 1
+        out.append(v)
+    return np.array(out, np.uint64)
+
+
+# ---------------------------------------------------------------- reference --
+def ref_pipeline(scale, ef, mh, threads):
+    """The reference's own untimed preprocessing (bench.cpp:253-256) via oracle/_ref."""
+    import oracle as O
+    O.ref().ref_set_threads(threads)
+    t0 = time.perf_counter()
+    pairs = O.ref_generate(scale, ef, 1)
+    csr = O.RefCsr(1 << scale, pairs)
+    del pairs
+    prep = O.RefPrepared(csr, mh)
+    a = prep.arrays()
+    deg = np.diff(a["row"]).astype(np.int64)
+    old2new = np.empty(1 << scale, np.int64)
+    old2new[a["new2old"].astype(np.int64)] = np.arange(1 << scale)
+    return csr, prep, deg, old2new, time.perf_counter() - t0
+
+
+def ref_time_roots(prep, deg, starts):
+    """Time the reference's et_bfs (the timed `traverse`, bench.cpp:269-271) per root."""
+    secs, tes = [], []
+    for s in starts:
+        par, _, sec = prep.et_bfs(int(s), kernel=1, replay=0)
+        tes.append(int(deg[par != 0xFFFFFFFFFFFFFFFF].sum() // 2))
+        secs.append(sec)
+    return np.array(secs), np.array(tes, np.float64)
+
+
+def cpu_baseline(args, roots_orig):
+    import oracle as O
+    if not O.ref_available():
+        return {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    threads = os.cpu_count() or 1
+    csr, prep, deg, old2new, prep_s = ref_pipeline(args.scale, args.edgefactor, args.mh, threads)
+    starts = old2new[roots_orig.astype(np.int64)]
+    secs, tes = ref_time_roots(prep, deg, starts)
+    hm, _ = harmonic_gteps(tes, secs)
+    return {"value": round(hm, 4), "unit": "GTEPS", "cores": threads, "kind": "reference",
+            "sample": f"reference et_bfs (kHybrid, TEET, mh={args.mh}) on the first "
+                      f"{len(starts)} of the 64 seed-1 roots, s{args.scale}/ef{args.edgefactor}, "
+                      f"{threads} OpenMP threads; reference preprocessing {prep_s:.1f}s untimed",
+            "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    threads = os.cpu_count() or 1
+    csr, prep, deg, old2new, prep_s = ref_pipeline(args.scale, args.edgefactor, args.mh, threads)
+    roots = csr.select_roots(NROOTS, 1)
+    starts = old2new[roots.astype(np.int64)]
+    per_step = args.ref_roots_per_step
+    for w in range(args.warmup):
+        ref_time_roots(prep, deg, starts[(w * per_step) % NROOTS:][:per_step])
+    secs, tes = [], []
+    for k in range(args.steps):
+        sl = [(k * per_step + j) % NROOTS for j in range(per_step)]
+        s, t = ref_time_roots(prep, deg, starts[sl])
+        secs.append(s)
+        tes.append(t)
+    secs = np.concatenate(secs)
+    tes = np.concatenate(tes)
+    hm, per = harmonic_gteps(tes, secs)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(hm, 4), "unit": "GTEPS",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(float(secs.sum() / args.steps * 1e3), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-seed1",
+                   "scale": args.scale, "edgefactor": args.edgefactor, "roots": NROOTS,
+                   "root_seed": 1, "mh": args.mh, "replay": "teet", "alpha": 14.0, "beta": 24.0,
+                   "parallelism": f"openmp{threads}"},
+        "cpu_baseline": {"value": round(hm, 4), "unit": "GTEPS", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{per_step} roots per step (round robin over the 64 seed-1 "
+                                   f"roots), unmodified reference et_bfs via oracle/_ref",
+                         "cpu_model": cpu_model()},
+        "e2e": {"value": round(hm, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "detail": {"mean_gteps": round(float(per.mean()), 4), "preprocessing_s": round(prep_s, 2)},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--edgefactor", type=int, default=16)
+    ap.add_argument("--mh", type=int, default=-1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-roots", type=int, default=16)
+    ap.add_argument("--ref-roots-per-step", type=int, default=4)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/* etbfs_cuda.h — the C-ABI drop-in boundary of the B200 edge-tree BFS.
+ *
+ * Plain C: pointers, sizes and int status codes; no torch or C++ types.
+ * Every entry point returns ETB_OK (0) or a negative status and never lets
+ * a C++ exception cross the ABI; etb_last_error() holds the message, which
+ * for caller errors is the reference's own message text.
+ *
+ * Each function names the reference interface it replaces
+ * (paths relative to /root/reference/proj):
+ *
+ *   etb_generate_kronecker      include/etbfs/kronecker.hpp:34  generate_kronecker
+ *   etb_graph_from_edges        include/etbfs/build.hpp:19      build_csr
+ *   etb_graph_generate          kronecker.hpp:34 + build.hpp:19 (fused, tuples never leave HBM)
+ *   etb_graph_download          include/etbfs/types.hpp:38-50   CsrGraph fields
+ *   etb_classify                include/etbfs/classify.hpp:33   classify_vertices
+ *   etb_peak_height             include/etbfs/classify.hpp:38   compute_peak_height
+ *   etb_layout_build(_types)    include/etbfs/relayout.hpp:40   relayout_csr
+ *   etb_layout_download_etl     include/etbfs/relayout.hpp:52   extract_edge_tree_list
+ *   etb_bfs / etb_bfs_device    include/etbfs/et_bfs.hpp:53     et_bfs (CoreKernel::kHybrid)
+ *   etb_layout_restricted_edges include/etbfs/bfs.hpp:123       restricted_edge_count
+ *
+ * Index spaces: "original" ids are the input graph's; "relaid" ids are the
+ * relayout_csr space (core block [0, core), then edge trees, then isolated
+ * vertices), exactly as the reference's ClassifiedGraph.
+ */
+#ifndef ETBFS_CUDA_H
+#define ETBFS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ETB_OK 0
+#define ETB_EINVAL -1   /* std::invalid_argument in the reference */
+#define ETB_ERUNTIME -2 /* std::runtime_error in the reference */
+#define ETB_ECUDA -3    /* CUDA / NCCL failure (no reference analogue) */
+#define ETB_ENOTSUP -4  /* not available in this build */
+
+#define ETB_NO_VERTEX UINT64_MAX /* types.hpp:13 kNoVertex */
+#define ETB_UNREACHED_DEPTH (-1)
+
+/* VertexType numbering, types.hpp:55-61 */
+enum { ETB_CI = 0, ETB_CE = 1, ETB_TI = 2, ETB_TL = 3, ETB_VZ = 4 };
+
+/* CoreKernel (et_bfs.hpp:10-16) values accepted by etb_bfs. */
+enum { ETB_KERNEL_TOP_DOWN = 0, ETB_KERNEL_HYBRID = 1 };
+/* TreeReplay (et_bfs.hpp:19-22). */
+enum { ETB_REPLAY_TEET = 0, ETB_REPLAY_TEOLV = 1 };
+
+typedef struct etb_graph etb_graph;   /* device CSR, original ids */
+typedef struct etb_layout etb_layout; /* device ET layout, relaid ids, BFS-ready */
+
+typedef struct {
+  uint32_t scale;      /* kronecker.hpp:12-20 KroneckerParams */
+  uint64_t edgefactor;
+  double a, b, c, d;
+  uint64_t seed;
+} etb_kron_params;
+
+typedef struct {
+  uint64_t vertex_count;
+  uint64_t core_vertex_count;   /* ClassifiedGraph::core_vertex_count */
+  uint64_t tree_vertex_count;   /* EdgeTreeList size */
+  uint64_t isolated_count;
+  uint64_t core_directed_edges; /* restricted_edge_count(graph, core) */
+  uint64_t directed_edges;      /* whole relabelled graph */
+  uint64_t tree_count;
+  uint64_t max_tree_size;
+  int64_t mh;
+} etb_layout_info;
+
+typedef struct {
+  int kernel;        /* ETB_KERNEL_* */
+  int replay;        /* ETB_REPLAY_* */
+  double alpha;      /* HybridPolicy, bfs.hpp:19-22 */
+  double beta;
+} etb_bfs_options;
+
+typedef struct {
+  uint32_t levels;           /* KernelStats::levels */
+  uint32_t bottom_up_levels; /* KernelStats::bottom_up_levels */
+  char direction_trace[256]; /* KernelStats::direction_trace, NUL-terminated */
+  uint64_t level_claims[256];
+} etb_bfs_stats;
+
+/* ---- library ------------------------------------------------------------ */
+const char* etb_last_error(void);
+int etb_version(void);
+int etb_device_count(int* count);
+int etb_set_device(int device);
+
+/* ---- (1) graph construction --------------------------------------------- */
+/* Writes 2 * 2^scale * edgefactor u64 (src, dst) into host out_pairs. */
+int etb_generate_kronecker(const etb_kron_params* p, uint64_t* out_pairs);
+int etb_graph_from_edges(uint64_t vertex_count, const uint64_t* pairs, uint64_t count,
+                         etb_graph** out, uint64_t* dropped_self_loops,
+                         uint64_t* dropped_duplicates);
+int etb_graph_generate(const etb_kron_params* p, etb_graph** out, uint64_t* dropped_self_loops,
+                       uint64_t* dropped_duplicates);
+int etb_graph_info(const etb_graph* g, uint64_t* vertex_count, uint64_t* directed_edges);
+/* Any output may be NULL. row_offsets: n+1 u64, cols: directed_edges u64, degrees: n u64. */
+int etb_graph_download(const etb_graph* g, uint64_t* row_offsets, uint64_t* cols,
+                       uint64_t* degrees);
+void etb_graph_free(etb_graph* g);
+
+/* ---- (2) edge-tree preprocessing ----------------------------------------- */
+/* types_out (n u8, may be NULL); counts_out (5 u64 CI/CE/TI/TL/VZ, may be NULL). */
+int etb_classify(const etb_graph* g, int64_t mh, uint8_t* types_out, uint64_t* counts_out);
+int etb_peak_height(const etb_graph* g, uint64_t* peak_height);
+/* classify_vertices(g, mh) + relayout_csr + extract_edge_tree_list, on device. */
+int etb_layout_build(const etb_graph* g, int64_t mh, etb_layout** out);
+/* relayout_csr(g, types, mh) with caller-supplied types (host, n u8). */
+int etb_layout_build_types(const etb_graph* g, const uint8_t* types, int64_t mh,
+                           etb_layout** out);
+int etb_layout_info_get(const etb_layout* L, etb_layout_info* info);
+/* new2old / old2new (n u64), types (n u8); any may be NULL. */
+int etb_layout_download_maps(const etb_layout* L, uint64_t* new2old, uint64_t* old2new,
+                             uint8_t* types);
+/* The whole relabelled CSR (relabel_graph, build.cpp:144-166): row_offsets n+1,
+ * cols info.directed_edges, both u64. */
+int etb_layout_download_graph(const etb_layout* L, uint64_t* row_offsets, uint64_t* cols);
+/* EdgeTreeList (relayout.hpp:52): tree_vertex_count entries sorted by dst;
+ * core_edge uses ETB_NO_VERTEX for whole-component trees. */
+int etb_layout_download_etl(const etb_layout* L, uint64_t* src, uint64_t* dst,
+                            uint64_t* core_edge);
+int etb_layout_restricted_edges(const etb_layout* L, uint64_t* count);
+void etb_layout_free(etb_layout* L);
+
+/* ---- (3)+(4) traversal ----------------------------------------------------- */
+/* et_bfs from relaid `start`, results stay in HBM (the timed hot path). opts may be NULL
+ * (kHybrid, kTeet, α=14, β=24). stats may be NULL (then no device->host copy). */
+int etb_bfs_device(etb_layout* L, uint64_t start, const etb_bfs_options* opts,
+                   etb_bfs_stats* stats);
+/* et_bfs with host outputs (the reference-facing call): depth (n i32, -1 unreached)
+ * and/or parent (n u64, ETB_NO_VERTEX unreached), relaid ids. */
+int etb_bfs(etb_layout* L, uint64_t start, const etb_bfs_options* opts, int32_t* depth_out,
+            uint64_t* parent_out, etb_bfs_stats* stats);
+/* Device pointers to the last result (n entries each, relaid ids). */
+int etb_result_device_ptrs(etb_layout* L, int32_t** depth, uint32_t** parent);
+/* Copy the last result to host as compact i32 depth / u32 parent (UINT32_MAX unreached). */
+int etb_result_download(etb_layout* L, int32_t* depth, uint32_t* parent);
+/* ½ Σ full degree over reached vertices of the last result (validate.cpp:151-156). */
+int etb_result_traversed_edges(etb_layout* L, uint64_t* te);
+/* Page-lock a caller buffer so result downloads run at full link speed. */
+int etb_host_register(void* ptr, uint64_t bytes);
+int etb_host_unregister(void* ptr);
+
+/* ---- measurement ---------------------------------------------------------- */
+/* Times etb_bfs_device per start with CUDA events on the layout's stream, after
+ * `warmup` untimed runs; flush_l2 != 0 writes a >L2 buffer between roots (outside
+ * the timed events). ms_out[i] per start. kernel_ms_out (may be NULL) receives the
+ * BFS kernel's own event-timed duration per start. */
+int etb_time_roots(etb_layout* L, const uint64_t* starts, uint64_t count, int warmup,
+                   int flush_l2, const etb_bfs_options* opts, double* ms_out,
+                   double* kernel_ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ETBFS_CUDA_H */

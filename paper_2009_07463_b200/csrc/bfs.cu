@@ -1,0 +1,542 @@
+// (3)+(4) The ET-BFS traversal on sm_100a: one persistent cooperative kernel
+// per root runs the whole of et_bfs (src/et_bfs.cpp:59-124) —
+//   init            visited/frontier bitmaps sized to the CORE (not n), seeded
+//                   with the effective start (et_bfs.cpp:96-98);
+//   level loop      the reference's α/β direction-optimizing driver
+//                   (src/bfs.cpp:232-293), decided redundantly by every thread
+//                   from grid-reduced counters, with no host round trip;
+//                     top-down  (bfs.cpp:61-86): work items are 256-edge chunks
+//                               of frontier rows, one warp per item, check-then-
+//                               atomicOr claims, claimed vertices staged in smem
+//                               and appended with one atomic per item;
+//                     bottom-up (bfs.cpp:88-111): one warp per 32-vertex visited
+//                               word, first probe on the contiguous first-
+//                               neighbour array (the highest-degree neighbour,
+//                               since relaid ids are degree sorted), early exit,
+//                               one word write-back per warp;
+//   tree replay     TEET/TEOLV (et_bfs.cpp:14-32) as one streaming pass giving
+//                   every tree vertex parent = src and depth = depth(anchor) +
+//                   tree depth; unreached core vertices get -1 in the same phase;
+//   start tree      the start-side walk (et_bfs.cpp:34-57) is precomputed on the
+//                   host and applied as a patch.
+// Levels are separated by a grid barrier; the grid is one wave of co-resident
+// CTAs (cooperative launch).
+#include <algorithm>
+
+#include "bfs.cuh"
+
+namespace etb {
+namespace {
+
+constexpr int kBlock = 512;
+constexpr int kWarps = kBlock / 32;
+constexpr int kItemShift = 36;
+constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
+
+struct Smem {
+  uint32_t cbuf[kWarps][kTdChunk];
+  unsigned long long red[kWarps];
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// Monotonic-counter grid barrier: every CTA adds 1; the barrier of a CTA that
+// saw value `old` completes at the next multiple of gridDim.x.
+__device__ void grid_sync(unsigned long long* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long nb = gridDim.x;
+    __threadfence();
+    const unsigned long long old = atomicAdd(bar, 1ull);
+    const unsigned long long target = (old / nb + 1) * nb;
+    const long long t0 = clock64();
+    while (ld_acquire(bar) < target) {
+      if (clock64() - t0 > 40000000000ll) __trap();  // ~20 s: never hang the GPU
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ void block_add(unsigned long long v, unsigned long long* dst, Smem& sm) {
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sm.red[wib] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = lane < kWarps ? sm.red[lane] : 0ull;
+    v = warp_sum(v);
+    if (lane == 0 && v) atomicAdd(dst, v);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool test_bit(const uint32_t* bm, uint32_t v) {
+  return (bm[v >> 5] >> (v & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t nchunks(uint64_t d) {
+  return static_cast<uint32_t>((d + kTdChunk - 1) / kTdChunk);
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const unsigned lane = threadIdx.x & 31;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// Append the items (row chunks) of `ncl` claimed vertices staged in cbuf;
+// one atomic per call carries both the claim count and the item count.
+__device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, uint32_t ncl,
+                             uint64_t* items_out, unsigned long long* slot,
+                             unsigned long long& scout_acc) {
+  const unsigned lane = threadIdx.x & 31;
+  unsigned long long nit = 0, sc = 0;
+  for (uint32_t i = lane; i < ncl; i += 32) {
+    const uint32_t w = cbuf[i];
+    nit += nchunks(p.crow[w + 1] - p.crow[w]);
+    sc += p.degn[w];
+  }
+  nit = warp_sum(nit);
+  sc = warp_sum(sc);
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(slot, ((unsigned long long)ncl << kItemShift) | nit) & kItemMask;
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (lane == 0) scout_acc += sc;
+  for (uint32_t i0 = 0; i0 < ncl; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    uint32_t w = 0, c = 0;
+    if (i < ncl) {
+      w = cbuf[i];
+      c = nchunks(p.crow[w + 1] - p.crow[w]);
+    }
+    const uint32_t incl = warp_incl_scan(c);
+    uint64_t pos = base + incl - c;
+    for (uint32_t k = 0; k < c; ++k) items_out[pos + k] = (uint64_t(w) << 32) | k;
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+__device__ void td_step(const BfsParams& p, Smem& sm, const uint64_t* items_in, uint64_t nitems,
+                        uint64_t* items_out, uint32_t* fnext, unsigned long long* slot,
+                        int32_t dnext, unsigned long long& scout_acc) {
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  uint32_t* cbuf = sm.cbuf[wib];
+  for (uint64_t it = gw; it < nitems; it += nw) {
+    const uint64_t item = items_in[it];
+    const uint32_t u = static_cast<uint32_t>(item >> 32);
+    const uint32_t k = static_cast<uint32_t>(item);
+    const uint64_t beg = p.crow[u] + (uint64_t)k * kTdChunk;
+    const uint64_t end = min(p.crow[u + 1], beg + kTdChunk);
+    uint32_t ncl = 0;
+    for (uint64_t e0 = beg; e0 < end; e0 += 32) {
+      const uint64_t e = e0 + lane;
+      bool claim = false;
+      uint32_t w = 0;
+      if (e < end) {
+        w = p.ccol[e];
+        const uint32_t bit = 1u << (w & 31);
+        if (!(p.visited[w >> 5] & bit)) claim = !(atomicOr(&p.visited[w >> 5], bit) & bit);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, claim);
+      if (claim) {
+        p.depth[w] = dnext;
+        p.parent[w] = u;
+        atomicOr(&fnext[w >> 5], 1u << (w & 31));
+        cbuf[ncl + __popc(m & ((1u << lane) - 1))] = w;
+      }
+      ncl += __popc(m);
+    }
+    __syncwarp();
+    if (ncl) flush_claims(p, cbuf, ncl, items_out, slot, scout_acc);
+    __syncwarp();
+  }
+}
+
+__device__ void bu_step(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext, int32_t dnext,
+                        unsigned long long& claims_acc) {
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t wi = gw; wi < p.nwords; wi += nw) {
+    const uint32_t vis = p.visited[wi];  // a BU level writes word wi from this warp only
+    if (vis == 0xFFFFFFFFu) continue;
+    const uint32_t v = static_cast<uint32_t>(wi * 32 + lane);
+    bool claim = false;
+    uint32_t par = 0;
+    if (!((vis >> lane) & 1u)) {  // padding bits past nc are pre-set in `visited`
+      const uint32_t f = p.cfirst[v];
+      if (f != kNone32) {
+        if (test_bit(fcur, f)) {
+          claim = true;
+          par = f;
+        } else {
+          const uint64_t re = p.crow[v + 1];
+          for (uint64_t e = p.crow[v] + 1; e < re; ++e) {
+            const uint32_t x = p.ccol[e];
+            if (test_bit(fcur, x)) {
+              claim = true;
+              par = x;
+              break;
+            }
+          }
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, claim);
+    if (claim) {
+      p.depth[v] = dnext;
+      p.parent[v] = par;
+    }
+    if (lane == 0 && m) {
+      p.visited[wi] = vis | m;
+      fnext[wi] = m;
+      claims_acc += __popc(m);
+    }
+  }
+}
+
+// Frontier bitmap -> top-down work items (needed only when a bottom-up phase
+// hands over to top-down). Lane = one bitmap word.
+__device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint64_t* items_out,
+                             unsigned long long* cslot) {
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t w0 = gw * 32; w0 < p.nwords; w0 += nw * 32) {
+    const uint64_t wi = w0 + lane;
+    const uint32_t bits = wi < p.nwords ? fcur[wi] : 0u;
+    uint32_t cnt = 0;
+    for (uint32_t b = bits; b; b &= b - 1) {
+      const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
+      cnt += nchunks(p.crow[v + 1] - p.crow[v]);
+    }
+    const uint32_t incl = warp_incl_scan(cnt);
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(cslot, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    uint64_t pos = base + incl - cnt;
+    for (uint32_t b = bits; b; b &= b - 1) {
+      const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
+      const uint32_t c = nchunks(p.crow[v + 1] - p.crow[v]);
+      for (uint32_t k = 0; k < c; ++k) items_out[pos++] = (uint64_t(v) << 32) | k;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
+  __shared__ Smem sm;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t start = p.start;
+  const bool run_core = start != kNone32;
+
+  // ---- init: core-sized state only (the reference allocates n-sized state,
+  // et_bfs.cpp:82,96) --------------------------------------------------------
+  const uint32_t tail = p.nc & 31u;
+  for (uint64_t i = tid; i < p.nwords; i += nthreads) {
+    uint32_t vis = 0, f0 = 0;
+    if (i == p.nwords - 1 && tail) vis = ~0u << tail;  // padding reads as visited
+    if (run_core && i == (start >> 5)) {
+      vis |= 1u << (start & 31);
+      f0 = 1u << (start & 31);
+    }
+    p.visited[i] = vis;
+    p.fb0[i] = f0;
+    p.fb1[i] = 0;
+    p.fb2[i] = 0;
+  }
+  if (tid < 24) p.ctr[tid] = 0;
+  uint64_t nitems = 0;
+  if (run_core) {
+    nitems = nchunks(p.crow[start + 1] - p.crow[start]);
+    for (uint64_t k = tid; k < nitems; k += nthreads) p.items0[k] = (uint64_t(start) << 32) | k;
+    if (tid == 0) {
+      p.depth[start] = p.base_depth;
+      p.parent[start] = p.start_parent;
+    }
+  }
+  grid_sync(p.bar);
+
+  // ---- level loop: run_hybrid (bfs.cpp:232-293) ---------------------------------
+  uint32_t L = 0;
+  if (run_core) {
+    uint32_t* F[3] = {p.fb0, p.fb1, p.fb2};
+    uint64_t* items_in = p.items0;
+    uint64_t* items_out = p.items1;
+    unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0;
+    double etc = p.edges_to_check;
+    bool bu = !p.top_down_only && (double)scout > etc / p.alpha;
+    if (bu) awake = frontier;
+    for (;;) {
+      uint32_t* fcur = F[L % 3];
+      uint32_t* fnext = F[(L + 1) % 3];
+      uint32_t* fzero = F[(L + 2) % 3];
+      unsigned long long* slot = p.ctr + (L & 3) * 4;
+      for (uint64_t i = tid; i < p.nwords; i += nthreads) fzero[i] = 0;
+      if (tid == 0) {
+        p.ctr[((L + 2) & 3) * 4 + 0] = 0;
+        p.ctr[((L + 2) & 3) * 4 + 1] = 0;
+        p.ctr[16 + ((L + 1) & 1)] = 0;
+        if (p.trace && L < 255) p.trace[L] = bu ? 'b' : 't';
+      }
+      const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
+      unsigned long long acc = 0;
+      if (bu) {
+        prev = awake;
+        bu_step(p, fcur, fnext, dnext, acc);
+        block_add(acc << kItemShift, &slot[0], sm);
+      } else {
+        etc -= (double)scout;
+        td_step(p, sm, items_in, nitems, items_out, fnext, slot, dnext, acc);
+        block_add(acc, &slot[1], sm);
+      }
+      grid_sync(p.bar);
+      const unsigned long long packed = ld_volatile(&slot[0]);
+      const unsigned long long claims = packed >> kItemShift;
+      if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = claims;
+      ++L;
+      bool need_convert = false;
+      if (bu) {
+        awake = claims;
+        if (!(awake > 0 && (awake >= prev || (double)awake > (double)p.nc / p.beta))) {
+          bu = false;
+          frontier = awake;
+          scout = 1;
+          need_convert = true;
+        }
+      } else {
+        frontier = claims;
+        scout = ld_volatile(&slot[1]);
+        nitems = packed & kItemMask;
+        uint64_t* t = items_in;
+        items_in = items_out;
+        items_out = t;
+      }
+      if (!bu) {
+        if (frontier == 0) break;
+        if (!p.top_down_only && (double)scout > etc / p.alpha) {
+          bu = true;
+          awake = frontier;
+          need_convert = false;
+        }
+      }
+      if (need_convert) {
+        unsigned long long* cslot = p.ctr + 16 + (L & 1);
+        convert_step(p, F[L % 3], items_in, cslot);
+        grid_sync(p.bar);
+        nitems = ld_volatile(cslot);
+      }
+    }
+  }
+  if (tid == 0 && p.nlevels) *p.nlevels = L;
+
+  // ---- unreached core vertices + tree replay + start-tree patch ----------------
+  for (uint64_t v = tid; v < p.nc; v += nthreads) {
+    if (!test_bit(p.visited, static_cast<uint32_t>(v))) {
+      p.depth[v] = -1;
+      p.parent[v] = kNone32;
+    }
+  }
+  for (uint64_t t = tid; t < p.nt; t += nthreads) {
+    const uint32_t tv = static_cast<uint32_t>(p.nc + t);
+    if (tv >= p.skip_lo && tv < p.skip_hi) continue;
+    const uint32_t a = p.tanchor[t];
+    if (a != kNone32 && test_bit(p.visited, a)) {
+      p.depth[tv] = __ldcg(&p.depth[a]) + static_cast<int32_t>(p.tdepth[t]);
+      p.parent[tv] = p.tsrc[t];
+    } else {
+      p.depth[tv] = -1;
+      p.parent[tv] = kNone32;
+    }
+  }
+  for (uint64_t i = tid; i < p.npatch; i += nthreads) {
+    const uint32_t v = p.patch[3 * i];
+    p.depth[v] = static_cast<int32_t>(p.patch[3 * i + 1]);
+    p.parent[v] = p.patch[3 * i + 2];
+  }
+}
+
+}  // namespace
+
+void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
+  const uint64_t n = L.n;
+  S.n = n;
+  const uint64_t words = (L.nc + 31) / 32 + 1;
+  S.visited.alloc(words);
+  S.fb0.alloc(words);
+  S.fb1.alloc(words);
+  S.fb2.alloc(words);
+  const uint64_t cap = L.nc + L.ecore / kTdChunk + 2;
+  S.items0.alloc(cap);
+  S.items1.alloc(cap);
+  S.ctr.alloc(32);
+  S.bar.alloc(1);
+  ETB_CUDA(cudaMemsetAsync(S.bar.get(), 0, 8, s));
+  S.depth.alloc(n ? n : 1);
+  S.parent.alloc(n ? n : 1);
+  // Isolated vertices stay unreached unless they are the start; everything
+  // else is rewritten by every traversal.
+  ETB_CUDA(cudaMemsetAsync(S.depth.get(), 0xFF, (n ? n : 1) * 4, s));
+  ETB_CUDA(cudaMemsetAsync(S.parent.get(), 0xFF, (n ? n : 1) * 4, s));
+  S.trace.alloc(256);
+  S.level_claims.alloc(256);
+  S.nlevels.alloc(1);
+  const uint64_t pcap = std::max<uint64_t>(L.max_tree, 1) + 2;
+  S.patch.alloc(3 * pcap);
+  S.h_patch.alloc(3 * pcap);
+  if (!S.patch_done) ETB_CUDA(cudaEventCreateWithFlags(&S.patch_done, cudaEventDisableTiming));
+  int dev = 0, sms = 0, per_sm = 0;
+  ETB_CUDA(cudaGetDevice(&dev));
+  ETB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, et_bfs_kernel, kBlock, 0));
+  if (per_sm < 1) throw CudaError("et_bfs_kernel cannot be resident");
+  S.block = kBlock;
+  S.grid = sms * std::min(per_sm, 2);
+  ETB_CUDA(cudaStreamSynchronize(s));
+}
+
+void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
+  p.crow = L.crow.get();
+  p.ccol = L.ccol.get();
+  p.cfirst = L.cfirst.get();
+  p.degn = L.degn.get();
+  p.nc = static_cast<uint32_t>(L.nc);
+  p.nwords = static_cast<uint32_t>((L.nc + 31) / 32);
+  p.tsrc = L.tsrc.get();
+  p.tanchor = L.tanchor.get();
+  p.tdepth = L.tdepth.get();
+  p.nt = static_cast<uint32_t>(L.nt);
+  p.visited = S.visited.get();
+  p.fb0 = S.fb0.get();
+  p.fb1 = S.fb1.get();
+  p.fb2 = S.fb2.get();
+  p.items0 = S.items0.get();
+  p.items1 = S.items1.get();
+  p.ctr = S.ctr.get();
+  p.bar = S.bar.get();
+  p.depth = S.depth.get();
+  p.parent = S.parent.get();
+  p.patch = S.patch.get();
+  p.npatch = 0;
+  p.edges_to_check = static_cast<double>(L.ecore);
+  p.trace = nullptr;
+  p.level_claims = nullptr;
+  p.nlevels = nullptr;
+}
+
+void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParams& p,
+                       cudaStream_t s) {
+  const uint64_t nc = L.nc, nt = L.nt;
+  if (S.patch_done) ETB_CUDA(cudaEventSynchronize(S.patch_done));
+  uint32_t* ph = S.h_patch.get();
+  uint32_t np = 0;
+  p.skip_lo = p.skip_hi = 0;
+  p.start = kNone32;
+  p.base_depth = 0;
+  p.start_parent = kNone32;
+  if (S.last_isolated != kNone32 && S.last_isolated != start) {
+    ph[3 * np] = S.last_isolated;
+    ph[3 * np + 1] = 0xFFFFFFFFu;
+    ph[3 * np + 2] = kNone32;
+    ++np;
+  }
+  S.last_isolated = kNone32;
+  if (start < nc) {
+    p.start = static_cast<uint32_t>(start);
+    p.start_parent = static_cast<uint32_t>(start);
+  } else if (start < nc + nt) {
+    // Start-side walk over the start's tree (et_bfs.cpp:34-57): the tree is a
+    // contiguous id range; parents always precede children.
+    const uint32_t* src = L.h_tsrc.data();
+    const uint32_t* dep = L.h_tdepth.data();
+    uint32_t r = static_cast<uint32_t>(start);
+    for (;;) {
+      const uint32_t sp = src[r - nc];
+      if (sp == r || sp < nc) break;
+      r = sp;
+    }
+    const auto it = std::upper_bound(L.h_tree_start.begin(), L.h_tree_start.end(), r);
+    const uint32_t lo = r;
+    const uint32_t hi = it == L.h_tree_start.end() ? static_cast<uint32_t>(nc + nt) : *it;
+    const uint32_t sz = hi - lo;
+    static thread_local std::vector<uint32_t> dist, par;
+    static thread_local std::vector<uint8_t> anc;
+    dist.assign(sz, 0);
+    par.assign(sz, kNone32);
+    anc.assign(sz, 0);
+    const uint32_t s0 = static_cast<uint32_t>(start);
+    anc[s0 - lo] = 1;
+    par[s0 - lo] = s0;
+    for (uint32_t x = s0, prevx = s0; x != r;) {
+      const uint32_t up = src[x - nc];
+      anc[up - lo] = 1;
+      par[up - lo] = x;
+      prevx = x;
+      x = up;
+      (void)prevx;
+    }
+    const uint32_t ds = dep[s0 - nc];
+    for (uint32_t x = lo; x < hi; ++x) {
+      const uint32_t i = x - lo;
+      if (anc[i]) {
+        dist[i] = ds - dep[x - nc];
+      } else {
+        const uint32_t up = src[x - nc];
+        dist[i] = dist[up - lo] + 1;
+        par[i] = up;
+      }
+      ph[3 * np] = x;
+      ph[3 * np + 1] = dist[i];
+      ph[3 * np + 2] = par[i];
+      ++np;
+    }
+    p.skip_lo = lo;
+    p.skip_hi = hi;
+    const uint32_t ce = src[r - nc];
+    if (ce != r) {  // attached tree: continue from its core-edge vertex
+      p.start = ce;
+      p.base_depth = static_cast<int32_t>(ds);
+      p.start_parent = r;
+    }
+  } else {
+    ph[3 * np] = static_cast<uint32_t>(start);
+    ph[3 * np + 1] = 0;
+    ph[3 * np + 2] = static_cast<uint32_t>(start);
+    ++np;
+    S.last_isolated = static_cast<uint32_t>(start);
+  }
+  p.npatch = np;
+  if (np) {
+    ETB_CUDA(cudaMemcpyAsync(S.patch.get(), ph, np * 12, cudaMemcpyHostToDevice, s));
+    ETB_CUDA(cudaEventRecord(S.patch_done, s));
+  }
+}
+
+void bfs_launch(const BfsParams& p, const BfsState& S, cudaStream_t s) {
+  void* args[] = {const_cast<BfsParams*>(&p)};
+  ETB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(et_bfs_kernel), dim3(S.grid),
+                                       dim3(S.block), args, 0, s));
+}
+
+}  // namespace etb

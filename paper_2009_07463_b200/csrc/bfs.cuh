@@ -1,0 +1,82 @@
+// Persistent ET-BFS kernel interface (bfs.cu).
+#pragma once
+
+#include "internal.cuh"
+
+namespace etb {
+
+// Chunk of a core row one warp expands in a top-down step.
+constexpr uint32_t kTdChunk = 256;
+
+struct BfsParams {
+  // core graph (relaid ids)
+  const uint64_t* crow;
+  const uint32_t* ccol;
+  const uint32_t* cfirst;
+  const uint32_t* degn;  // full degree (scout, bfs.cpp:80)
+  uint32_t nc;
+  uint32_t nwords;       // ceil(nc / 32)
+  // edge trees
+  const uint32_t* tsrc;
+  const uint32_t* tanchor;
+  const uint32_t* tdepth;
+  uint32_t nt;
+  // traversal state
+  uint32_t* visited;
+  uint32_t* fb0;
+  uint32_t* fb1;
+  uint32_t* fb2;
+  uint64_t* items0;
+  uint64_t* items1;
+  unsigned long long* ctr;  // 4 level slots x 4 + conversion counters
+  unsigned long long* bar;  // grid barrier counter (monotonic)
+  // outputs (relaid ids, all n vertices)
+  int32_t* depth;
+  uint32_t* parent;
+  // per call
+  uint32_t start;         // core vertex the core BFS starts at, kNone32 for none
+  int32_t base_depth;     // depth of `start`
+  uint32_t start_parent;  // parent of `start`
+  uint32_t skip_lo, skip_hi;  // tree range filled by the start-side walk
+  const uint32_t* patch;  // (vertex, depth, parent) triples
+  uint32_t npatch;
+  double alpha, beta, edges_to_check;
+  int top_down_only;
+  // stats (may be null)
+  char* trace;
+  unsigned long long* level_claims;
+  uint32_t* nlevels;
+};
+
+struct BfsState {
+  uint64_t n = 0;
+  DevBuf<uint32_t> visited, fb0, fb1, fb2;
+  DevBuf<uint64_t> items0, items1;
+  DevBuf<unsigned long long> ctr, bar;
+  DevBuf<int32_t> depth;
+  DevBuf<uint32_t> parent;
+  DevBuf<char> trace;
+  DevBuf<unsigned long long> level_claims;
+  DevBuf<uint32_t> nlevels;
+  DevBuf<uint32_t> patch;
+  HostBuf<uint32_t> h_patch;
+  cudaEvent_t patch_done = nullptr;  // the pinned patch may be rewritten after this
+  ~BfsState() {
+    if (patch_done) cudaEventDestroy(patch_done);
+  }
+  uint32_t last_isolated = kNone32;  // isolated start to reset on the next call
+  int grid = 0, block = 0;
+  bool has_result = false;
+  uint64_t last_start = ~uint64_t{0};
+};
+
+void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s);
+void bfs_launch(const BfsParams& p, const BfsState& S, cudaStream_t s);
+// Fills depth/parent of the start's tree on the host (traverse_return_core_edge,
+// et_bfs.cpp:34-57) and returns the core vertex to start from (kNone32 if the
+// start's component is a pure tree or the start is isolated).
+void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParams& p,
+                       cudaStream_t s);
+void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p);
+
+}  // namespace etb

@@ -1,0 +1,524 @@
+// The extern "C" boundary (include/etbfs_cuda.h). Every entry point converts
+// exceptions into status codes: std::invalid_argument -> ETB_EINVAL (the
+// reference's caller errors, same messages), std::runtime_error ->
+// ETB_ERUNTIME, CUDA failures -> ETB_ECUDA.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <unistd.h>
+
+#include "bfs.cuh"
+
+struct etb_graph {
+  etb::DevGraph g;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ~etb_graph() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+struct etb_layout {
+  etb::DevLayout L;
+  etb::BfsState S;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  etb::DevBuf<uint8_t> flush;
+  ~etb_layout() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ETB_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return ETB_EINVAL;
+  } catch (const etb::CudaError& e) {
+    g_err = e.what();
+    return ETB_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return ETB_ERUNTIME;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return ETB_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ETB_ERUNTIME;
+  } catch (...) {
+    g_err = "unknown error";
+    return ETB_ERUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string(what) + ": null argument");
+}
+
+cudaStream_t new_stream() {
+  cudaStream_t s;
+  ETB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+int current_device() {
+  int d = 0;
+  ETB_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+uint64_t physical_memory_bytes() {
+  const long pages = sysconf(_SC_PHYS_PAGES), page = sysconf(_SC_PAGE_SIZE);
+  if (pages <= 0 || page <= 0) return ~uint64_t{0};
+  return uint64_t(pages) * uint64_t(page);
+}
+
+void widen(const uint32_t* in, uint64_t n, uint64_t* out) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = in[i] == etb::kNone32 ? ETB_NO_VERTEX : in[i];
+}
+
+template <typename T>
+std::vector<T> download(const T* d, uint64_t n, cudaStream_t s) {
+  std::vector<T> h(n);
+  if (n) ETB_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  ETB_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+void finish_layout(etb_layout* h) {
+  etb::bfs_state_init(h->L, h->S, h->stream);
+  for (auto& e : h->ev) ETB_CUDA(cudaEventCreate(&e));
+}
+
+etb::BfsParams run_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* o,
+                       bool want_stats, cudaEvent_t pre_launch = nullptr) {
+  const etb::DevLayout& L = h->L;
+  if (start >= L.n) throw std::invalid_argument("et_bfs: start out of range");
+  etb_bfs_options opt{ETB_KERNEL_HYBRID, ETB_REPLAY_TEET, 14.0, 24.0};
+  if (o) opt = *o;
+  if (opt.replay == ETB_REPLAY_TEOLV && L.mh != 0)
+    throw std::invalid_argument("et_bfs: leaves-only replay needs a height-0 classification");
+  if (opt.replay != ETB_REPLAY_TEET && opt.replay != ETB_REPLAY_TEOLV)
+    throw std::invalid_argument("et_bfs: unknown tree replay");
+  if (opt.kernel != ETB_KERNEL_HYBRID && opt.kernel != ETB_KERNEL_TOP_DOWN)
+    throw std::invalid_argument("et_bfs: kernel needs a degree split");
+  etb::BfsParams p{};
+  etb::bfs_fill_params(L, h->S, p);
+  etb::bfs_prepare_start(L, h->S, start, p, h->stream);
+  if (p.start != etb::kNone32 && opt.kernel == ETB_KERNEL_HYBRID &&
+      (!(opt.alpha > 0.0) || !(opt.beta > 0.0)))
+    throw std::invalid_argument("run_hybrid: alpha and beta must be positive");
+  p.alpha = opt.alpha;
+  p.beta = opt.beta;
+  p.top_down_only = opt.kernel == ETB_KERNEL_TOP_DOWN;
+  if (want_stats) {
+    p.trace = h->S.trace.get();
+    p.level_claims = h->S.level_claims.get();
+    p.nlevels = h->S.nlevels.get();
+    ETB_CUDA(cudaMemsetAsync(p.trace, 0, 256, h->stream));
+  }
+  if (pre_launch) ETB_CUDA(cudaEventRecord(pre_launch, h->stream));
+  etb::bfs_launch(p, h->S, h->stream);
+  h->S.has_result = true;
+  h->S.last_start = start;
+  return p;
+}
+
+void collect_stats(etb_layout* h, etb_bfs_stats* st) {
+  uint32_t nl = 0;
+  std::memset(st, 0, sizeof(*st));
+  ETB_CUDA(cudaMemcpyAsync(&nl, h->S.nlevels.get(), 4, cudaMemcpyDeviceToHost, h->stream));
+  ETB_CUDA(cudaMemcpyAsync(st->direction_trace, h->S.trace.get(), 255, cudaMemcpyDeviceToHost,
+                           h->stream));
+  ETB_CUDA(cudaMemcpyAsync(st->level_claims, h->S.level_claims.get(), 256 * 8,
+                           cudaMemcpyDeviceToHost, h->stream));
+  ETB_CUDA(cudaStreamSynchronize(h->stream));
+  st->levels = nl;
+  st->direction_trace[std::min<uint32_t>(nl, 255)] = 0;
+  for (uint32_t i = 0; i < nl && i < 255; ++i) st->bottom_up_levels += st->direction_trace[i] == 'b';
+}
+
+__global__ void te_kernel(const int32_t* depth, const uint32_t* degn, uint64_t n,
+                          unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (depth[i] >= 0) acc += degn[i];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+__global__ void widen_kernel(const uint32_t* in, uint64_t n, uint64_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] == etb::kNone32 ? ~0ull : in[i];
+}
+
+void download_widened(const uint32_t* d, uint64_t n, uint64_t* host, cudaStream_t s) {
+  if (!n) return;
+  etb::DevBuf<uint64_t> tmp(n);
+  widen_kernel<<<etb::grid_for(n, 256), 256, 0, s>>>(d, n, tmp.get());
+  ETB_LAUNCH_CHECK();
+  ETB_CUDA(cudaMemcpyAsync(host, tmp.get(), n * 8, cudaMemcpyDeviceToHost, s));
+  ETB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* etb_last_error(void) { return g_err.c_str(); }
+
+int etb_version(void) { return 1; }
+
+int etb_device_count(int* count) {
+  return guarded([&] {
+    need(count, "etb_device_count");
+    ETB_CUDA(cudaGetDeviceCount(count));
+  });
+}
+
+int etb_set_device(int device) { return guarded([&] { ETB_CUDA(cudaSetDevice(device)); }); }
+
+int etb_generate_kronecker(const etb_kron_params* p, uint64_t* out_pairs) {
+  return guarded([&] {
+    need(p, "generate_kronecker");
+    etb::kron_validate(*p);
+    const uint64_t n = uint64_t{1} << p->scale;
+    const uint64_t t = n * p->edgefactor;
+    if (t > physical_memory_bytes() / 16)
+      throw std::runtime_error("generate_kronecker: edge list would exceed physical memory");
+    need(out_pairs, "generate_kronecker");
+    cudaStream_t s = new_stream();
+    std::unique_ptr<CUstream_st, decltype(&cudaStreamDestroy)> guard(s, cudaStreamDestroy);
+    const uint64_t chunk = std::min<uint64_t>(t, uint64_t{1} << 25);
+    etb::DevBuf<uint64_t> buf(2 * (chunk ? chunk : 1));
+    for (uint64_t first = 0; first < t; first += chunk) {
+      const uint64_t c = std::min(chunk, t - first);
+      etb::kron_generate_pairs64(*p, first, c, buf.get(), s);
+      ETB_CUDA(cudaMemcpyAsync(out_pairs + 2 * first, buf.get(), c * 16, cudaMemcpyDeviceToHost,
+                               s));
+      ETB_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int etb_graph_from_edges(uint64_t n, const uint64_t* pairs, uint64_t count, etb_graph** out,
+                         uint64_t* self_loops, uint64_t* dups) {
+  return guarded([&] {
+    need(out, "build_csr");
+    *out = nullptr;
+    if (n > (uint64_t{1} << 48))
+      throw std::invalid_argument("build_csr: vertex count exceeds 2^48");
+    if (count) need(pairs, "build_csr");
+    for (uint64_t i = 0; i < count; ++i)  // build.cpp:26-31, same message
+      if (pairs[2 * i] >= n || pairs[2 * i + 1] >= n)
+        throw std::invalid_argument("build_csr: endpoint out of range at edge index " +
+                                    std::to_string(i));
+    auto h = std::make_unique<etb_graph>();
+    h->device = current_device();
+    h->stream = new_stream();
+    etb::build_csr_from_host_pairs(n, pairs, count, h->g, self_loops, dups, h->stream);
+    *out = h.release();
+  });
+}
+
+int etb_graph_generate(const etb_kron_params* p, etb_graph** out, uint64_t* self_loops,
+                       uint64_t* dups) {
+  return guarded([&] {
+    need(p, "generate_kronecker");
+    need(out, "generate_kronecker");
+    *out = nullptr;
+    auto h = std::make_unique<etb_graph>();
+    h->device = current_device();
+    h->stream = new_stream();
+    etb::build_csr_from_generator(*p, h->g, self_loops, dups, h->stream);
+    *out = h.release();
+  });
+}
+
+int etb_graph_info(const etb_graph* g, uint64_t* n, uint64_t* nnz) {
+  return guarded([&] {
+    need(g, "etb_graph_info");
+    if (n) *n = g->g.n;
+    if (nnz) *nnz = g->g.nnz;
+  });
+}
+
+int etb_graph_download(const etb_graph* g, uint64_t* row, uint64_t* cols, uint64_t* degrees) {
+  return guarded([&] {
+    need(g, "etb_graph_download");
+    ETB_CUDA(cudaSetDevice(g->device));
+    const auto& G = g->g;
+    if (row && G.n + 1)
+      ETB_CUDA(cudaMemcpyAsync(row, G.row.get(), (G.n + 1) * 8, cudaMemcpyDeviceToHost, g->stream));
+    if (cols) download_widened(G.col.get(), G.nnz, cols, g->stream);
+    if (degrees && G.n) {
+      auto d = download(G.deg.get(), G.n, g->stream);
+      for (uint64_t i = 0; i < G.n; ++i) degrees[i] = d[i];
+    }
+    ETB_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+void etb_graph_free(etb_graph* g) { delete g; }
+
+int etb_classify(const etb_graph* g, int64_t mh, uint8_t* types_out, uint64_t* counts_out) {
+  return guarded([&] {
+    need(g, "classify_vertices");
+    ETB_CUDA(cudaSetDevice(g->device));
+    etb::DevBuf<uint8_t> type;
+    uint64_t counts[5];
+    etb::classify_device(g->g, mh, type, counts, nullptr, g->stream);
+    if (types_out && g->g.n)
+      ETB_CUDA(cudaMemcpyAsync(types_out, type.get(), g->g.n, cudaMemcpyDeviceToHost, g->stream));
+    ETB_CUDA(cudaStreamSynchronize(g->stream));
+    if (counts_out) std::memcpy(counts_out, counts, sizeof counts);
+  });
+}
+
+int etb_peak_height(const etb_graph* g, uint64_t* ph) {
+  return guarded([&] {
+    need(g, "compute_peak_height");
+    need(ph, "compute_peak_height");
+    ETB_CUDA(cudaSetDevice(g->device));
+    etb::DevBuf<uint8_t> type;
+    uint64_t counts[5];
+    etb::classify_device(g->g, -1, type, counts, ph, g->stream);
+  });
+}
+
+int etb_layout_build(const etb_graph* g, int64_t mh, etb_layout** out) {
+  return guarded([&] {
+    need(g, "relayout_csr");
+    need(out, "relayout_csr");
+    *out = nullptr;
+    ETB_CUDA(cudaSetDevice(g->device));
+    auto h = std::make_unique<etb_layout>();
+    h->device = g->device;
+    h->stream = new_stream();
+    {
+      etb::DevBuf<uint8_t> type;
+      uint64_t counts[5];
+      etb::classify_device(g->g, mh, type, counts, nullptr, h->stream);
+      etb::build_layout(g->g, type.get(), mh, h->L, h->stream);
+    }
+    finish_layout(h.get());
+    *out = h.release();
+  });
+}
+
+int etb_layout_build_types(const etb_graph* g, const uint8_t* types, int64_t mh,
+                           etb_layout** out) {
+  return guarded([&] {
+    need(g, "relayout_csr");
+    need(out, "relayout_csr");
+    *out = nullptr;
+    if (g->g.n) need(types, "relayout_csr");
+    for (uint64_t i = 0; i < g->g.n; ++i)
+      if (types[i] > ETB_VZ) throw std::invalid_argument("relayout_csr: bad vertex type");
+    ETB_CUDA(cudaSetDevice(g->device));
+    auto h = std::make_unique<etb_layout>();
+    h->device = g->device;
+    h->stream = new_stream();
+    {
+      etb::DevBuf<uint8_t> type(g->g.n ? g->g.n : 1);
+      if (g->g.n)
+        ETB_CUDA(cudaMemcpyAsync(type.get(), types, g->g.n, cudaMemcpyHostToDevice, h->stream));
+      etb::build_layout(g->g, type.get(), mh, h->L, h->stream);
+    }
+    finish_layout(h.get());
+    *out = h.release();
+  });
+}
+
+int etb_layout_info_get(const etb_layout* h, etb_layout_info* info) {
+  return guarded([&] {
+    need(h, "etb_layout_info");
+    need(info, "etb_layout_info");
+    const auto& L = h->L;
+    info->vertex_count = L.n;
+    info->core_vertex_count = L.nc;
+    info->tree_vertex_count = L.nt;
+    info->isolated_count = L.nz;
+    info->core_directed_edges = L.ecore;
+    info->directed_edges = L.nnz_full;
+    info->tree_count = L.tree_count;
+    info->max_tree_size = L.max_tree;
+    info->mh = L.mh;
+  });
+}
+
+int etb_layout_download_maps(const etb_layout* h, uint64_t* new2old, uint64_t* old2new,
+                             uint8_t* types) {
+  return guarded([&] {
+    need(h, "etb_layout_download_maps");
+    ETB_CUDA(cudaSetDevice(h->device));
+    const auto& L = h->L;
+    if (new2old) widen(download(L.new2old.get(), L.n, h->stream).data(), L.n, new2old);
+    if (old2new) widen(download(L.old2new.get(), L.n, h->stream).data(), L.n, old2new);
+    if (types && L.n) {
+      ETB_CUDA(cudaMemcpyAsync(types, L.type.get(), L.n, cudaMemcpyDeviceToHost, h->stream));
+      ETB_CUDA(cudaStreamSynchronize(h->stream));
+    }
+  });
+}
+
+int etb_layout_download_graph(const etb_layout* h, uint64_t* row, uint64_t* cols) {
+  return guarded([&] {
+    need(h, "etb_layout_download_graph");
+    ETB_CUDA(cudaSetDevice(h->device));
+    etb::DevBuf<uint64_t> r;
+    etb::DevBuf<uint32_t> c;
+    etb::build_full_relabelled(h->L, r, c, h->stream);
+    if (row)
+      ETB_CUDA(cudaMemcpyAsync(row, r.get(), (h->L.n + 1) * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (cols) download_widened(c.get(), h->L.nnz_full, cols, h->stream);
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int etb_layout_download_etl(const etb_layout* h, uint64_t* src, uint64_t* dst, uint64_t* ce) {
+  return guarded([&] {
+    need(h, "extract_edge_tree_list");
+    const auto& L = h->L;
+    for (uint64_t i = 0; i < L.nt; ++i) {
+      if (src) src[i] = L.h_tsrc[i];
+      if (dst) dst[i] = L.nc + i;
+      if (ce) ce[i] = L.h_tanchor[i] == etb::kNone32 ? ETB_NO_VERTEX : L.h_tanchor[i];
+    }
+  });
+}
+
+int etb_layout_restricted_edges(const etb_layout* h, uint64_t* count) {
+  return guarded([&] {
+    need(h, "restricted_edge_count");
+    need(count, "restricted_edge_count");
+    *count = h->L.ecore;
+  });
+}
+
+void etb_layout_free(etb_layout* h) { delete h; }
+
+int etb_bfs_device(etb_layout* h, uint64_t start, const etb_bfs_options* opts,
+                   etb_bfs_stats* stats) {
+  return guarded([&] {
+    need(h, "et_bfs");
+    ETB_CUDA(cudaSetDevice(h->device));
+    run_bfs(h, start, opts, stats != nullptr);
+    if (stats) collect_stats(h, stats);
+  });
+}
+
+int etb_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* opts, int32_t* depth_out,
+            uint64_t* parent_out, etb_bfs_stats* stats) {
+  return guarded([&] {
+    need(h, "et_bfs");
+    ETB_CUDA(cudaSetDevice(h->device));
+    run_bfs(h, start, opts, stats != nullptr);
+    const uint64_t n = h->L.n;
+    if (depth_out && n)
+      ETB_CUDA(cudaMemcpyAsync(depth_out, h->S.depth.get(), n * 4, cudaMemcpyDeviceToHost,
+                               h->stream));
+    if (parent_out) download_widened(h->S.parent.get(), n, parent_out, h->stream);
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
+    if (stats) collect_stats(h, stats);
+  });
+}
+
+int etb_result_device_ptrs(etb_layout* h, int32_t** depth, uint32_t** parent) {
+  return guarded([&] {
+    need(h, "etb_result_device_ptrs");
+    if (depth) *depth = h->S.depth.get();
+    if (parent) *parent = h->S.parent.get();
+  });
+}
+
+int etb_result_download(etb_layout* h, int32_t* depth, uint32_t* parent) {
+  return guarded([&] {
+    need(h, "etb_result_download");
+    ETB_CUDA(cudaSetDevice(h->device));
+    const uint64_t n = h->L.n;
+    if (depth && n)
+      ETB_CUDA(cudaMemcpyAsync(depth, h->S.depth.get(), n * 4, cudaMemcpyDeviceToHost, h->stream));
+    if (parent && n)
+      ETB_CUDA(cudaMemcpyAsync(parent, h->S.parent.get(), n * 4, cudaMemcpyDeviceToHost,
+                               h->stream));
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int etb_result_traversed_edges(etb_layout* h, uint64_t* te) {
+  return guarded([&] {
+    need(h, "etb_result_traversed_edges");
+    need(te, "etb_result_traversed_edges");
+    ETB_CUDA(cudaSetDevice(h->device));
+    etb::DevBuf<unsigned long long> acc(1);
+    ETB_CUDA(cudaMemsetAsync(acc.get(), 0, 8, h->stream));
+    te_kernel<<<etb::grid_for(h->L.n, 256), 256, 0, h->stream>>>(h->S.depth.get(), h->L.degn.get(),
+                                                                  h->L.n, acc.get());
+    ETB_LAUNCH_CHECK();
+    *te = etb::read_u64(reinterpret_cast<uint64_t*>(acc.get()), h->stream) / 2;
+  });
+}
+
+int etb_host_register(void* ptr, uint64_t bytes) {
+  return guarded([&] {
+    need(ptr, "etb_host_register");
+    ETB_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  });
+}
+
+int etb_host_unregister(void* ptr) {
+  return guarded([&] {
+    need(ptr, "etb_host_unregister");
+    ETB_CUDA(cudaHostUnregister(ptr));
+  });
+}
+
+int etb_time_roots(etb_layout* h, const uint64_t* starts, uint64_t count, int warmup,
+                   int flush_l2, const etb_bfs_options* opts, double* ms_out,
+                   double* kernel_ms_out) {
+  return guarded([&] {
+    need(h, "etb_time_roots");
+    if (count) need(starts, "etb_time_roots");
+    ETB_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    if (flush_l2 && !h->flush) {
+      int l2 = 0;
+      ETB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device));
+      h->flush.alloc(std::max<uint64_t>(uint64_t(l2) * 2, uint64_t{1} << 26));
+    }
+    for (int w = 0; w < warmup && count; ++w) run_bfs(h, starts[w % count], opts, false);
+    ETB_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < count; ++i) {
+      if (flush_l2) ETB_CUDA(cudaMemsetAsync(h->flush.get(), i & 0xFF, h->flush.size(), s));
+      ETB_CUDA(cudaStreamSynchronize(s));
+      ETB_CUDA(cudaEventRecord(h->ev[0], s));
+      run_bfs(h, starts[i], opts, false, h->ev[2]);
+      ETB_CUDA(cudaEventRecord(h->ev[1], s));
+      ETB_CUDA(cudaEventSynchronize(h->ev[1]));
+      float ms = 0.f, kms = 0.f;
+      ETB_CUDA(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+      ETB_CUDA(cudaEventElapsedTime(&kms, h->ev[2], h->ev[1]));
+      if (ms_out) ms_out[i] = ms;
+      if (kernel_ms_out) kernel_ms_out[i] = kms;
+    }
+  });
+}
+
+}  // extern "C"

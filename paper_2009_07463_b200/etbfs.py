@@ -1,0 +1,442 @@
+"""ctypes mirror of the reference ``etbfs`` API over the C-ABI (include/etbfs_cuda.h).
+
+Reference interfaces mirrored (paths under /root/reference/proj/include/etbfs):
+  generate_kronecker      kronecker.hpp:34        -> generate_kronecker()
+  build_csr               build.hpp:19            -> build_csr()
+  classify_vertices       classify.hpp:33         -> classify_vertices()
+  compute_peak_height     classify.hpp:38         -> compute_peak_height()
+  count_types             classify.hpp:40         -> count_types()
+  relayout_csr            relayout.hpp:40         -> relayout_csr()
+  extract_edge_tree_list  relayout.hpp:52         -> extract_edge_tree_list()
+  et_bfs                  et_bfs.hpp:53           -> et_bfs()
+  restricted_edge_count   bfs.hpp:123             -> EtLayout.restricted_edge_count
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(HERE, "lib", "libetbfs_b200.so")
+
+NO_VERTEX = np.uint64(0xFFFFFFFFFFFFFFFF)  # types.hpp:13 kNoVertex
+
+ETB_OK, ETB_EINVAL, ETB_ERUNTIME, ETB_ECUDA, ETB_ENOTSUP = 0, -1, -2, -3, -4
+
+
+class VertexType(enum.IntEnum):  # types.hpp:55-61
+    CORE_INTERNAL = 0
+    CORE_EDGE = 1
+    TREE_INTERNAL = 2
+    TREE_LEAF = 3
+    VERTEX_ZERO = 4
+
+
+class CoreKernel(enum.IntEnum):  # et_bfs.hpp:10-16 (kDegreeAware / kBlockSearch not built yet)
+    TOP_DOWN = 0
+    HYBRID = 1
+
+
+class TreeReplay(enum.IntEnum):  # et_bfs.hpp:19-22
+    TEET = 0
+    TEOLV = 1
+
+
+@dataclass
+class HybridPolicy:  # bfs.hpp:19-22
+    alpha: float = 14.0
+    beta: float = 24.0
+
+
+@dataclass
+class KroneckerParams:  # kronecker.hpp:12-20
+    scale: int = 0
+    edgefactor: int = 16
+    a: float = 0.57
+    b: float = 0.19
+    c: float = 0.19
+    d: float = 0.05
+    seed: int = 0
+
+
+@dataclass
+class TypeCounts:  # classify.hpp:12-27
+    core_internal: int = 0
+    core_edge: int = 0
+    tree_internal: int = 0
+    tree_leaf: int = 0
+    vertex_zero: int = 0
+
+    def total(self):
+        return self.core_internal + self.core_edge + self.tree_internal + self.tree_leaf + \
+            self.vertex_zero
+
+    def core(self):
+        return self.core_internal + self.core_edge
+
+    def tree(self):
+        return self.tree_internal + self.tree_leaf
+
+
+# ------------------------------------------------------------------ ctypes --
+class _Kron(C.Structure):
+    _fields_ = [("scale", C.c_uint32), ("edgefactor", C.c_uint64), ("a", C.c_double),
+                ("b", C.c_double), ("c", C.c_double), ("d", C.c_double), ("seed", C.c_uint64)]
+
+
+class _LayoutInfo(C.Structure):
+    _fields_ = [("vertex_count", C.c_uint64), ("core_vertex_count", C.c_uint64),
+                ("tree_vertex_count", C.c_uint64), ("isolated_count", C.c_uint64),
+                ("core_directed_edges", C.c_uint64), ("directed_edges", C.c_uint64),
+                ("tree_count", C.c_uint64), ("max_tree_size", C.c_uint64), ("mh", C.c_int64)]
+
+
+class _BfsOptions(C.Structure):
+    _fields_ = [("kernel", C.c_int), ("replay", C.c_int), ("alpha", C.c_double),
+                ("beta", C.c_double)]
+
+
+class _BfsStats(C.Structure):
+    _fields_ = [("levels", C.c_uint32), ("bottom_up_levels", C.c_uint32),
+                ("direction_trace", C.c_char * 256), ("level_claims", C.c_uint64 * 256)]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib() -> C.CDLL:
+    """Load the sm_100a library; fails loudly (no fallback) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(f"{_LIB_PATH} is not built; run __graft_entry__.build() "
+                           "(python paper_2009_07463_b200/build_lib.py)")
+    L = C.CDLL(_LIB_PATH)
+    vp, u64, i64, i32 = C.c_void_p, C.c_uint64, C.c_int64, C.c_int
+    P64 = C.POINTER(C.c_uint64)
+
+    def sig(name, *args):
+        f = getattr(L, name)
+        f.restype = i32
+        f.argtypes = list(args)
+
+    L.etb_last_error.restype = C.c_char_p
+    L.etb_last_error.argtypes = []
+    sig("etb_version")
+    sig("etb_device_count", C.POINTER(C.c_int))
+    sig("etb_set_device", C.c_int)
+    sig("etb_generate_kronecker", C.POINTER(_Kron), vp)
+    sig("etb_graph_from_edges", u64, vp, u64, C.POINTER(vp), P64, P64)
+    sig("etb_graph_generate", C.POINTER(_Kron), C.POINTER(vp), P64, P64)
+    sig("etb_graph_info", vp, P64, P64)
+    sig("etb_graph_download", vp, vp, vp, vp)
+    L.etb_graph_free.restype = None
+    L.etb_graph_free.argtypes = [vp]
+    sig("etb_classify", vp, i64, vp, vp)
+    sig("etb_peak_height", vp, P64)
+    sig("etb_layout_build", vp, i64, C.POINTER(vp))
+    sig("etb_layout_build_types", vp, vp, i64, C.POINTER(vp))
+    sig("etb_layout_info_get", vp, C.POINTER(_LayoutInfo))
+    sig("etb_layout_download_maps", vp, vp, vp, vp)
+    sig("etb_layout_download_graph", vp, vp, vp)
+    sig("etb_layout_download_etl", vp, vp, vp, vp)
+    sig("etb_layout_restricted_edges", vp, P64)
+    L.etb_layout_free.restype = None
+    L.etb_layout_free.argtypes = [vp]
+    sig("etb_bfs_device", vp, u64, C.POINTER(_BfsOptions), C.POINTER(_BfsStats))
+    sig("etb_bfs", vp, u64, C.POINTER(_BfsOptions), vp, vp, C.POINTER(_BfsStats))
+    sig("etb_result_device_ptrs", vp, C.POINTER(vp), C.POINTER(vp))
+    sig("etb_result_download", vp, vp, vp)
+    sig("etb_result_traversed_edges", vp, P64)
+    sig("etb_host_register", vp, u64)
+    sig("etb_host_unregister", vp)
+    sig("etb_time_roots", vp, vp, u64, C.c_int, C.c_int, C.POINTER(_BfsOptions), vp, vp)
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc == ETB_OK:
+        return
+    msg = lib().etb_last_error().decode()
+    if rc == ETB_EINVAL:
+        raise ValueError(msg)
+    if rc == ETB_ENOTSUP:
+        raise NotImplementedError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _kron(p: KroneckerParams) -> _Kron:
+    return _Kron(p.scale, p.edgefactor, p.a, p.b, p.c, p.d, p.seed)
+
+
+def _opts(kernel, replay, policy) -> _BfsOptions:
+    pol = policy or HybridPolicy()
+    return _BfsOptions(int(kernel), int(replay), float(pol.alpha), float(pol.beta))
+
+
+# ------------------------------------------------------------------- graph --
+def generate_kronecker(params: KroneckerParams | None = None, **kw) -> np.ndarray:
+    """generate_kronecker (kronecker.hpp:34) on the GPU: (T, 2) u64 (src, dst)."""
+    p = params or KroneckerParams(**kw)
+    t = (1 << p.scale) * p.edgefactor if p.scale <= 48 else 0
+    out = np.empty((max(t, 1), 2), np.uint64)
+    _check(lib().etb_generate_kronecker(C.byref(_kron(p)), _ptr(out)))
+    return out[:t]
+
+
+class Csr:
+    """A CsrGraph (types.hpp:38-50) resident in HBM (original ids)."""
+
+    def __init__(self, handle, n, nnz, self_loops=0, duplicates=0):
+        self._h = handle
+        self.vertex_count = n
+        self.directed_edge_count = nnz
+        self.dropped_self_loops = self_loops
+        self.dropped_duplicates = duplicates
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.etb_graph_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def undirected_edge_count(self):
+        return self.directed_edge_count // 2
+
+    def degrees(self):
+        """degrees u64[n] (types.hpp:43) without downloading the adjacency."""
+        deg = np.empty(max(self.vertex_count, 1), np.uint64)
+        _check(lib().etb_graph_download(self._h, None, None, _ptr(deg)))
+        return deg[: self.vertex_count]
+
+    def download(self):
+        """(row_offsets u64[n+1], col_indices u64[nnz], degrees u64[n])."""
+        n, m = self.vertex_count, self.directed_edge_count
+        row = np.empty(n + 1, np.uint64)
+        col = np.empty(max(m, 1), np.uint64)
+        deg = np.empty(max(n, 1), np.uint64)
+        _check(lib().etb_graph_download(self._h, _ptr(row), _ptr(col), _ptr(deg)))
+        return row, col[:m], deg[:n]
+
+
+def _finish_csr(h, sl, du) -> Csr:
+    n, m = C.c_uint64(), C.c_uint64()
+    _check(lib().etb_graph_info(h, C.byref(n), C.byref(m)))
+    return Csr(h, n.value, m.value, sl.value, du.value)
+
+
+def build_csr(vertex_count: int, pairs: np.ndarray) -> Csr:
+    """build_csr (build.hpp:19): symmetric, deduplicated, self-loop free, on the GPU."""
+    pairs = np.ascontiguousarray(pairs, dtype=np.uint64).reshape(-1, 2)
+    h = C.c_void_p()
+    sl, du = C.c_uint64(), C.c_uint64()
+    _check(lib().etb_graph_from_edges(int(vertex_count), _ptr(pairs), pairs.shape[0],
+                                      C.byref(h), C.byref(sl), C.byref(du)))
+    return _finish_csr(h, sl, du)
+
+
+def generate_graph(params: KroneckerParams | None = None, **kw) -> Csr:
+    """generate_kronecker + build_csr fused on the device (tuples never leave HBM)."""
+    p = params or KroneckerParams(**kw)
+    h = C.c_void_p()
+    sl, du = C.c_uint64(), C.c_uint64()
+    _check(lib().etb_graph_generate(C.byref(_kron(p)), C.byref(h), C.byref(sl), C.byref(du)))
+    return _finish_csr(h, sl, du)
+
+
+# ------------------------------------------------------------ preprocessing --
+def classify_vertices(g: Csr, mh: int) -> np.ndarray:
+    """classify_vertices (classify.hpp:33): u8 VertexType per original id."""
+    t = np.empty(max(g.vertex_count, 1), np.uint8)
+    _check(lib().etb_classify(g.handle, int(mh), _ptr(t), None))
+    return t[: g.vertex_count]
+
+
+def compute_peak_height(g: Csr) -> int:
+    """compute_peak_height (classify.hpp:38), exact Gauss-Seidel emulation."""
+    ph = C.c_uint64()
+    _check(lib().etb_peak_height(g.handle, C.byref(ph)))
+    return ph.value
+
+
+def count_types(types) -> TypeCounts:
+    """count_types (classify.hpp:40)."""
+    c = np.bincount(np.asarray(types, np.uint8), minlength=5)
+    return TypeCounts(*[int(x) for x in c[:5]])
+
+
+class EtLayout:
+    """A ClassifiedGraph (types.hpp:69-76) + its EdgeTreeList, BFS-ready in HBM."""
+
+    def __init__(self, handle):
+        self._h = handle
+        info = _LayoutInfo()
+        _check(lib().etb_layout_info_get(handle, C.byref(info)))
+        self.vertex_count = info.vertex_count
+        self.core_vertex_count = info.core_vertex_count
+        self.tree_vertex_count = info.tree_vertex_count
+        self.isolated_count = info.isolated_count
+        self.restricted_edge_count = info.core_directed_edges
+        self.directed_edge_count = info.directed_edges
+        self.tree_count = info.tree_count
+        self.max_tree_size = info.max_tree_size
+        self.mh = info.mh
+        self._maps = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.etb_layout_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _load_maps(self):
+        if self._maps is None:
+            n = self.vertex_count
+            a = np.empty(max(n, 1), np.uint64)
+            b = np.empty(max(n, 1), np.uint64)
+            t = np.empty(max(n, 1), np.uint8)
+            _check(lib().etb_layout_download_maps(self._h, _ptr(a), _ptr(b), _ptr(t)))
+            self._maps = (a[:n], b[:n], t[:n])
+        return self._maps
+
+    @property
+    def new2old(self):
+        return self._load_maps()[0]
+
+    @property
+    def old2new(self):
+        return self._load_maps()[1]
+
+    @property
+    def vertex_type(self):
+        return self._load_maps()[2]
+
+    def graph(self):
+        """The relabelled CsrGraph: (row_offsets, col_indices) u64."""
+        n, m = self.vertex_count, self.directed_edge_count
+        row = np.empty(n + 1, np.uint64)
+        col = np.empty(max(m, 1), np.uint64)
+        _check(lib().etb_layout_download_graph(self._h, _ptr(row), _ptr(col)))
+        return row, col[:m]
+
+
+def relayout_csr(g: Csr, types=None, mh: int = -1) -> EtLayout:
+    """relayout_csr (relayout.hpp:40). types=None classifies on the device first."""
+    h = C.c_void_p()
+    if types is None:
+        _check(lib().etb_layout_build(g.handle, int(mh), C.byref(h)))
+    else:
+        t = np.ascontiguousarray(types, np.uint8)
+        if t.size != g.vertex_count:
+            raise ValueError("relayout_csr: types length does not match vertex count")
+        _check(lib().etb_layout_build_types(g.handle, _ptr(t), int(mh), C.byref(h)))
+    return EtLayout(h)
+
+
+def extract_edge_tree_list(cg: EtLayout):
+    """extract_edge_tree_list (relayout.hpp:52): (src, dst, core_edge) u64 arrays."""
+    m = cg.tree_vertex_count
+    s, d, c = (np.empty(max(m, 1), np.uint64) for _ in range(3))
+    _check(lib().etb_layout_download_etl(cg.handle, _ptr(s), _ptr(d), _ptr(c)))
+    return s[:m], d[:m], c[:m]
+
+
+# ---------------------------------------------------------------- traversal --
+@dataclass
+class BfsStats:  # bfs.hpp:27-33 KernelStats
+    levels: int = 0
+    bottom_up_levels: int = 0
+    direction_trace: str = ""
+    level_claims: list = field(default_factory=list)
+
+
+@dataclass
+class BfsResult:  # types.hpp:96-99 BfsTree (+ the device's exact depth array)
+    root: int
+    parent: np.ndarray   # u64, relaid ids, NO_VERTEX unreached
+    depth: np.ndarray    # i32, -1 unreached
+    stats: BfsStats | None = None
+
+
+def et_bfs(cg: EtLayout, start: int, kernel=CoreKernel.HYBRID, replay=TreeReplay.TEET,
+           policy: HybridPolicy | None = None, stats: bool = False,
+           want_parent: bool = True, want_depth: bool = True) -> BfsResult:
+    """et_bfs (et_bfs.hpp:53) on the GPU; results in relaid ids."""
+    n = cg.vertex_count
+    depth = np.empty(max(n, 1), np.int32) if want_depth else None
+    parent = np.empty(max(n, 1), np.uint64) if want_parent else None
+    st = _BfsStats() if stats else None
+    o = _opts(kernel, replay, policy)
+    _check(lib().etb_bfs(cg.handle, int(start), C.byref(o), _ptr(depth), _ptr(parent),
+                         C.byref(st) if st is not None else None))
+    bs = None
+    if st is not None:
+        bs = BfsStats(st.levels, st.bottom_up_levels, st.direction_trace.decode(),
+                      list(st.level_claims[: st.levels]))
+    return BfsResult(int(start), parent[:n] if parent is not None else None,
+                     depth[:n] if depth is not None else None, bs)
+
+
+def bfs_device(cg: EtLayout, start: int, kernel=CoreKernel.HYBRID, replay=TreeReplay.TEET,
+               policy: HybridPolicy | None = None) -> None:
+    """et_bfs leaving depth/parent in HBM (the timed hot path)."""
+    o = _opts(kernel, replay, policy)
+    _check(lib().etb_bfs_device(cg.handle, int(start), C.byref(o), None))
+
+
+def result_download(cg: EtLayout, depth: np.ndarray | None = None,
+                    parent: np.ndarray | None = None):
+    """Last result as compact i32 depth / u32 parent (UINT32_MAX unreached)."""
+    n = cg.vertex_count
+    if depth is None:
+        depth = np.empty(max(n, 1), np.int32)
+    if parent is None:
+        parent = np.empty(max(n, 1), np.uint32)
+    _check(lib().etb_result_download(cg.handle, _ptr(depth), _ptr(parent)))
+    return depth[:n], parent[:n]
+
+
+def result_traversed_edges(cg: EtLayout) -> int:
+    te = C.c_uint64()
+    _check(lib().etb_result_traversed_edges(cg.handle, C.byref(te)))
+    return te.value
+
+
+def time_roots(cg: EtLayout, starts, warmup=3, flush_l2=True, kernel=CoreKernel.HYBRID,
+               replay=TreeReplay.TEET, policy: HybridPolicy | None = None):
+    """Per-root CUDA-event times (ms): (whole call incl. start-side walk, kernel only)."""
+    s = np.ascontiguousarray(starts, np.uint64)
+    ms = np.empty(max(s.size, 1), np.float64)
+    kms = np.empty(max(s.size, 1), np.float64)
+    o = _opts(kernel, replay, policy)
+    _check(lib().etb_time_roots(cg.handle, _ptr(s), s.size, int(warmup), int(bool(flush_l2)),
+                                C.byref(o), _ptr(ms), _ptr(kms)))
+    return ms[: s.size], kms[: s.size]
+
+
+def device_count() -> int:
+    c = C.c_int()
+    _check(lib().etb_device_count(C.byref(c)))
+    return c.value
