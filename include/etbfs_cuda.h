@@ -100,6 +100,10 @@ int etb_graph_from_edges(uint64_t vertex_count, const uint64_t* pairs, uint64_t 
                          uint64_t* dropped_duplicates);
 int etb_graph_generate(const etb_kron_params* p, etb_graph** out, uint64_t* dropped_self_loops,
                        uint64_t* dropped_duplicates);
+/* Upload an existing CsrGraph (row_offsets n+1 u64, cols u64; rows must be sorted,
+ * symmetric and duplicate free, as every CsrGraph the reference produces). */
+int etb_graph_from_csr(uint64_t vertex_count, const uint64_t* row_offsets, const uint64_t* cols,
+                       etb_graph** out);
 int etb_graph_info(const etb_graph* g, uint64_t* vertex_count, uint64_t* directed_edges);
 /* Any output may be NULL. row_offsets: n+1 u64, cols: directed_edges u64, degrees: n u64. */
 int etb_graph_download(const etb_graph* g, uint64_t* row_offsets, uint64_t* cols,

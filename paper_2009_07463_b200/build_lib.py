@@ -17,13 +17,17 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "lib", "libetbfs_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
 
 
 def sources():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+    cu = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+    host = os.path.join(CSRC, "host")
+    cpp = sorted(os.path.join(host, f) for f in os.listdir(host) if f.endswith(".cpp"))
+    return cu + cpp
 
 
 def headers():
@@ -37,8 +41,13 @@ def _compile(src: str, verbose: bool) -> str:
     dep_mtime = max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in headers()])
     if os.path.exists(obj) and os.path.getmtime(obj) >= dep_mtime:
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
-    if verbose:
+    if src.endswith(".cpp"):
+        # The C++ drop-in (reference signatures, C++20 std::span) is host-only code.
+        cmd = [CXX, "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra",
+               "-I" + os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+    else:
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    if verbose and not src.endswith(".cpp"):
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -65,3 +74,21 @@ def build(verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
+
+
+def build_cpp_tests() -> str:
+    """tests/cpp/test_dropin: the C++ drop-in API test binary (links the library)."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    out = os.path.join(ROOT, "tests", "cpp", "bin", "test_dropin")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    deps = [src, LIB] + [os.path.join(ROOT, "include", "etbfs", f)
+                         for f in os.listdir(os.path.join(ROOT, "include", "etbfs"))]
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
+        return out
+    cmd = [CXX, "-std=c++20", "-O2", "-Wall", "-I" + os.path.join(ROOT, "include"), src, "-o", out,
+           "-L" + os.path.dirname(LIB), "-letbfs_b200",
+           "-Wl,-rpath,$ORIGIN/../../../paper_2009_07463_b200/lib"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"test_dropin build failed:\n{r.stderr}")
+    return out

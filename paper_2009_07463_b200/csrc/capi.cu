@@ -251,6 +251,44 @@ int etb_graph_generate(const etb_kron_params* p, etb_graph** out, uint64_t* self
   });
 }
 
+int etb_graph_from_csr(uint64_t n, const uint64_t* row, const uint64_t* cols, etb_graph** out) {
+  return guarded([&] {
+    need(out, "etb_graph_from_csr");
+    need(row, "etb_graph_from_csr");
+    *out = nullptr;
+    if (n > etb::kMaxDeviceVertices)
+      throw std::invalid_argument("etb_graph_from_csr: vertex count exceeds the device id range");
+    const uint64_t nnz = row[n];
+    if (nnz) need(cols, "etb_graph_from_csr");
+    std::vector<uint32_t> c32(nnz);
+    for (uint64_t i = 0; i < nnz; ++i) {
+      if (cols[i] >= n) throw std::invalid_argument("etb_graph_from_csr: column out of range");
+      c32[i] = static_cast<uint32_t>(cols[i]);
+    }
+    std::vector<uint32_t> deg(n);
+    for (uint64_t v = 0; v < n; ++v) {
+      if (row[v + 1] < row[v]) throw std::invalid_argument("etb_graph_from_csr: bad row offsets");
+      deg[v] = static_cast<uint32_t>(row[v + 1] - row[v]);
+    }
+    auto h = std::make_unique<etb_graph>();
+    h->device = current_device();
+    h->stream = new_stream();
+    auto& G = h->g;
+    G.n = n;
+    G.nnz = nnz;
+    G.row.alloc(n + 1);
+    G.col.alloc(nnz ? nnz : 1);
+    G.deg.alloc(n ? n : 1);
+    ETB_CUDA(cudaMemcpyAsync(G.row.get(), row, (n + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+    if (nnz)
+      ETB_CUDA(cudaMemcpyAsync(G.col.get(), c32.data(), nnz * 4, cudaMemcpyHostToDevice, h->stream));
+    if (n)
+      ETB_CUDA(cudaMemcpyAsync(G.deg.get(), deg.data(), n * 4, cudaMemcpyHostToDevice, h->stream));
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
+    *out = h.release();
+  });
+}
+
 int etb_graph_info(const etb_graph* g, uint64_t* n, uint64_t* nnz) {
   return guarded([&] {
     need(g, "etb_graph_info");

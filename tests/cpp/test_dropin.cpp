@@ -1,0 +1,353 @@
+// C++ drop-in test: the reference's public API (include/etbfs/*.hpp) driven
+// exactly as the reference's own unit tests drive it (proj/tests/*.cpp KATs,
+// restated), with an independent host BFS as the level oracle. Every call
+// goes through the C-ABI to the sm_100a kernels. Exit status = failures.
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <deque>
+#include <functional>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "etbfs/bfs.hpp"
+#include "etbfs/build.hpp"
+#include "etbfs/classify.hpp"
+#include "etbfs/et_bfs.hpp"
+#include "etbfs/kronecker.hpp"
+#include "etbfs/relayout.hpp"
+
+using namespace etbfs;
+
+static int g_fail = 0, g_checks = 0;
+static std::string g_case;
+#define EXPECT(cond)                                                                  \
+  do {                                                                                \
+    ++g_checks;                                                                       \
+    if (!(cond)) {                                                                    \
+      ++g_fail;                                                                       \
+      std::fprintf(stderr, "FAIL [%s] %s:%d: %s\n", g_case.c_str(), __FILE__, __LINE__, #cond); \
+    }                                                                                 \
+  } while (0)
+template <typename E, typename F>
+bool throws_with(F&& f, const char* needle) {
+  try {
+    f();
+  } catch (const E& e) {
+    return needle == nullptr || std::string(e.what()).find(needle) != std::string::npos;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+namespace {
+
+using Types = std::vector<VertexType>;
+constexpr auto CI = VertexType::kCoreInternal;
+constexpr auto CE = VertexType::kCoreEdge;
+constexpr auto TI = VertexType::kTreeInternal;
+constexpr auto TL = VertexType::kTreeLeaf;
+constexpr auto VZ = VertexType::kVertexZero;
+
+EdgeList edges(uint64_t n, std::vector<std::pair<vertex_t, vertex_t>> p) {
+  EdgeList e;
+  e.vertex_count = n;
+  for (auto [a, b] : p) e.edges.push_back({a, b});
+  return e;
+}
+EdgeList path(uint64_t n) {
+  EdgeList e;
+  e.vertex_count = n;
+  for (vertex_t v = 0; v + 1 < n; ++v) e.edges.push_back({v, v + 1});
+  return e;
+}
+EdgeList cycle(uint64_t n) {
+  EdgeList e = path(n);
+  if (n >= 3) e.edges.push_back({n - 1, 0});
+  return e;
+}
+EdgeList star(uint64_t n) {
+  EdgeList e;
+  e.vertex_count = n;
+  for (vertex_t v = 1; v < n; ++v) e.edges.push_back({0, v});
+  return e;
+}
+EdgeList clique(uint64_t n) {
+  EdgeList e;
+  e.vertex_count = n;
+  for (vertex_t u = 0; u < n; ++u)
+    for (vertex_t v = u + 1; v < n; ++v) e.edges.push_back({u, v});
+  return e;
+}
+EdgeList binary_tree(uint64_t n) {
+  EdgeList e;
+  e.vertex_count = n;
+  for (vertex_t v = 1; v < n; ++v) e.edges.push_back({(v - 1) / 2, v});
+  return e;
+}
+// Deterministic raw tuples (self loops and duplicates left in).
+EdgeList random_tuples(uint64_t n, uint64_t m, uint64_t seed) {
+  EdgeList e;
+  e.vertex_count = n;
+  uint64_t s = seed * 0x9E3779B97F4A7C15ull + 1;
+  auto next = [&] {
+    s ^= s << 13;
+    s ^= s >> 7;
+    s ^= s << 17;
+    return s;
+  };
+  for (uint64_t i = 0; i < m; ++i) e.edges.push_back({next() % n, next() % n});
+  return e;
+}
+
+// Independent level oracle: adjacency sets + deque BFS (not the library's CSR).
+std::vector<uint64_t> host_levels(const EdgeList& el, vertex_t root) {
+  std::vector<std::set<vertex_t>> adj(el.vertex_count);
+  for (const Edge& e : el.edges)
+    if (e.src != e.dst) adj[e.src].insert(e.dst), adj[e.dst].insert(e.src);
+  std::vector<uint64_t> lv(el.vertex_count, kUnreached);
+  std::deque<vertex_t> q{root};
+  lv[root] = 0;
+  while (!q.empty()) {
+    vertex_t u = q.front();
+    q.pop_front();
+    for (vertex_t w : adj[u])
+      if (lv[w] == kUnreached) lv[w] = lv[u] + 1, q.push_back(w);
+  }
+  return lv;
+}
+
+// Levels implied by a parent tree, by fixpoint (shares nothing with the library).
+std::vector<uint64_t> tree_levels(const BfsTree& t) {
+  const uint64_t n = t.parent.size();
+  std::vector<uint64_t> lv(n, kUnreached);
+  if (t.root >= n || t.parent[t.root] != t.root) return {};
+  lv[t.root] = 0;
+  for (uint64_t sweep = 0; sweep <= n; ++sweep) {
+    bool changed = false;
+    for (vertex_t v = 0; v < n; ++v) {
+      if (v == t.root || t.parent[v] == kNoVertex || t.parent[v] >= n) continue;
+      const uint64_t pl = lv[t.parent[v]];
+      if (pl != kUnreached && lv[v] != pl + 1) lv[v] = pl + 1, changed = true;
+    }
+    if (!changed) break;
+  }
+  return lv;
+}
+
+EdgeList relabeled(const ClassifiedGraph& cg) {
+  EdgeList e;
+  e.vertex_count = cg.graph.vertex_count;
+  for (vertex_t v = 0; v < cg.graph.vertex_count; ++v)
+    for (vertex_t w : cg.graph.neighbors(v))
+      if (v < w) e.edges.push_back({v, w});
+  return e;
+}
+
+void check_tree_exact(const EdgeList& el, const BfsTree& t, vertex_t root) {
+  EXPECT(t.root == root);
+  const auto want = host_levels(el, root);
+  EXPECT(tree_levels(t) == want);
+  std::vector<std::set<vertex_t>> adj(el.vertex_count);
+  for (const Edge& e : el.edges)
+    if (e.src != e.dst) adj[e.src].insert(e.dst), adj[e.dst].insert(e.src);
+  for (vertex_t v = 0; v < el.vertex_count; ++v)
+    if (v != root && t.parent[v] != kNoVertex) EXPECT(adj[v].count(t.parent[v]) == 1);
+}
+
+std::vector<EdgeList> corpus() {
+  std::vector<EdgeList> c = {path(1), path(2), path(9), cycle(8), star(17), clique(6),
+                             binary_tree(31), edges(6, {}), edges(7, {{0, 1}, {2, 3}, {3, 4}})};
+  for (uint64_t s = 1; s <= 10; ++s) c.push_back(random_tuples(20 + s * 13, 30 + s * 40, s));
+  return c;
+}
+
+void run_case(const char* name, const std::function<void()>& f) {
+  g_case = name;
+  const int before = g_fail;
+  try {
+    f();
+  } catch (const std::exception& e) {
+    ++g_fail;
+    std::fprintf(stderr, "FAIL [%s] unexpected exception: %s\n", name, e.what());
+  }
+  std::printf("%s %s\n", g_fail == before ? "PASS" : "FAIL", name);
+}
+
+}  // namespace
+
+int main() {
+  run_case("build_csr KAT (test_graph_core.cpp:17-36)", [] {
+    BuildStats st;
+    const CsrGraph g = build_csr(
+        edges(5, {{0, 1}, {1, 0}, {0, 1}, {2, 2}, {3, 1}, {1, 3}, {4, 0}, {0, 4}, {0, 4}}), &st);
+    EXPECT(g.vertex_count == 5);
+    EXPECT(g.undirected_edge_count() == 3);
+    EXPECT(st.dropped_self_loops == 1);
+    EXPECT(st.dropped_duplicates == 5);
+    EXPECT(std::vector<vertex_t>(g.neighbors(0).begin(), g.neighbors(0).end()) ==
+           (std::vector<vertex_t>{1, 4}));
+    EXPECT(g.degrees[2] == 0);
+    EXPECT(throws_with<std::invalid_argument>([] { build_csr(edges(3, {{0, 1}, {1, 3}})); },
+                                              "endpoint out of range at edge index 1"));
+  });
+
+  run_case("generate_kronecker determinism and validation", [] {
+    KroneckerParams p;
+    p.scale = 10;
+    p.seed = 7;
+    const EdgeList a = generate_kronecker(p), b = generate_kronecker(p);
+    EXPECT(a.edges.size() == (1u << 10) * 16u && a.edges == b.edges && a.vertex_count == 1024);
+    for (const Edge& e : a.edges) EXPECT(e.src < 1024 && e.dst < 1024);
+    p.scale = 49;
+    EXPECT(throws_with<std::invalid_argument>([&] { generate_kronecker(p); }, "scale > 48"));
+    p.scale = 4;
+    p.a = 0.6;
+    EXPECT(throws_with<std::invalid_argument>([&] { generate_kronecker(p); }, "sum to 1"));
+  });
+
+  run_case("classification KATs (test_classify.cpp:80-138)", [] {
+    const CsrGraph p3 = build_csr(path(3));
+    EXPECT(classify_vertices(p3, -1) == (Types{TL, TI, TL}));
+    EXPECT(classify_vertices(p3, 0) == (Types{TL, CE, TL}));
+    EXPECT(compute_peak_height(p3) == 1);
+    const CsrGraph p5 = build_csr(path(5));
+    EXPECT(classify_vertices(p5, -1) == (Types{TL, TI, TI, TI, TL}));
+    EXPECT(compute_peak_height(p5) == 2);
+    EXPECT(classify_vertices(p5, 1) == (Types{TL, TI, TI, CE, TL}));
+    EXPECT(classify_vertices(p5, 0) == (Types{TL, CE, CI, CE, TL}));
+    const CsrGraph p7 = build_csr(path(7));
+    EXPECT(compute_peak_height(p7) == 2);
+    EXPECT(classify_vertices(p7, 1) == (Types{TL, TI, TI, TI, TI, CE, TL}));
+    const CsrGraph s5 = build_csr(star(5));
+    EXPECT(classify_vertices(s5, -1) == (Types{TI, TL, TL, TL, TL}));
+    EXPECT(classify_vertices(s5, 0) == (Types{CE, TL, TL, TL, TL}));
+    const CsrGraph tri =
+        build_csr(edges(6, {{0, 1}, {1, 2}, {0, 2}, {2, 3}, {3, 4}, {3, 5}}));
+    EXPECT(classify_vertices(tri, -1) == (Types{CI, CI, CE, TI, TL, TL}));
+    EXPECT(classify_vertices(tri, 0) == (Types{CI, CI, CI, CE, TL, TL}));
+    EXPECT(compute_peak_height(build_csr(cycle(6))) == 0);
+    EXPECT(classify_vertices(build_csr(clique(5)), -1) == Types(5, CI));
+    const CsrGraph pair = build_csr(edges(4, {{0, 1}}));
+    EXPECT(classify_vertices(pair, -1) == (Types{TL, TL, VZ, VZ}));
+    EXPECT(compute_peak_height(pair) == 0);
+    EXPECT(throws_with<std::invalid_argument>([&] { classify_vertices(p3, -2); }, nullptr));
+    const TypeCounts c = count_types({CI, CE, CE, TI, TL, TL, TL, VZ});
+    EXPECT(c.core() == 3 && c.tree() == 4 && c.total() == 8);
+  });
+
+  run_case("relayout frozen layouts (test_relayout.cpp:110-158)", [] {
+    const CsrGraph g = build_csr(edges(6, {{0, 1}, {1, 2}, {0, 2}, {2, 3}, {3, 4}, {3, 5}}));
+    const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, -1), -1);
+    EXPECT(cg.core_vertex_count == 3);
+    EXPECT(cg.new2old == (std::vector<vertex_t>{2, 0, 1, 3, 4, 5}));
+    EXPECT(cg.vertex_type[0] == CE && cg.vertex_type[3] == TI);
+    const EdgeTreeList etl = extract_edge_tree_list(cg);
+    EXPECT(etl.entries == (std::vector<EdgeTreeEntry>{{0, 3, 0}, {3, 4, 0}, {3, 5, 0}}));
+    const CsrGraph s = build_csr(star(5));
+    const ClassifiedGraph sc = relayout_csr(s, classify_vertices(s, -1), -1);
+    EXPECT(sc.core_vertex_count == 0 && sc.new2old == (std::vector<vertex_t>{0, 1, 2, 3, 4}));
+    const EdgeTreeList se = extract_edge_tree_list(sc);
+    EXPECT(se.entries.size() == 5 && se.entries[0] == (EdgeTreeEntry{0, 0, kNoVertex}));
+    const CsrGraph pr = build_csr(edges(4, {{0, 1}}));
+    const ClassifiedGraph pc = relayout_csr(pr, classify_vertices(pr, 0), 0);
+    EXPECT(extract_edge_tree_list(pc).entries ==
+           (std::vector<EdgeTreeEntry>{{0, 0, kNoVertex}, {0, 1, kNoVertex}}));
+    EXPECT(throws_with<std::invalid_argument>(
+        [&] { relayout_csr(g, Types(2, CI), -1); }, "types length does not match"));
+  });
+
+  run_case("composite traversal is level-exact across the corpus (test_et_bfs.cpp:158-169)", [] {
+    for (const EdgeList& el : corpus()) {
+      const CsrGraph g = build_csr(el);
+      for (std::int64_t mh : {std::int64_t{-1}, std::int64_t{0}, std::int64_t{1}}) {
+        const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, mh), mh);
+        const EdgeTreeList etl = extract_edge_tree_list(cg);
+        const EdgeList rel = relabeled(cg);
+        for (vertex_t s = 0; s < g.vertex_count; ++s) {
+          for (CoreKernel k : {CoreKernel::kTopDown, CoreKernel::kHybrid})
+            check_tree_exact(rel, et_bfs(cg, etl, s, k), s);
+          if (mh == 0)
+            check_tree_exact(rel, et_bfs(cg, etl, s, CoreKernel::kHybrid, TreeReplay::kTeolv), s);
+        }
+      }
+    }
+  });
+
+  run_case("composite config errors (test_et_bfs.cpp:181-195)", [] {
+    const CsrGraph g = build_csr(path(8));
+    const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, -1), -1);
+    const EdgeTreeList etl = extract_edge_tree_list(cg);
+    EXPECT(throws_with<std::invalid_argument>([&] { et_bfs(cg, etl, 99); }, "out of range"));
+    EXPECT(throws_with<std::invalid_argument>(
+        [&] { et_bfs(cg, etl, 0, CoreKernel::kHybrid, TreeReplay::kTeolv); }, "height-0"));
+    EXPECT(throws_with<std::invalid_argument>(
+        [&] { et_bfs(cg, etl, 0, CoreKernel::kDegreeAware); }, "degree split"));
+  });
+
+  run_case("isolated start yields the one-vertex tree (test_et_bfs.cpp:171-179)", [] {
+    const CsrGraph g = build_csr(edges(5, {{0, 1}, {1, 2}}));
+    const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, -1), -1);
+    const EdgeTreeList etl = extract_edge_tree_list(cg);
+    EXPECT(cg.vertex_type[4] == VZ);
+    const BfsTree t = et_bfs(cg, etl, 4);
+    EXPECT(t.parent[4] == 4);
+    for (vertex_t v = 0; v < 4; ++v) EXPECT(t.parent[v] == kNoVertex);
+  });
+
+  run_case("hybrid policy KATs (test_bfs_kernels.cpp:185-218)", [] {
+    HybridPolicy tiny;
+    tiny.alpha = 1e-9;
+    KernelStats st;
+    const BfsTree t = bfs_hybrid(build_csr(path(4)), 0, tiny, &st);
+    check_tree_exact(path(4), t, 0);
+    EXPECT(st.levels == 4 && st.bottom_up_levels == 0 && st.direction_trace == "tttt");
+    HybridPolicy huge;
+    huge.alpha = 1e18;
+    KernelStats st2;
+    check_tree_exact(path(6), bfs_hybrid(build_csr(path(6)), 0, huge, &st2), 0);
+    EXPECT(!st2.direction_trace.empty() && st2.direction_trace[0] == 'b');
+    EXPECT(st2.bottom_up_levels == st2.levels);
+    KernelStats st3;
+    check_tree_exact(star(300), bfs_hybrid(build_csr(star(300)), 5, {}, &st3), 5);
+    EXPECT(st3.bottom_up_levels > 0 && st3.bottom_up_levels < st3.levels);
+    HybridPolicy zero;
+    zero.alpha = 0.0;
+    EXPECT(throws_with<std::invalid_argument>(
+        [&] { bfs_hybrid(build_csr(path(4)), 0, zero); }, "alpha and beta"));
+    EXPECT(throws_with<std::invalid_argument>([&] { bfs_top_down(build_csr(path(4)), 4); },
+                                              "out of range"));
+    KernelStats one;
+    EXPECT(bfs_hybrid(build_csr(path(1)), 0, {}, &one).parent == std::vector<vertex_t>{0});
+    EXPECT(one.levels == 1);
+    const CsrGraph g = build_csr(edges(5, {{0, 1}, {0, 2}, {1, 2}, {2, 3}, {3, 4}, {0, 4}}));
+    EXPECT(restricted_edge_count(g, 0) == 0 && restricted_edge_count(g, 3) == 6);
+  });
+
+  run_case("Kronecker s14 end to end vs host BFS on the original ids", [] {
+    KroneckerParams p;
+    p.scale = 14;
+    p.seed = 1;
+    const EdgeList el = generate_kronecker(p);
+    const CsrGraph g = build_csr(el);
+    for (std::int64_t mh : {std::int64_t{-1}, std::int64_t{0}}) {
+      const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, mh), mh);
+      const EdgeTreeList etl = extract_edge_tree_list(cg);
+      for (vertex_t r : {vertex_t{0}, vertex_t{1}, vertex_t{777}, vertex_t{4095}, vertex_t{12345}}) {
+        const BfsTree t = et_bfs(cg, etl, cg.old2new[r]);
+        BfsTree lifted;
+        lifted.root = r;
+        lifted.parent.assign(g.vertex_count, kNoVertex);
+        for (vertex_t v = 0; v < g.vertex_count; ++v)
+          if (t.parent[v] != kNoVertex) lifted.parent[cg.new2old[v]] = cg.new2old[t.parent[v]];
+        check_tree_exact(el, lifted, r);
+      }
+    }
+  });
+
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
