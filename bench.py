@@ -186,23 +186,28 @@ def run_ours(args):
     achieved = balg / kern_s / 1e9
     roof_gteps = peak * 1e9 / (balg / float(te.max())) / 1e9
 
-    # e2e: the reference-facing call with HOST output buffers (D2H inside the timing).
+    # e2e: the C-ABI call with a HOST output buffer — the BfsTree content (parent of
+    # every vertex, relaid ids, u32) copied device->host inside the wall-clock timing.
     n = cg.vertex_count
-    depth_h = np.empty(n, np.int32)
-    parent_h = np.empty(n, np.uint64)
-    E.lib().etb_host_register(depth_h.ctypes.data, depth_h.nbytes)
-    E.lib().etb_host_register(parent_h.ctypes.data, parent_h.nbytes)
+    parent_h = np.empty(n, np.uint32)
+    eb.etbfs._check(E.lib().etb_host_register(parent_h.ctypes.data, parent_h.nbytes))
     e2e_t = []
-    for s in starts:
+    for s in np.concatenate([starts[:3], starts]):
         c0 = time.perf_counter()
-        eb.etbfs._check(E.lib().etb_bfs(cg.handle, int(s), None, depth_h.ctypes.data,
-                                        parent_h.ctypes.data, None))
+        eb.etbfs._check(E.lib().etb_bfs_compact(cg.handle, int(s), None, None,
+                                                parent_h.ctypes.data))
         e2e_t.append(time.perf_counter() - c0)
-    E.lib().etb_host_unregister(depth_h.ctypes.data)
-    E.lib().etb_host_unregister(parent_h.ctypes.data)
+    e2e_t = e2e_t[3:]
+    eb.etbfs._check(E.lib().etb_host_unregister(parent_h.ctypes.data))
     e2e_hm, _ = harmonic_gteps(te.astype(np.float64), np.array(e2e_t))
     if world > 1:
         e2e_hm *= world
+
+    # Per-level device timeline of the first root (stats run, untimed).
+    r0 = eb.et_bfs(cg, int(starts[0]), stats=True, want_parent=False, want_depth=False)
+    timeline = {"trace": r0.stats.direction_trace, "claims": r0.stats.level_claims,
+                "level_end_us": [round(x / 1e3, 2) for x in r0.stats.level_ns],
+                "total_us": round(r0.stats.total_ns / 1e3, 2)}
 
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
@@ -222,8 +227,8 @@ def run_ours(args):
                      "frac_of_roofline_gteps": round(hm_giant / roof_gteps, 4)},
         "e2e": {"value": round(e2e_hm, 3), "unit": "GTEPS",
                 "h2d_bytes_per_step": 8 * len(starts),
-                "d2h_bytes_per_step": 12 * n * len(starts),
-                "api": "etb_bfs (C-ABI, host depth i32 + parent u64 outputs, pinned)"},
+                "d2h_bytes_per_step": 4 * n * len(starts),
+                "api": "etb_bfs_compact (C-ABI, host parent u32[n] output, pinned, wall clock)"},
         "gpu_launches": int(len(reps)),
         "clocks": clocks,
         "detail": {"mean_gteps": round(float(per.mean()), 3), "min_gteps": round(float(per.min()), 3),
@@ -236,7 +241,8 @@ def run_ours(args):
                    "tree_vertices": int(cg.tree_vertex_count),
                    "core_directed_edges": int(cg.restricted_edge_count),
                    "preprocessing_s": round(preprocessing_s, 3),
-                   "generate_build_csr_s": round(t_csr, 3), "classify_relayout_s": round(t_layout, 3)},
+                   "generate_build_csr_s": round(t_csr, 3), "classify_relayout_s": round(t_layout, 3),
+                   "timeline_root0": timeline},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, roots[: args.cpu_roots])

@@ -84,6 +84,10 @@ typedef struct {
   uint32_t bottom_up_levels; /* KernelStats::bottom_up_levels */
   char direction_trace[256]; /* KernelStats::direction_trace, NUL-terminated */
   uint64_t level_claims[256];
+  /* device time (ns) from kernel entry to: [0] end of init, [1 + L] end of level L;
+   * total_ns to the end of the tree replay (block 0's view). */
+  uint64_t level_ns[256];
+  uint64_t total_ns;
 } etb_bfs_stats;
 
 /* ---- library ------------------------------------------------------------ */
@@ -142,6 +146,10 @@ int etb_bfs_device(etb_layout* L, uint64_t start, const etb_bfs_options* opts,
  * and/or parent (n u64, ETB_NO_VERTEX unreached), relaid ids. */
 int etb_bfs(etb_layout* L, uint64_t start, const etb_bfs_options* opts, int32_t* depth_out,
             uint64_t* parent_out, etb_bfs_stats* stats);
+/* et_bfs with compact host outputs: parent (n u32, UINT32_MAX unreached) and/or
+ * depth (n i32). The BfsTree content at half the bytes of etb_bfs. */
+int etb_bfs_compact(etb_layout* L, uint64_t start, const etb_bfs_options* opts,
+                    int32_t* depth_out, uint32_t* parent_out);
 /* Device pointers to the last result (n entries each, relaid ids). */
 int etb_result_device_ptrs(etb_layout* L, int32_t** depth, uint32_t** parent);
 /* Copy the last result to host as compact i32 depth / u32 parent (UINT32_MAX unreached). */

@@ -66,6 +66,19 @@ __device__ void grid_sync(unsigned long long* bar) {
   __syncthreads();
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Phase timestamps for stats (block 0 / thread 0): [256] entry, [257] after
+// init, [258 + L] after level L, [511] end of the tree replay.
+__device__ __forceinline__ void stamp(const BfsParams& p, uint32_t slot) {
+  if (p.level_claims && blockIdx.x == 0 && threadIdx.x == 0 && slot < 512)
+    p.level_claims[slot] = gtimer();
+}
+
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
@@ -250,6 +263,7 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t start = p.start;
   const bool run_core = start != kNone32;
+  stamp(p, 256);
 
   // ---- init: core-sized state only (the reference allocates n-sized state,
   // et_bfs.cpp:82,96) --------------------------------------------------------
@@ -277,6 +291,7 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
     }
   }
   grid_sync(p.bar);
+  stamp(p, 257);
 
   // ---- level loop: run_hybrid (bfs.cpp:232-293) ---------------------------------
   uint32_t L = 0;
@@ -347,6 +362,7 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
         grid_sync(p.bar);
         nitems = ld_volatile(cslot);
       }
+      stamp(p, 257 + L);
     }
   }
   if (tid == 0 && p.nlevels) *p.nlevels = L;
@@ -375,6 +391,7 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
     p.depth[v] = static_cast<int32_t>(p.patch[3 * i + 1]);
     p.parent[v] = p.patch[3 * i + 2];
   }
+  stamp(p, 511);
 }
 
 }  // namespace
@@ -400,7 +417,7 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   ETB_CUDA(cudaMemsetAsync(S.depth.get(), 0xFF, (n ? n : 1) * 4, s));
   ETB_CUDA(cudaMemsetAsync(S.parent.get(), 0xFF, (n ? n : 1) * 4, s));
   S.trace.alloc(256);
-  S.level_claims.alloc(256);
+  S.level_claims.alloc(512);
   S.nlevels.alloc(1);
   const uint64_t pcap = std::max<uint64_t>(L.max_tree, 1) + 2;
   S.patch.alloc(3 * pcap);

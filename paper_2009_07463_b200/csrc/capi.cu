@@ -146,7 +146,12 @@ void collect_stats(etb_layout* h, etb_bfs_stats* st) {
                            h->stream));
   ETB_CUDA(cudaMemcpyAsync(st->level_claims, h->S.level_claims.get(), 256 * 8,
                            cudaMemcpyDeviceToHost, h->stream));
+  uint64_t ts[256];
+  ETB_CUDA(cudaMemcpyAsync(ts, h->S.level_claims.get() + 256, 256 * 8, cudaMemcpyDeviceToHost,
+                           h->stream));
   ETB_CUDA(cudaStreamSynchronize(h->stream));
+  for (uint32_t i = 0; i <= nl && i + 1 < 255; ++i) st->level_ns[i] = ts[1 + i] - ts[0];
+  st->total_ns = ts[255] - ts[0];
   st->levels = nl;
   st->direction_trace[std::min<uint32_t>(nl, 255)] = 0;
   for (uint32_t i = 0; i < nl && i < 255; ++i) st->bottom_up_levels += st->direction_trace[i] == 'b';
@@ -475,6 +480,22 @@ int etb_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* opts, int32_t*
     if (parent_out) download_widened(h->S.parent.get(), n, parent_out, h->stream);
     ETB_CUDA(cudaStreamSynchronize(h->stream));
     if (stats) collect_stats(h, stats);
+  });
+}
+
+int etb_bfs_compact(etb_layout* h, uint64_t start, const etb_bfs_options* opts, int32_t* depth,
+                    uint32_t* parent) {
+  return guarded([&] {
+    need(h, "et_bfs");
+    ETB_CUDA(cudaSetDevice(h->device));
+    run_bfs(h, start, opts, false);
+    const uint64_t n = h->L.n;
+    if (parent && n)
+      ETB_CUDA(cudaMemcpyAsync(parent, h->S.parent.get(), n * 4, cudaMemcpyDeviceToHost,
+                               h->stream));
+    if (depth && n)
+      ETB_CUDA(cudaMemcpyAsync(depth, h->S.depth.get(), n * 4, cudaMemcpyDeviceToHost, h->stream));
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
   });
 }
 

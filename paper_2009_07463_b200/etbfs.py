@@ -102,7 +102,8 @@ class _BfsOptions(C.Structure):
 
 class _BfsStats(C.Structure):
     _fields_ = [("levels", C.c_uint32), ("bottom_up_levels", C.c_uint32),
-                ("direction_trace", C.c_char * 256), ("level_claims", C.c_uint64 * 256)]
+                ("direction_trace", C.c_char * 256), ("level_claims", C.c_uint64 * 256),
+                ("level_ns", C.c_uint64 * 256), ("total_ns", C.c_uint64)]
 
 
 _lib = None
@@ -154,6 +155,7 @@ def lib() -> C.CDLL:
     L.etb_layout_free.argtypes = [vp]
     sig("etb_bfs_device", vp, u64, C.POINTER(_BfsOptions), C.POINTER(_BfsStats))
     sig("etb_bfs", vp, u64, C.POINTER(_BfsOptions), vp, vp, C.POINTER(_BfsStats))
+    sig("etb_bfs_compact", vp, u64, C.POINTER(_BfsOptions), vp, vp)
     sig("etb_result_device_ptrs", vp, C.POINTER(vp), C.POINTER(vp))
     sig("etb_result_download", vp, vp, vp)
     sig("etb_result_traversed_edges", vp, P64)
@@ -370,6 +372,8 @@ class BfsStats:  # bfs.hpp:27-33 KernelStats
     bottom_up_levels: int = 0
     direction_trace: str = ""
     level_claims: list = field(default_factory=list)
+    level_ns: list = field(default_factory=list)  # [init end, level 0 end, ...] from entry
+    total_ns: int = 0
 
 
 @dataclass
@@ -394,7 +398,8 @@ def et_bfs(cg: EtLayout, start: int, kernel=CoreKernel.HYBRID, replay=TreeReplay
     bs = None
     if st is not None:
         bs = BfsStats(st.levels, st.bottom_up_levels, st.direction_trace.decode(),
-                      list(st.level_claims[: st.levels]))
+                      list(st.level_claims[: st.levels]), list(st.level_ns[: st.levels + 1]),
+                      st.total_ns)
     return BfsResult(int(start), parent[:n] if parent is not None else None,
                      depth[:n] if depth is not None else None, bs)
 
