@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
       const unsigned long long claims = packed >> kItemShift;
       if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = claims;
       ++L;
+      stamp(p, 257 + L);
       bool need_convert = false;
       if (bu) {
         awake = claims;
@@ -362,7 +363,6 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
         grid_sync(p.bar);
         nitems = ld_volatile(cslot);
       }
-      stamp(p, 257 + L);
     }
   }
   if (tid == 0 && p.nlevels) *p.nlevels = L;

@@ -1,0 +1,50 @@
+"""Per-root device timeline of the persistent ET-BFS kernel (diagnostics only).
+
+For each of the 64 seed-1 roots: direction trace, claims per level and the
+per-level device durations (block 0's globaltimer stamps), plus the CUDA-event
+kernel time. Usage: python tools/root_profile.py [--scale S] [--edgefactor E] [--mh M]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2009_07463_b200 as eb  # noqa: E402
+from paper_2009_07463_b200 import etbfs as E  # noqa: E402
+from bench import select_roots_from_degrees  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--edgefactor", type=int, default=16)
+    ap.add_argument("--mh", type=int, default=-1)
+    ap.add_argument("--roots", type=int, default=64)
+    args = ap.parse_args()
+    g = eb.generate_graph(scale=args.scale, edgefactor=args.edgefactor, seed=1)
+    cg = eb.relayout_csr(g, mh=args.mh)
+    roots = select_roots_from_degrees(g.degrees(), 64, 1)[: args.roots]
+    starts = cg.old2new[roots.astype(np.int64)]
+    ms, kms = E.time_roots(cg, starts, warmup=8, flush_l2=True)
+    out = []
+    for i, s in enumerate(starts):
+        E.time_roots(cg, starts[i:i + 1], warmup=0, flush_l2=True)  # flush before the stats run
+        r = eb.et_bfs(cg, int(s), stats=True, want_parent=False, want_depth=False)
+        ns = r.stats.level_ns
+        dur = [round((ns[j + 1] - ns[j]) / 1e3, 1) for j in range(len(ns) - 1)]
+        rec = {"root": int(roots[i]), "start": int(s), "type": int(cg.vertex_type[int(s)]),
+               "kernel_us": round(float(kms[i]) * 1e3, 1), "device_us": round(r.stats.total_ns / 1e3, 1),
+               "init_us": round(ns[0] / 1e3, 1) if ns else None, "trace": r.stats.direction_trace,
+               "claims": r.stats.level_claims, "level_us": dur}
+        out.append(rec)
+        print(json.dumps(rec), flush=True)
+    k = np.array([o["kernel_us"] for o in out])
+    print(json.dumps({"kernel_us_mean": float(k.mean()), "kernel_us_max": float(k.max()),
+                      "kernel_us_min": float(k.min())}))
+
+
+if __name__ == "__main__":
+    main()
