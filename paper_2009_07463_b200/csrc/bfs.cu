@@ -33,8 +33,12 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kItemShift = 36;
 constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 
+constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down item
+constexpr int kCbuf = 2 * kTdChunk;  // staged claims per warp
+constexpr int kBuU = 4;              // visited words per warp per bottom-up iteration
+
 struct Smem {
-  uint32_t cbuf[kWarps][kTdChunk];
+  uint64_t cbuf[kWarps][kCbuf];  // (nchunks << 32) | vertex
   unsigned long long red[kWarps];
 };
 
@@ -114,115 +118,156 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   return x;
 }
 
-// Append the items (row chunks) of `ncl` claimed vertices staged in cbuf;
-// one atomic per call carries both the claim count and the item count.
-__device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, uint32_t ncl,
-                             uint64_t* items_out, unsigned long long* slot,
-                             unsigned long long& scout_acc) {
+// Append the items (row chunks) of the `ncl` claimed vertices staged in the
+// warp's smem buffer (entries (nchunks << 32) | vertex); one atomic carries both
+// the claim count (α/β) and the item count (positions).
+__device__ void flush_claims(const uint64_t* cbuf, uint32_t ncl, uint64_t* items_out,
+                             unsigned long long* slot) {
   const unsigned lane = threadIdx.x & 31;
-  unsigned long long nit = 0, sc = 0;
-  for (uint32_t i = lane; i < ncl; i += 32) {
-    const uint32_t w = cbuf[i];
-    nit += nchunks(p.crow[w + 1] - p.crow[w]);
-    sc += p.degn[w];
-  }
+  unsigned long long nit = 0;
+  for (uint32_t i = lane; i < ncl; i += 32) nit += cbuf[i] >> 32;
   nit = warp_sum(nit);
-  sc = warp_sum(sc);
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(slot, ((unsigned long long)ncl << kItemShift) | nit) & kItemMask;
   base = __shfl_sync(0xffffffffu, base, 0);
-  if (lane == 0) scout_acc += sc;
   for (uint32_t i0 = 0; i0 < ncl; i0 += 32) {
     const uint32_t i = i0 + lane;
-    uint32_t w = 0, c = 0;
-    if (i < ncl) {
-      w = cbuf[i];
-      c = nchunks(p.crow[w + 1] - p.crow[w]);
-    }
+    const uint64_t e = i < ncl ? cbuf[i] : 0ull;
+    const uint32_t c = static_cast<uint32_t>(e >> 32);
+    const uint32_t w = static_cast<uint32_t>(e);
     const uint32_t incl = warp_incl_scan(c);
-    uint64_t pos = base + incl - c;
+    const uint64_t pos = base + incl - c;
     for (uint32_t k = 0; k < c; ++k) items_out[pos + k] = (uint64_t(w) << 32) | k;
     base += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 
-__device__ void td_step(const BfsParams& p, Smem& sm, const uint64_t* items_in, uint64_t nitems,
-                        uint64_t* items_out, uint32_t* fnext, unsigned long long* slot,
-                        int32_t dnext, unsigned long long& scout_acc) {
+// Top-down step (bfs.cpp:61-86). One warp per 256-edge item; each lane owns 8
+// edges whose column loads, visited probes and claim atomics are all issued
+// before any result is consumed, so an item costs ~4 memory round trips
+// instead of 8 x 4. Claims are staged in smem and flushed >= 256 at a time.
+__device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint64_t* items_in,
+                        uint64_t nitems, uint64_t* items_out, uint32_t* fnext,
+                        unsigned long long* slot, int32_t dnext, unsigned long long& scout_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  uint32_t* cbuf = sm.cbuf[wib];
+  const unsigned lt = (1u << lane) - 1;
+  uint32_t ncl = 0;
   for (uint64_t it = gw; it < nitems; it += nw) {
     const uint64_t item = items_in[it];
     const uint32_t u = static_cast<uint32_t>(item >> 32);
     const uint32_t k = static_cast<uint32_t>(item);
     const uint64_t beg = p.crow[u] + (uint64_t)k * kTdChunk;
     const uint64_t end = min(p.crow[u + 1], beg + kTdChunk);
-    uint32_t ncl = 0;
-    for (uint64_t e0 = beg; e0 < end; e0 += 32) {
-      const uint64_t e = e0 + lane;
-      bool claim = false;
-      uint32_t w = 0;
-      if (e < end) {
-        w = p.ccol[e];
-        const uint32_t bit = 1u << (w & 31);
-        if (!(p.visited[w >> 5] & bit)) claim = !(atomicOr(&p.visited[w >> 5], bit) & bit);
+    uint32_t w[kEpl], vw[kEpl];
+    bool cl[kEpl];
+#pragma unroll
+    for (int j = 0; j < kEpl; ++j) {
+      const uint64_t e = beg + lane + 32 * j;
+      w[j] = e < end ? p.ccol[e] : kNone32;
+    }
+#pragma unroll
+    for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
+#pragma unroll
+    for (int j = 0; j < kEpl; ++j) {
+      const uint32_t bit = 1u << (w[j] & 31);
+      cl[j] = false;
+      if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
+    }
+    uint2 meta[kEpl];
+#pragma unroll
+    for (int j = 0; j < kEpl; ++j) {
+      if (cl[j]) {
+        p.depth[w[j]] = dnext;
+        p.parent[w[j]] = u;
+        atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
+        meta[j] = p.cmeta[w[j]];
       }
-      const unsigned m = __ballot_sync(0xffffffffu, claim);
-      if (claim) {
-        p.depth[w] = dnext;
-        p.parent[w] = u;
-        atomicOr(&fnext[w >> 5], 1u << (w & 31));
-        cbuf[ncl + __popc(m & ((1u << lane) - 1))] = w;
+    }
+#pragma unroll
+    for (int j = 0; j < kEpl; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, cl[j]);
+      if (cl[j]) {
+        scout_acc += meta[j].y;
+        const uint64_t nch = (meta[j].x + kTdChunk - 1) / kTdChunk;
+        cbuf[ncl + __popc(m & lt)] = (nch << 32) | w[j];
       }
       ncl += __popc(m);
     }
     __syncwarp();
-    if (ncl) flush_claims(p, cbuf, ncl, items_out, slot, scout_acc);
-    __syncwarp();
+    if (ncl > kCbuf - kTdChunk) {
+      flush_claims(cbuf, ncl, items_out, slot);
+      ncl = 0;
+      __syncwarp();
+    }
   }
+  if (ncl) flush_claims(cbuf, ncl, items_out, slot);
+  __syncwarp();
 }
 
+__device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcur, uint32_t v,
+                                         uint32_t& par) {
+  // The first (highest-degree) neighbour was already probed; the rest of the
+  // row is probed four at a time (independent loads) with early exit.
+  const uint64_t re = p.crow[v + 1];
+  for (uint64_t e = p.crow[v] + 1; e < re; e += 4) {
+    uint32_t x[4];
+    bool b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = e + j < re ? p.ccol[e + j] : kNone32;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = x[j] != kNone32 && test_bit(fcur, x[j]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (b[j]) {
+        par = x[j];
+        return true;
+      }
+  }
+  return false;
+}
+
+// Bottom-up step (bfs.cpp:88-111). A warp takes kBuU consecutive visited words
+// per iteration, lane = one vertex of each; all first-neighbour probes of the
+// kBuU words are in flight together. Each word is written back once.
 __device__ void bu_step(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext, int32_t dnext,
                         unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t wi = gw; wi < p.nwords; wi += nw) {
-    const uint32_t vis = p.visited[wi];  // a BU level writes word wi from this warp only
-    if (vis == 0xFFFFFFFFu) continue;
-    const uint32_t v = static_cast<uint32_t>(wi * 32 + lane);
-    bool claim = false;
-    uint32_t par = 0;
-    if (!((vis >> lane) & 1u)) {  // padding bits past nc are pre-set in `visited`
-      const uint32_t f = p.cfirst[v];
-      if (f != kNone32) {
-        if (test_bit(fcur, f)) {
-          claim = true;
-          par = f;
-        } else {
-          const uint64_t re = p.crow[v + 1];
-          for (uint64_t e = p.crow[v] + 1; e < re; ++e) {
-            const uint32_t x = p.ccol[e];
-            if (test_bit(fcur, x)) {
-              claim = true;
-              par = x;
-              break;
-            }
-          }
-        }
+  for (uint64_t w0 = gw * kBuU; w0 < p.nwords; w0 += nw * kBuU) {
+    uint32_t vis[kBuU];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < kBuU; ++k) {
+      vis[k] = w0 + k < p.nwords ? p.visited[w0 + k] : ~0u;
+      any |= vis[k] != ~0u;
+    }
+    if (!any) continue;
+    uint32_t f[kBuU];
+#pragma unroll
+    for (int k = 0; k < kBuU; ++k)
+      f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[(w0 + k) * 32 + lane];
+    bool hit[kBuU];
+#pragma unroll
+    for (int k = 0; k < kBuU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
+#pragma unroll
+    for (int k = 0; k < kBuU; ++k) {
+      uint32_t par = f[k];
+      if (f[k] != kNone32 && !hit[k])
+        hit[k] = scan_row(p, fcur, static_cast<uint32_t>((w0 + k) * 32 + lane), par);
+      const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
+      if (hit[k]) {
+        const uint32_t v = static_cast<uint32_t>((w0 + k) * 32 + lane);
+        p.depth[v] = dnext;
+        p.parent[v] = par;
       }
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, claim);
-    if (claim) {
-      p.depth[v] = dnext;
-      p.parent[v] = par;
-    }
-    if (lane == 0 && m) {
-      p.visited[wi] = vis | m;
-      fnext[wi] = m;
-      claims_acc += __popc(m);
+      if (lane == 0 && m) {
+        p.visited[w0 + k] = vis[k] | m;
+        fnext[w0 + k] = m;
+        claims_acc += __popc(m);
+      }
     }
   }
 }
@@ -240,7 +285,7 @@ __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint64_t*
     uint32_t cnt = 0;
     for (uint32_t b = bits; b; b &= b - 1) {
       const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
-      cnt += nchunks(p.crow[v + 1] - p.crow[v]);
+      cnt += (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
     }
     const uint32_t incl = warp_incl_scan(cnt);
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
@@ -251,14 +296,15 @@ __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint64_t*
     uint64_t pos = base + incl - cnt;
     for (uint32_t b = bits; b; b &= b - 1) {
       const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
-      const uint32_t c = nchunks(p.crow[v + 1] - p.crow[v]);
+      const uint32_t c = (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
       for (uint32_t k = 0; k < c; ++k) items_out[pos++] = (uint64_t(v) << 32) | k;
     }
   }
 }
 
-__global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
-  __shared__ Smem sm;
+__global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t start = p.start;
@@ -283,7 +329,7 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
   if (tid < 24) p.ctr[tid] = 0;
   uint64_t nitems = 0;
   if (run_core) {
-    nitems = nchunks(p.crow[start + 1] - p.crow[start]);
+    nitems = (p.cmeta[start].x + kTdChunk - 1) / kTdChunk;
     for (uint64_t k = tid; k < nitems; k += nthreads) p.items0[k] = (uint64_t(start) << 32) | k;
     if (tid == 0) {
       p.depth[start] = p.base_depth;
@@ -323,7 +369,8 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
         block_add(acc << kItemShift, &slot[0], sm);
       } else {
         etc -= (double)scout;
-        td_step(p, sm, items_in, nitems, items_out, fnext, slot, dnext, acc);
+        td_step(p, sm.cbuf[threadIdx.x >> 5], items_in, nitems, items_out, fnext, slot, dnext,
+                acc);
         block_add(acc, &slot[1], sm);
       }
       grid_sync(p.bar);
@@ -368,22 +415,35 @@ __global__ void __launch_bounds__(kBlock) et_bfs_kernel(BfsParams p) {
   if (tid == 0 && p.nlevels) *p.nlevels = L;
 
   // ---- unreached core vertices + tree replay + start-tree patch ----------------
-  for (uint64_t v = tid; v < p.nc; v += nthreads) {
-    if (!test_bit(p.visited, static_cast<uint32_t>(v))) {
+  for (uint64_t wi = tid; wi < p.nwords; wi += nthreads) {
+    for (uint32_t un = ~p.visited[wi]; un; un &= un - 1) {  // padding bits are set
+      const uint64_t v = wi * 32 + __ffs(un) - 1;
       p.depth[v] = -1;
       p.parent[v] = kNone32;
     }
   }
-  for (uint64_t t = tid; t < p.nt; t += nthreads) {
-    const uint32_t tv = static_cast<uint32_t>(p.nc + t);
-    if (tv >= p.skip_lo && tv < p.skip_hi) continue;
-    const uint32_t a = p.tanchor[t];
-    if (a != kNone32 && test_bit(p.visited, a)) {
-      p.depth[tv] = __ldcg(&p.depth[a]) + static_cast<int32_t>(p.tdepth[t]);
-      p.parent[tv] = p.tsrc[t];
-    } else {
-      p.depth[tv] = -1;
-      p.parent[tv] = kNone32;
+  for (uint64_t t0 = tid; t0 < p.nt; t0 += 4 * nthreads) {
+    uint32_t a[4], vis[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t t = t0 + k * nthreads;
+      const uint32_t tv = static_cast<uint32_t>(p.nc + t);
+      a[k] = (t < p.nt && !(tv >= p.skip_lo && tv < p.skip_hi)) ? p.tanchor[t] : kNone32 - 1;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) vis[k] = a[k] < kNone32 - 1 ? test_bit(p.visited, a[k]) : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (a[k] == kNone32 - 1) continue;  // out of range or inside the start's tree
+      const uint64_t t = t0 + k * nthreads;
+      const uint32_t tv = static_cast<uint32_t>(p.nc + t);
+      if (vis[k]) {
+        p.depth[tv] = __ldcg(&p.depth[a[k]]) + static_cast<int32_t>(p.tdepth[t]);
+        p.parent[tv] = p.tsrc[t];
+      } else {
+        p.depth[tv] = -1;
+        p.parent[tv] = kNone32;
+      }
     }
   }
   for (uint64_t i = tid; i < p.npatch; i += nthreads) {
@@ -426,7 +486,10 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   int dev = 0, sms = 0, per_sm = 0;
   ETB_CUDA(cudaGetDevice(&dev));
   ETB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, et_bfs_kernel, kBlock, 0));
+  ETB_CUDA(cudaFuncSetAttribute(et_bfs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(Smem)));
+  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, et_bfs_kernel, kBlock,
+                                                         sizeof(Smem)));
   if (per_sm < 1) throw CudaError("et_bfs_kernel cannot be resident");
   S.block = kBlock;
   S.grid = sms * std::min(per_sm, 2);
@@ -438,6 +501,7 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.ccol = L.ccol.get();
   p.cfirst = L.cfirst.get();
   p.degn = L.degn.get();
+  p.cmeta = L.cmeta.get();
   p.nc = static_cast<uint32_t>(L.nc);
   p.nwords = static_cast<uint32_t>((L.nc + 31) / 32);
   p.tsrc = L.tsrc.get();
@@ -553,7 +617,7 @@ void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParam
 void bfs_launch(const BfsParams& p, const BfsState& S, cudaStream_t s) {
   void* args[] = {const_cast<BfsParams*>(&p)};
   ETB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(et_bfs_kernel), dim3(S.grid),
-                                       dim3(S.block), args, 0, s));
+                                       dim3(S.block), args, sizeof(Smem), s));
 }
 
 }  // namespace etb

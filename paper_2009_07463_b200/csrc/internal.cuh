@@ -53,6 +53,7 @@ struct DevLayout {
   DevBuf<uint64_t> crow;   // nc + 1
   DevBuf<uint32_t> ccol;   // ecore
   DevBuf<uint32_t> cfirst; // nc: first (highest-degree) core neighbour or kNone32
+  DevBuf<uint2> cmeta;     // nc: {core degree, full degree} — one load per claim
   // edge-tree arrays, index t - nc for t in [nc, nc + nt)
   DevBuf<uint32_t> tsrc;    // tree parent (CE for attached roots, self for component roots)
   DevBuf<uint32_t> tanchor; // CE, or kNone32 for whole-component trees

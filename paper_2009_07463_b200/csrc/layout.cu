@@ -406,9 +406,12 @@ __global__ void key_cols_kernel(const uint64_t* keys, uint64_t count, uint64_t m
   GRID_LOOP(i, count) col[i] = static_cast<uint32_t>(keys[i] & mask);
 }
 
-__global__ void first_nbr_kernel(const uint64_t* crow, const uint32_t* ccol, uint64_t nc,
-                                 uint32_t* first) {
-  GRID_LOOP(i, nc) first[i] = crow[i] < crow[i + 1] ? ccol[crow[i]] : kNone32;
+__global__ void first_nbr_kernel(const uint64_t* crow, const uint32_t* ccol, const uint32_t* degn,
+                                 uint64_t nc, uint32_t* first, uint2* meta) {
+  GRID_LOOP(i, nc) {
+    first[i] = crow[i] < crow[i + 1] ? ccol[crow[i]] : kNone32;
+    meta[i] = make_uint2(static_cast<uint32_t>(crow[i + 1] - crow[i]), degn[i]);
+  }
 }
 
 __global__ void gather_u32_kernel(const uint32_t* src, const uint32_t* idx, uint64_t n,
@@ -635,6 +638,7 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
   L.ecore = read_u64(L.crow.get() + nc, s);
   L.ccol.alloc(L.ecore ? L.ecore : 1);
   L.cfirst.alloc(nc ? nc : 1);
+  L.cmeta.alloc(nc ? nc : 1);
   if (L.ecore) {
     const int b = bits_for(nc);
     DevBuf<uint64_t> keys(L.ecore), alt;
@@ -649,8 +653,8 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
     ETB_LAUNCH_CHECK();
   }
   if (nc) {
-    first_nbr_kernel<<<grid_for(nc, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), nc,
-                                                       L.cfirst.get());
+    first_nbr_kernel<<<grid_for(nc, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), L.degn.get(),
+                                                       nc, L.cfirst.get(), L.cmeta.get());
     ETB_LAUNCH_CHECK();
   }
   ETB_CUDA(cudaStreamSynchronize(s));
