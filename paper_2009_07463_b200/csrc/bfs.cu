@@ -118,6 +118,22 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   return x;
 }
 
+// Each lane owns `c` items of vertex w starting at pos. Short runs are written
+// by their lane; long runs (hub rows) by the whole warp, strided.
+__device__ __forceinline__ void write_items(uint64_t* items_out, uint64_t pos, uint32_t w,
+                                            uint32_t c) {
+  const unsigned lane = threadIdx.x & 31;
+  if (c <= 8)
+    for (uint32_t k = 0; k < c; ++k) items_out[pos + k] = (uint64_t(w) << 32) | k;
+  for (unsigned big = __ballot_sync(0xffffffffu, c > 8); big; big &= big - 1) {
+    const int src = __ffs(big) - 1;
+    const uint32_t bw = __shfl_sync(0xffffffffu, w, src);
+    const uint64_t bp = __shfl_sync(0xffffffffu, pos, src);
+    const uint32_t bc = __shfl_sync(0xffffffffu, c, src);
+    for (uint32_t k = lane; k < bc; k += 32) items_out[bp + k] = (uint64_t(bw) << 32) | k;
+  }
+}
+
 // Append the items (row chunks) of the `ncl` claimed vertices staged in the
 // warp's smem buffer (entries (nchunks << 32) | vertex); one atomic carries both
 // the claim count (α/β) and the item count (positions).
@@ -136,8 +152,7 @@ __device__ void flush_claims(const uint64_t* cbuf, uint32_t ncl, uint64_t* items
     const uint32_t c = static_cast<uint32_t>(e >> 32);
     const uint32_t w = static_cast<uint32_t>(e);
     const uint32_t incl = warp_incl_scan(c);
-    const uint64_t pos = base + incl - c;
-    for (uint32_t k = 0; k < c; ++k) items_out[pos + k] = (uint64_t(w) << 32) | k;
+    write_items(items_out, base + incl - c, w, c);
     base += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
@@ -148,7 +163,8 @@ __device__ void flush_claims(const uint64_t* cbuf, uint32_t ncl, uint64_t* items
 // instead of 8 x 4. Claims are staged in smem and flushed >= 256 at a time.
 __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint64_t* items_in,
                         uint64_t nitems, uint64_t* items_out, uint32_t* fnext,
-                        unsigned long long* slot, int32_t dnext, unsigned long long& scout_acc) {
+                        unsigned long long* slot, int32_t dnext, bool emit,
+                        unsigned long long& scout_acc, unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
@@ -174,6 +190,27 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint64_t* item
       const uint32_t bit = 1u << (w[j] & 31);
       cl[j] = false;
       if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
+    }
+    if (!emit) {
+      // Large frontier: no work items (a bottom-up level almost surely follows;
+      // if not, the bitmap is converted). Claims are only counted.
+      uint32_t dg[kEpl];
+#pragma unroll
+      for (int j = 0; j < kEpl; ++j) {
+        dg[j] = 0;
+        if (cl[j]) {
+          p.depth[w[j]] = dnext;
+          p.parent[w[j]] = u;
+          atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
+          dg[j] = p.degn[w[j]];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kEpl; ++j) {
+        scout_acc += dg[j];
+        claims_acc += cl[j];
+      }
+      continue;
     }
     uint2 meta[kEpl];
 #pragma unroll
@@ -230,12 +267,74 @@ __device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcu
 
 // Bottom-up step (bfs.cpp:88-111). A warp takes kBuU consecutive visited words
 // per iteration, lane = one vertex of each; all first-neighbour probes of the
-// kBuU words are in flight together. Each word is written back once.
-__device__ void bu_step(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext, int32_t dnext,
-                        unsigned long long& claims_acc) {
+// kBuU words are in flight together and each word is written back once.
+// Vertices whose first (highest-degree) neighbour is not in the frontier are
+// deferred to a per-warp smem list and scanned afterwards, one lane per vertex
+// (rows of <= kLaneScan core neighbours) or the whole warp per vertex (longer
+// rows), so one long row no longer stalls 31 idle lanes.
+constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (reuses the claim buffer)
+constexpr uint32_t kLaneScan = 64;
+
+__device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext,
+                               uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
+                               unsigned long long& claims_acc) {
+  const unsigned lane = threadIdx.x & 31;
+  __syncwarp();
+  uint32_t nlong = 0;
+  for (uint32_t i0 = 0; i0 < nmiss; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t v = i < nmiss ? mbuf[i] : kNone32;
+    bool lng = false, hit = false;
+    uint32_t par = 0;
+    if (v != kNone32) {
+      if (p.cmeta[v].x > kLaneScan) lng = true;
+      else hit = scan_row(p, fcur, v, par);
+    }
+    if (hit) {
+      p.depth[v] = dnext;
+      p.parent[v] = par;
+      atomicOr(&p.visited[v >> 5], 1u << (v & 31));
+      atomicOr(&fnext[v >> 5], 1u << (v & 31));
+      ++claims_acc;
+    }
+    // compact long rows to the front of the buffer (slots < i0 are consumed)
+    const unsigned lm = __ballot_sync(0xffffffffu, lng);
+    __syncwarp();
+    if (lng) mbuf[nlong + __popc(lm & ((1u << lane) - 1))] = v;
+    nlong += __popc(lm);
+    __syncwarp();
+  }
+  for (uint32_t i = 0; i < nlong; ++i) {
+    const uint32_t v = mbuf[i];
+    const uint64_t rb = p.crow[v] + 1, re = p.crow[v + 1];
+    uint32_t par = kNone32;
+    for (uint64_t e0 = rb; e0 < re; e0 += 32) {
+      const uint64_t e = e0 + lane;
+      const uint32_t x = e < re ? p.ccol[e] : kNone32;
+      const unsigned m = __ballot_sync(0xffffffffu, x != kNone32 && test_bit(fcur, x));
+      if (m) {
+        par = __shfl_sync(0xffffffffu, x, __ffs(m) - 1);
+        break;
+      }
+    }
+    if (lane == 0 && par != kNone32) {
+      p.depth[v] = dnext;
+      p.parent[v] = par;
+      atomicOr(&p.visited[v >> 5], 1u << (v & 31));
+      atomicOr(&fnext[v >> 5], 1u << (v & 31));
+      ++claims_acc;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur,
+                        uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  const unsigned lt = (1u << lane) - 1;
+  uint32_t nmiss = 0;
   for (uint64_t w0 = gw * kBuU; w0 < p.nwords; w0 += nw * kBuU) {
     uint32_t vis[kBuU];
     bool any = false;
@@ -254,22 +353,28 @@ __device__ void bu_step(const BfsParams& p, const uint32_t* fcur, uint32_t* fnex
     for (int k = 0; k < kBuU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
 #pragma unroll
     for (int k = 0; k < kBuU; ++k) {
-      uint32_t par = f[k];
-      if (f[k] != kNone32 && !hit[k])
-        hit[k] = scan_row(p, fcur, static_cast<uint32_t>((w0 + k) * 32 + lane), par);
+      const uint32_t v = static_cast<uint32_t>((w0 + k) * 32 + lane);
       const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
       if (hit[k]) {
-        const uint32_t v = static_cast<uint32_t>((w0 + k) * 32 + lane);
         p.depth[v] = dnext;
-        p.parent[v] = par;
+        p.parent[v] = f[k];
       }
       if (lane == 0 && m) {
         p.visited[w0 + k] = vis[k] | m;
         fnext[w0 + k] = m;
         claims_acc += __popc(m);
       }
+      const bool miss = f[k] != kNone32 && !hit[k];
+      const unsigned mm = __ballot_sync(0xffffffffu, miss);
+      if (miss) mbuf[nmiss + __popc(mm & lt)] = v;
+      nmiss += __popc(mm);
+    }
+    if (nmiss > kMissCap - 32 * kBuU) {
+      resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
+      nmiss = 0;
     }
   }
+  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
 }
 
 // Frontier bitmap -> top-down work items (needed only when a bottom-up phase
@@ -362,16 +467,24 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
         if (p.trace && L < 255) p.trace[L] = bu ? 'b' : 't';
       }
       const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
-      unsigned long long acc = 0;
+      unsigned long long claims_acc = 0, scout_acc = 0;
+      bool items_valid = true;
       if (bu) {
         prev = awake;
-        bu_step(p, fcur, fnext, dnext, acc);
-        block_add(acc << kItemShift, &slot[0], sm);
+        bu_step(p, reinterpret_cast<uint32_t*>(sm.cbuf[threadIdx.x >> 5]), fcur, fnext, dnext,
+                claims_acc);
+        block_add(claims_acc << kItemShift, &slot[0], sm);
       } else {
         etc -= (double)scout;
+        // Work items for the next level are emitted only for frontiers whose
+        // edge count is small; a large one is all but certain to hand over to
+        // bottom-up (which needs only the bitmap), else the bitmap is converted.
+        const bool emit = (double)scout < p.emit_limit;
+        items_valid = emit;
         td_step(p, sm.cbuf[threadIdx.x >> 5], items_in, nitems, items_out, fnext, slot, dnext,
-                acc);
-        block_add(acc, &slot[1], sm);
+                emit, scout_acc, claims_acc);
+        block_add(scout_acc, &slot[1], sm);
+        if (!emit) block_add(claims_acc << kItemShift, &slot[0], sm);
       }
       grid_sync(p.bar);
       const unsigned long long packed = ld_volatile(&slot[0]);
@@ -379,14 +492,13 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
       if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = claims;
       ++L;
       stamp(p, 257 + L);
-      bool need_convert = false;
       if (bu) {
         awake = claims;
         if (!(awake > 0 && (awake >= prev || (double)awake > (double)p.nc / p.beta))) {
           bu = false;
           frontier = awake;
           scout = 1;
-          need_convert = true;
+          items_valid = false;
         }
       } else {
         frontier = claims;
@@ -401,14 +513,12 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
         if (!p.top_down_only && (double)scout > etc / p.alpha) {
           bu = true;
           awake = frontier;
-          need_convert = false;
+        } else if (!items_valid) {
+          unsigned long long* cslot = p.ctr + 16 + (L & 1);
+          convert_step(p, F[L % 3], items_in, cslot);
+          grid_sync(p.bar);
+          nitems = ld_volatile(cslot);
         }
-      }
-      if (need_convert) {
-        unsigned long long* cslot = p.ctr + 16 + (L & 1);
-        convert_step(p, F[L % 3], items_in, cslot);
-        grid_sync(p.bar);
-        nitems = ld_volatile(cslot);
       }
     }
   }
@@ -521,6 +631,7 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.patch = S.patch.get();
   p.npatch = 0;
   p.edges_to_check = static_cast<double>(L.ecore);
+  p.emit_limit = static_cast<double>(L.nc) / 4.0 + 1024.0;
   p.trace = nullptr;
   p.level_claims = nullptr;
   p.nlevels = nullptr;

@@ -42,6 +42,7 @@ struct BfsParams {
   const uint32_t* patch;  // (vertex, depth, parent) triples
   uint32_t npatch;
   double alpha, beta, edges_to_check;
+  double emit_limit;  // top-down levels with scout >= this skip work-item emission
   int top_down_only;
   // stats (may be null)
   char* trace;
