@@ -5,10 +5,10 @@
 //   level loop      the reference's α/β direction-optimizing driver
 //                   (src/bfs.cpp:232-293), decided redundantly by every thread
 //                   from grid-reduced counters, with no host round trip;
-//                     top-down  (bfs.cpp:61-86): work items are 256-edge chunks
-//                               of frontier rows, one warp per item, check-then-
-//                               atomicOr claims, claimed vertices staged in smem
-//                               and appended with one atomic per item;
+//                     top-down  (bfs.cpp:61-86): the frontier's rows are cut in
+//                               256-edge chunks spread evenly over all warps,
+//                               8 edges per lane in flight, check-then-atomicOr
+//                               claims staged in smem and appended in batches;
 //                     bottom-up (bfs.cpp:88-111): one warp per 32-vertex visited
 //                               word, first probe on the contiguous first-
 //                               neighbour array (the highest-degree neighbour,
@@ -118,128 +118,132 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   return x;
 }
 
-// Each lane owns `c` items of vertex w starting at pos. Short runs are written
-// by their lane; long runs (hub rows) by the whole warp, strided.
-__device__ __forceinline__ void write_items(uint64_t* items_out, uint64_t pos, uint32_t w,
-                                            uint32_t c) {
-  const unsigned lane = threadIdx.x & 31;
-  if (c <= 8)
-    for (uint32_t k = 0; k < c; ++k) items_out[pos + k] = (uint64_t(w) << 32) | k;
-  for (unsigned big = __ballot_sync(0xffffffffu, c > 8); big; big &= big - 1) {
-    const int src = __ffs(big) - 1;
-    const uint32_t bw = __shfl_sync(0xffffffffu, w, src);
-    const uint64_t bp = __shfl_sync(0xffffffffu, pos, src);
-    const uint32_t bc = __shfl_sync(0xffffffffu, c, src);
-    for (uint32_t k = lane; k < bc; k += 32) items_out[bp + k] = (uint64_t(bw) << 32) | k;
-  }
-}
+// Frontier list: vertex ids qv[0..nq) plus the exclusive prefix qp[] of their
+// row-chunk counts (a chunk = kTdChunk core edges). A top-down level splits the
+// nu = sum(chunks) chunks evenly over all warps: each warp takes a contiguous
+// chunk range, finds its first vertex with one 32-ary warp search and walks
+// forward. Claims append (vertex, chunk prefix) pairs with one packed atomic per
+// staged batch: (claims << 36) | chunks returns both positions at once.
 
-// Append the items (row chunks) of the `ncl` claimed vertices staged in the
-// warp's smem buffer (entries (nchunks << 32) | vertex); one atomic carries both
-// the claim count (α/β) and the item count (positions).
-__device__ void flush_claims(const uint64_t* cbuf, uint32_t ncl, uint64_t* items_out,
-                             unsigned long long* slot) {
+// Append the staged claims (entries (nchunks << 32) | vertex) to the next list.
+__device__ void flush_claims(const uint64_t* cbuf, uint32_t ncl, uint32_t* qv_out,
+                             uint64_t* qp_out, unsigned long long* slot) {
   const unsigned lane = threadIdx.x & 31;
-  unsigned long long nit = 0;
-  for (uint32_t i = lane; i < ncl; i += 32) nit += cbuf[i] >> 32;
-  nit = warp_sum(nit);
-  unsigned long long base = 0;
-  if (lane == 0) base = atomicAdd(slot, ((unsigned long long)ncl << kItemShift) | nit) & kItemMask;
-  base = __shfl_sync(0xffffffffu, base, 0);
+  unsigned long long nch = 0;
+  for (uint32_t i = lane; i < ncl; i += 32) nch += cbuf[i] >> 32;
+  nch = warp_sum(nch);
+  unsigned long long old = 0;
+  if (lane == 0) old = atomicAdd(slot, ((unsigned long long)ncl << kItemShift) | nch);
+  old = __shfl_sync(0xffffffffu, old, 0);
+  uint64_t vpos = old >> kItemShift, cpos = old & kItemMask;
   for (uint32_t i0 = 0; i0 < ncl; i0 += 32) {
     const uint32_t i = i0 + lane;
     const uint64_t e = i < ncl ? cbuf[i] : 0ull;
     const uint32_t c = static_cast<uint32_t>(e >> 32);
-    const uint32_t w = static_cast<uint32_t>(e);
     const uint32_t incl = warp_incl_scan(c);
-    write_items(items_out, base + incl - c, w, c);
-    base += __shfl_sync(0xffffffffu, incl, 31);
+    if (i < ncl) {
+      qv_out[vpos + i] = static_cast<uint32_t>(e);
+      qp_out[vpos + i] = cpos + incl - c;
+    }
+    cpos += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 
-// Top-down step (bfs.cpp:61-86). One warp per 256-edge item; each lane owns 8
-// edges whose column loads, visited probes and claim atomics are all issued
-// before any result is consumed, so an item costs ~4 memory round trips
-// instead of 8 x 4. Claims are staged in smem and flushed >= 256 at a time.
-__device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint64_t* items_in,
-                        uint64_t nitems, uint64_t* items_out, uint32_t* fnext,
-                        unsigned long long* slot, int32_t dnext, bool emit,
+// Index of the last list entry whose chunk prefix is <= unit (32-ary search).
+__device__ uint64_t find_vertex(const uint64_t* qp, uint64_t nq, uint64_t unit) {
+  const unsigned lane = threadIdx.x & 31;
+  uint64_t lo = 0, hi = nq;  // invariant: qp[lo] <= unit < qp[hi] (qp[nq] = +inf)
+  while (hi - lo > 32) {
+    const uint64_t stride = (hi - lo + 31) / 32;
+    const uint64_t idx = lo + lane * stride;
+    const bool le = idx < hi && qp[idx] <= unit;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    const uint64_t j = 31 - __clz(m);
+    const uint64_t nlo = lo + j * stride;
+    hi = min(hi, nlo + stride);
+    lo = nlo;
+  }
+  const uint64_t idx = lo + lane;
+  const unsigned m = __ballot_sync(0xffffffffu, idx < hi && qp[idx] <= unit);
+  return lo + (31 - __clz(m));
+}
+
+// Top-down step (bfs.cpp:61-86). Each lane owns 8 edges of the warp's current
+// chunk; their column loads, visited probes and claim atomics are issued
+// before any result is consumed.
+__device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, const uint64_t* qp,
+                        uint64_t nq, uint64_t nu, uint32_t* qv_out, uint64_t* qp_out,
+                        uint32_t* fnext, unsigned long long* slot, int32_t dnext, bool emit,
                         unsigned long long& scout_acc, unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
   const unsigned lt = (1u << lane) - 1;
+  const uint64_t per = (nu + nw - 1) / nw;
+  const uint64_t u0 = gw * per, u1 = min(nu, u0 + per);
   uint32_t ncl = 0;
-  for (uint64_t it = gw; it < nitems; it += nw) {
-    const uint64_t item = items_in[it];
-    const uint32_t u = static_cast<uint32_t>(item >> 32);
-    const uint32_t k = static_cast<uint32_t>(item);
-    const uint64_t beg = p.crow[u] + (uint64_t)k * kTdChunk;
-    const uint64_t end = min(p.crow[u + 1], beg + kTdChunk);
-    uint32_t w[kEpl], vw[kEpl];
-    bool cl[kEpl];
-#pragma unroll
-    for (int j = 0; j < kEpl; ++j) {
-      const uint64_t e = beg + lane + 32 * j;
-      w[j] = e < end ? p.ccol[e] : kNone32;
-    }
-#pragma unroll
-    for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
-#pragma unroll
-    for (int j = 0; j < kEpl; ++j) {
-      const uint32_t bit = 1u << (w[j] & 31);
-      cl[j] = false;
-      if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
-    }
-    if (!emit) {
-      // Large frontier: no work items (a bottom-up level almost surely follows;
-      // if not, the bitmap is converted). Claims are only counted.
-      uint32_t dg[kEpl];
+  if (u0 < u1) {
+    uint64_t i = find_vertex(qp, nq, u0);
+    for (uint64_t unit = u0; unit < u1; ++unit) {
+      while (i + 1 < nq && qp[i + 1] <= unit) ++i;
+      const uint32_t u = qv[i];
+      const uint64_t beg = p.crow[u] + (unit - qp[i]) * kTdChunk;
+      const uint64_t end = min(p.crow[u + 1], beg + kTdChunk);
+      uint32_t w[kEpl], vw[kEpl];
+      bool cl[kEpl];
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
-        dg[j] = 0;
+        const uint64_t e = beg + lane + 32 * j;
+        w[j] = e < end ? p.ccol[e] : kNone32;
+      }
+#pragma unroll
+      for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
+#pragma unroll
+      for (int j = 0; j < kEpl; ++j) {
+        const uint32_t bit = 1u << (w[j] & 31);
+        cl[j] = false;
+        if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
+      }
+      uint2 meta[kEpl];
+#pragma unroll
+      for (int j = 0; j < kEpl; ++j) {
         if (cl[j]) {
           p.depth[w[j]] = dnext;
           p.parent[w[j]] = u;
           atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
-          dg[j] = p.degn[w[j]];
+          meta[j] = p.cmeta[w[j]];
         }
+      }
+      if (!emit) {
+        // Large frontier: the next level is all but certainly bottom-up, which
+        // needs only the bitmap (otherwise the bitmap is converted); count only.
+#pragma unroll
+        for (int j = 0; j < kEpl; ++j)
+          if (cl[j]) {
+            scout_acc += meta[j].y;
+            ++claims_acc;
+          }
+        continue;
       }
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
-        scout_acc += dg[j];
-        claims_acc += cl[j];
+        const unsigned m = __ballot_sync(0xffffffffu, cl[j]);
+        if (cl[j]) {
+          scout_acc += meta[j].y;
+          const uint64_t nch = (meta[j].x + kTdChunk - 1) / kTdChunk;
+          cbuf[ncl + __popc(m & lt)] = (nch << 32) | w[j];
+        }
+        ncl += __popc(m);
       }
-      continue;
-    }
-    uint2 meta[kEpl];
-#pragma unroll
-    for (int j = 0; j < kEpl; ++j) {
-      if (cl[j]) {
-        p.depth[w[j]] = dnext;
-        p.parent[w[j]] = u;
-        atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
-        meta[j] = p.cmeta[w[j]];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kEpl; ++j) {
-      const unsigned m = __ballot_sync(0xffffffffu, cl[j]);
-      if (cl[j]) {
-        scout_acc += meta[j].y;
-        const uint64_t nch = (meta[j].x + kTdChunk - 1) / kTdChunk;
-        cbuf[ncl + __popc(m & lt)] = (nch << 32) | w[j];
-      }
-      ncl += __popc(m);
-    }
-    __syncwarp();
-    if (ncl > kCbuf - kTdChunk) {
-      flush_claims(cbuf, ncl, items_out, slot);
-      ncl = 0;
       __syncwarp();
+      if (ncl > kCbuf - kTdChunk) {
+        flush_claims(cbuf, ncl, qv_out, qp_out, slot);
+        ncl = 0;
+        __syncwarp();
+      }
     }
   }
-  if (ncl) flush_claims(cbuf, ncl, items_out, slot);
+  if (ncl) flush_claims(cbuf, ncl, qv_out, qp_out, slot);
   __syncwarp();
 }
 
@@ -377,32 +381,37 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
   if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
 }
 
-// Frontier bitmap -> top-down work items (needed only when a bottom-up phase
-// hands over to top-down). Lane = one bitmap word.
-__device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint64_t* items_out,
-                             unsigned long long* cslot) {
+// Frontier bitmap -> frontier list (when a top-down level follows one that did
+// not emit a list). Lane = one bitmap word; one packed atomic per 32 words.
+__device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t* qv_out,
+                             uint64_t* qp_out, unsigned long long* cslot) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
   for (uint64_t w0 = gw * 32; w0 < p.nwords; w0 += nw * 32) {
     const uint64_t wi = w0 + lane;
     const uint32_t bits = wi < p.nwords ? fcur[wi] : 0u;
-    uint32_t cnt = 0;
+    uint32_t cnt = __popc(bits), nch = 0;
     for (uint32_t b = bits; b; b &= b - 1) {
       const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
-      cnt += (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
+      nch += (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
     }
-    const uint32_t incl = warp_incl_scan(cnt);
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) continue;
-    unsigned long long base = 0;
-    if (lane == 31) base = atomicAdd(cslot, (unsigned long long)total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    uint64_t pos = base + incl - cnt;
+    const uint32_t vin = warp_incl_scan(cnt);
+    const uint32_t cin = warp_incl_scan(nch);
+    const uint32_t vtot = __shfl_sync(0xffffffffu, vin, 31);
+    if (vtot == 0) continue;
+    const uint32_t ctot = __shfl_sync(0xffffffffu, cin, 31);
+    unsigned long long old = 0;
+    if (lane == 31)
+      old = atomicAdd(cslot, ((unsigned long long)vtot << kItemShift) | ctot);
+    old = __shfl_sync(0xffffffffu, old, 31);
+    uint64_t vpos = (old >> kItemShift) + vin - cnt, cpos = (old & kItemMask) + cin - nch;
     for (uint32_t b = bits; b; b &= b - 1) {
       const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
-      const uint32_t c = (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
-      for (uint32_t k = 0; k < c; ++k) items_out[pos++] = (uint64_t(v) << 32) | k;
+      qv_out[vpos] = v;
+      qp_out[vpos] = cpos;
+      ++vpos;
+      cpos += (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
     }
   }
 }
@@ -432,11 +441,13 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
     p.fb2[i] = 0;
   }
   if (tid < 24) p.ctr[tid] = 0;
-  uint64_t nitems = 0;
+  uint64_t nq = 0, nu = 0;  // frontier list length and its chunk count
   if (run_core) {
-    nitems = (p.cmeta[start].x + kTdChunk - 1) / kTdChunk;
-    for (uint64_t k = tid; k < nitems; k += nthreads) p.items0[k] = (uint64_t(start) << 32) | k;
+    nq = 1;
+    nu = (p.cmeta[start].x + kTdChunk - 1) / kTdChunk;
     if (tid == 0) {
+      p.qv0[0] = start;
+      p.qp0[0] = 0;
       p.depth[start] = p.base_depth;
       p.parent[start] = p.start_parent;
     }
@@ -448,8 +459,10 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
   uint32_t L = 0;
   if (run_core) {
     uint32_t* F[3] = {p.fb0, p.fb1, p.fb2};
-    uint64_t* items_in = p.items0;
-    uint64_t* items_out = p.items1;
+    uint32_t* qv_in = p.qv0;
+    uint32_t* qv_out = p.qv1;
+    uint64_t* qp_in = p.qp0;
+    uint64_t* qp_out = p.qp1;
     unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0;
     double etc = p.edges_to_check;
     bool bu = !p.top_down_only && (double)scout > etc / p.alpha;
@@ -468,7 +481,7 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
       }
       const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
       unsigned long long claims_acc = 0, scout_acc = 0;
-      bool items_valid = true;
+      bool list_valid = true;
       if (bu) {
         prev = awake;
         bu_step(p, reinterpret_cast<uint32_t*>(sm.cbuf[threadIdx.x >> 5]), fcur, fnext, dnext,
@@ -476,13 +489,13 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
         block_add(claims_acc << kItemShift, &slot[0], sm);
       } else {
         etc -= (double)scout;
-        // Work items for the next level are emitted only for frontiers whose
-        // edge count is small; a large one is all but certain to hand over to
-        // bottom-up (which needs only the bitmap), else the bitmap is converted.
+        // The next frontier list is emitted only when this frontier's edge count
+        // is small; a large one is all but certain to hand over to bottom-up
+        // (which needs only the bitmap), else the bitmap is converted.
         const bool emit = (double)scout < p.emit_limit;
-        items_valid = emit;
-        td_step(p, sm.cbuf[threadIdx.x >> 5], items_in, nitems, items_out, fnext, slot, dnext,
-                emit, scout_acc, claims_acc);
+        list_valid = emit;
+        td_step(p, sm.cbuf[threadIdx.x >> 5], qv_in, qp_in, nq, nu, qv_out, qp_out, fnext, slot,
+                dnext, emit, scout_acc, claims_acc);
         block_add(scout_acc, &slot[1], sm);
         if (!emit) block_add(claims_acc << kItemShift, &slot[0], sm);
       }
@@ -498,26 +511,32 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
           bu = false;
           frontier = awake;
           scout = 1;
-          items_valid = false;
+          list_valid = false;
         }
       } else {
         frontier = claims;
         scout = ld_volatile(&slot[1]);
-        nitems = packed & kItemMask;
-        uint64_t* t = items_in;
-        items_in = items_out;
-        items_out = t;
+        nq = claims;
+        nu = packed & kItemMask;
+        uint32_t* tv = qv_in;
+        qv_in = qv_out;
+        qv_out = tv;
+        uint64_t* tp = qp_in;
+        qp_in = qp_out;
+        qp_out = tp;
       }
       if (!bu) {
         if (frontier == 0) break;
         if (!p.top_down_only && (double)scout > etc / p.alpha) {
           bu = true;
           awake = frontier;
-        } else if (!items_valid) {
+        } else if (!list_valid) {
           unsigned long long* cslot = p.ctr + 16 + (L & 1);
-          convert_step(p, F[L % 3], items_in, cslot);
+          convert_step(p, F[L % 3], qv_in, qp_in, cslot);
           grid_sync(p.bar);
-          nitems = ld_volatile(cslot);
+          const unsigned long long cp = ld_volatile(cslot);
+          nq = cp >> kItemShift;
+          nu = cp & kItemMask;
         }
       }
     }
@@ -574,9 +593,11 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   S.fb0.alloc(words);
   S.fb1.alloc(words);
   S.fb2.alloc(words);
-  const uint64_t cap = L.nc + L.ecore / kTdChunk + 2;
-  S.items0.alloc(cap);
-  S.items1.alloc(cap);
+  const uint64_t cap = L.nc + 2;
+  S.qv0.alloc(cap);
+  S.qv1.alloc(cap);
+  S.qp0.alloc(cap);
+  S.qp1.alloc(cap);
   S.ctr.alloc(32);
   S.bar.alloc(1);
   ETB_CUDA(cudaMemsetAsync(S.bar.get(), 0, 8, s));
@@ -622,8 +643,10 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.fb0 = S.fb0.get();
   p.fb1 = S.fb1.get();
   p.fb2 = S.fb2.get();
-  p.items0 = S.items0.get();
-  p.items1 = S.items1.get();
+  p.qv0 = S.qv0.get();
+  p.qv1 = S.qv1.get();
+  p.qp0 = S.qp0.get();
+  p.qp1 = S.qp1.get();
   p.ctr = S.ctr.get();
   p.bar = S.bar.get();
   p.depth = S.depth.get();

@@ -27,8 +27,10 @@ struct BfsParams {
   uint32_t* fb0;
   uint32_t* fb1;
   uint32_t* fb2;
-  uint64_t* items0;
-  uint64_t* items1;
+  uint32_t* qv0;  // frontier lists (vertex ids) ...
+  uint32_t* qv1;
+  uint64_t* qp0;  // ... and the exclusive prefix of their row-chunk counts
+  uint64_t* qp1;
   unsigned long long* ctr;  // 4 level slots x 4 + conversion counters
   unsigned long long* bar;  // grid barrier counter (monotonic)
   // outputs (relaid ids, all n vertices)
@@ -53,7 +55,8 @@ struct BfsParams {
 struct BfsState {
   uint64_t n = 0;
   DevBuf<uint32_t> visited, fb0, fb1, fb2;
-  DevBuf<uint64_t> items0, items1;
+  DevBuf<uint32_t> qv0, qv1;
+  DevBuf<uint64_t> qp0, qp1;
   DevBuf<unsigned long long> ctr, bar;
   DevBuf<int32_t> depth;
   DevBuf<uint32_t> parent;
