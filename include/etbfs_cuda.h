@@ -150,8 +150,9 @@ int etb_bfs(etb_layout* L, uint64_t start, const etb_bfs_options* opts, int32_t*
  * depth (n i32). The BfsTree content at half the bytes of etb_bfs. */
 int etb_bfs_compact(etb_layout* L, uint64_t start, const etb_bfs_options* opts,
                     int32_t* depth_out, uint32_t* parent_out);
-/* Device pointers to the last result (n entries each, relaid ids). */
-int etb_result_device_ptrs(etb_layout* L, int32_t** depth, uint32_t** parent);
+/* Device pointer to the last result: n interleaved {depth (i32, -1 unreached),
+ * parent (u32, UINT32_MAX unreached)} pairs, relaid ids. */
+int etb_result_device_ptr(etb_layout* L, uint32_t** dp);
 /* Copy the last result to host as compact i32 depth / u32 parent (UINT32_MAX unreached). */
 int etb_result_download(etb_layout* L, int32_t* depth, uint32_t* parent);
 /* ½ Σ full degree over reached vertices of the last result (validate.cpp:151-156). */

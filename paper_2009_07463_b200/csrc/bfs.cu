@@ -36,6 +36,7 @@ constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down item
 constexpr int kCbuf = 2 * kTdChunk;  // staged claims per warp
 constexpr int kBuU = 4;              // visited words per warp per bottom-up iteration
+constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab
 
 struct Smem {
   uint64_t cbuf[kWarps][kCbuf];  // (nchunks << 32) | vertex
@@ -179,12 +180,16 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, 
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
   const unsigned lt = (1u << lane) - 1;
-  const uint64_t per = (nu + nw - 1) / nw;
-  const uint64_t u0 = gw * per, u1 = min(nu, u0 + per);
+  // Chunks are handed out in batches of kGrab: first one static batch per
+  // warp, then (only when there is more work than that) from a per-level
+  // counter, so warps that draw cheap chunks keep pulling instead of idling at
+  // the barrier while others finish expensive ones.
+  const uint64_t static_units = nw * kGrab;
   uint32_t ncl = 0;
-  if (u0 < u1) {
-    uint64_t i = find_vertex(qp, nq, u0);
-    for (uint64_t unit = u0; unit < u1; ++unit) {
+  for (uint64_t g0 = gw * kGrab; g0 < nu;) {
+    const uint64_t g1 = min(nu, g0 + kGrab);
+    uint64_t i = find_vertex(qp, nq, g0);
+    for (uint64_t unit = g0; unit < g1; ++unit) {
       while (i + 1 < nq && qp[i + 1] <= unit) ++i;
       const uint32_t u = qv[i];
       const uint64_t beg = p.crow[u] + (unit - qp[i]) * kTdChunk;
@@ -208,8 +213,7 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, 
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
         if (cl[j]) {
-          p.depth[w[j]] = dnext;
-          p.parent[w[j]] = u;
+          p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u);
           atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
           meta[j] = p.cmeta[w[j]];
         }
@@ -242,6 +246,10 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, 
         __syncwarp();
       }
     }
+    if (nu <= static_units) break;
+    unsigned long long next = 0;
+    if (lane == 0) next = static_units + atomicAdd(&slot[2], (unsigned long long)kGrab);
+    g0 = __shfl_sync(0xffffffffu, next, 0);
   }
   if (ncl) flush_claims(cbuf, ncl, qv_out, qp_out, slot);
   __syncwarp();
@@ -295,8 +303,7 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
       else hit = scan_row(p, fcur, v, par);
     }
     if (hit) {
-      p.depth[v] = dnext;
-      p.parent[v] = par;
+      p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
       atomicOr(&p.visited[v >> 5], 1u << (v & 31));
       atomicOr(&fnext[v >> 5], 1u << (v & 31));
       ++claims_acc;
@@ -322,8 +329,7 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
       }
     }
     if (lane == 0 && par != kNone32) {
-      p.depth[v] = dnext;
-      p.parent[v] = par;
+      p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
       atomicOr(&p.visited[v >> 5], 1u << (v & 31));
       atomicOr(&fnext[v >> 5], 1u << (v & 31));
       ++claims_acc;
@@ -360,8 +366,7 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
       const uint32_t v = static_cast<uint32_t>((w0 + k) * 32 + lane);
       const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
       if (hit[k]) {
-        p.depth[v] = dnext;
-        p.parent[v] = f[k];
+        p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), f[k]);
       }
       if (lane == 0 && m) {
         p.visited[w0 + k] = vis[k] | m;
@@ -448,8 +453,7 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
     if (tid == 0) {
       p.qv0[0] = start;
       p.qp0[0] = 0;
-      p.depth[start] = p.base_depth;
-      p.parent[start] = p.start_parent;
+      p.dp[start] = make_uint2(static_cast<uint32_t>(p.base_depth), p.start_parent);
     }
   }
   grid_sync(p.bar);
@@ -476,6 +480,7 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
       if (tid == 0) {
         p.ctr[((L + 2) & 3) * 4 + 0] = 0;
         p.ctr[((L + 2) & 3) * 4 + 1] = 0;
+        p.ctr[((L + 2) & 3) * 4 + 2] = 0;
         p.ctr[16 + ((L + 1) & 1)] = 0;
         if (p.trace && L < 255) p.trace[L] = bu ? 'b' : 't';
       }
@@ -547,8 +552,7 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
   for (uint64_t wi = tid; wi < p.nwords; wi += nthreads) {
     for (uint32_t un = ~p.visited[wi]; un; un &= un - 1) {  // padding bits are set
       const uint64_t v = wi * 32 + __ffs(un) - 1;
-      p.depth[v] = -1;
-      p.parent[v] = kNone32;
+      p.dp[v] = make_uint2(kNone32, kNone32);
     }
   }
   for (uint64_t t0 = tid; t0 < p.nt; t0 += 4 * nthreads) {
@@ -567,18 +571,15 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
       const uint64_t t = t0 + k * nthreads;
       const uint32_t tv = static_cast<uint32_t>(p.nc + t);
       if (vis[k]) {
-        p.depth[tv] = __ldcg(&p.depth[a[k]]) + static_cast<int32_t>(p.tdepth[t]);
-        p.parent[tv] = p.tsrc[t];
+        p.dp[tv] = make_uint2(__ldcg(&p.dp[a[k]].x) + p.tdepth[t], p.tsrc[t]);
       } else {
-        p.depth[tv] = -1;
-        p.parent[tv] = kNone32;
+        p.dp[tv] = make_uint2(kNone32, kNone32);
       }
     }
   }
   for (uint64_t i = tid; i < p.npatch; i += nthreads) {
     const uint32_t v = p.patch[3 * i];
-    p.depth[v] = static_cast<int32_t>(p.patch[3 * i + 1]);
-    p.parent[v] = p.patch[3 * i + 2];
+    p.dp[v] = make_uint2(p.patch[3 * i + 1], p.patch[3 * i + 2]);
   }
   stamp(p, 511);
 }
@@ -601,12 +602,10 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   S.ctr.alloc(32);
   S.bar.alloc(1);
   ETB_CUDA(cudaMemsetAsync(S.bar.get(), 0, 8, s));
-  S.depth.alloc(n ? n : 1);
-  S.parent.alloc(n ? n : 1);
+  S.dp.alloc(n ? n : 1);
   // Isolated vertices stay unreached unless they are the start; everything
   // else is rewritten by every traversal.
-  ETB_CUDA(cudaMemsetAsync(S.depth.get(), 0xFF, (n ? n : 1) * 4, s));
-  ETB_CUDA(cudaMemsetAsync(S.parent.get(), 0xFF, (n ? n : 1) * 4, s));
+  ETB_CUDA(cudaMemsetAsync(S.dp.get(), 0xFF, (n ? n : 1) * 8, s));
   S.trace.alloc(256);
   S.level_claims.alloc(512);
   S.nlevels.alloc(1);
@@ -649,8 +648,7 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.qp1 = S.qp1.get();
   p.ctr = S.ctr.get();
   p.bar = S.bar.get();
-  p.depth = S.depth.get();
-  p.parent = S.parent.get();
+  p.dp = S.dp.get();
   p.patch = S.patch.get();
   p.npatch = 0;
   p.edges_to_check = static_cast<double>(L.ecore);

@@ -34,8 +34,7 @@ struct BfsParams {
   unsigned long long* ctr;  // 4 level slots x 4 + conversion counters
   unsigned long long* bar;  // grid barrier counter (monotonic)
   // outputs (relaid ids, all n vertices)
-  int32_t* depth;
-  uint32_t* parent;
+  uint2* dp;  // {depth (i32 bits, -1 unreached), parent (kNone32 unreached)} per vertex
   // per call
   uint32_t start;         // core vertex the core BFS starts at, kNone32 for none
   int32_t base_depth;     // depth of `start`
@@ -58,8 +57,9 @@ struct BfsState {
   DevBuf<uint32_t> qv0, qv1;
   DevBuf<uint64_t> qp0, qp1;
   DevBuf<unsigned long long> ctr, bar;
-  DevBuf<int32_t> depth;
-  DevBuf<uint32_t> parent;
+  DevBuf<uint2> dp;          // interleaved result: one 8-byte store per claim
+  DevBuf<int32_t> tmp_depth;  // de-interleaved staging for host downloads
+  DevBuf<uint32_t> tmp_parent;
   DevBuf<char> trace;
   DevBuf<unsigned long long> level_claims;
   DevBuf<uint32_t> nlevels;

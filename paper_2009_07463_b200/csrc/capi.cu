@@ -157,14 +157,46 @@ void collect_stats(etb_layout* h, etb_bfs_stats* st) {
   for (uint32_t i = 0; i < nl && i < 255; ++i) st->bottom_up_levels += st->direction_trace[i] == 'b';
 }
 
-__global__ void te_kernel(const int32_t* depth, const uint32_t* degn, uint64_t n,
+__global__ void te_kernel(const uint2* dp, const uint32_t* degn, uint64_t n,
                           unsigned long long* out) {
   unsigned long long acc = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
-    if (depth[i] >= 0) acc += degn[i];
+    if (static_cast<int32_t>(dp[i].x) >= 0) acc += degn[i];
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+// Interleaved {depth, parent} -> separate arrays (either may be null).
+__global__ void split_kernel(const uint2* dp, uint64_t n, int32_t* depth, uint32_t* parent,
+                             uint64_t* parent64) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 e = dp[i];
+    if (depth) depth[i] = static_cast<int32_t>(e.x);
+    if (parent) parent[i] = e.y;
+    if (parent64) parent64[i] = e.y == etb::kNone32 ? ~0ull : e.y;
+  }
+}
+
+// Split the last result on the device and copy the requested parts to host.
+void download_result(etb_layout* h, int32_t* depth, uint32_t* parent, uint64_t* parent64) {
+  const uint64_t n = h->L.n;
+  if (!n || (!depth && !parent && !parent64)) return;
+  auto& S = h->S;
+  cudaStream_t s = h->stream;
+  if (depth && S.tmp_depth.size() < n) S.tmp_depth.alloc(n);
+  if (parent && S.tmp_parent.size() < n) S.tmp_parent.alloc(n);
+  etb::DevBuf<uint64_t> p64;
+  if (parent64) p64.alloc(n);
+  split_kernel<<<etb::grid_for(n, 256), 256, 0, s>>>(S.dp.get(), n, depth ? S.tmp_depth.get() : nullptr,
+                                                     parent ? S.tmp_parent.get() : nullptr,
+                                                     parent64 ? p64.get() : nullptr);
+  ETB_LAUNCH_CHECK();
+  if (depth) ETB_CUDA(cudaMemcpyAsync(depth, S.tmp_depth.get(), n * 4, cudaMemcpyDeviceToHost, s));
+  if (parent) ETB_CUDA(cudaMemcpyAsync(parent, S.tmp_parent.get(), n * 4, cudaMemcpyDeviceToHost, s));
+  if (parent64) ETB_CUDA(cudaMemcpyAsync(parent64, p64.get(), n * 8, cudaMemcpyDeviceToHost, s));
+  ETB_CUDA(cudaStreamSynchronize(s));
 }
 
 __global__ void widen_kernel(const uint32_t* in, uint64_t n, uint64_t* out) {
@@ -473,12 +505,7 @@ int etb_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* opts, int32_t*
     need(h, "et_bfs");
     ETB_CUDA(cudaSetDevice(h->device));
     run_bfs(h, start, opts, stats != nullptr);
-    const uint64_t n = h->L.n;
-    if (depth_out && n)
-      ETB_CUDA(cudaMemcpyAsync(depth_out, h->S.depth.get(), n * 4, cudaMemcpyDeviceToHost,
-                               h->stream));
-    if (parent_out) download_widened(h->S.parent.get(), n, parent_out, h->stream);
-    ETB_CUDA(cudaStreamSynchronize(h->stream));
+    download_result(h, depth_out, nullptr, parent_out);
     if (stats) collect_stats(h, stats);
   });
 }
@@ -489,21 +516,15 @@ int etb_bfs_compact(etb_layout* h, uint64_t start, const etb_bfs_options* opts, 
     need(h, "et_bfs");
     ETB_CUDA(cudaSetDevice(h->device));
     run_bfs(h, start, opts, false);
-    const uint64_t n = h->L.n;
-    if (parent && n)
-      ETB_CUDA(cudaMemcpyAsync(parent, h->S.parent.get(), n * 4, cudaMemcpyDeviceToHost,
-                               h->stream));
-    if (depth && n)
-      ETB_CUDA(cudaMemcpyAsync(depth, h->S.depth.get(), n * 4, cudaMemcpyDeviceToHost, h->stream));
-    ETB_CUDA(cudaStreamSynchronize(h->stream));
+    download_result(h, depth, parent, nullptr);
   });
 }
 
-int etb_result_device_ptrs(etb_layout* h, int32_t** depth, uint32_t** parent) {
+int etb_result_device_ptr(etb_layout* h, uint32_t** dp) {
   return guarded([&] {
-    need(h, "etb_result_device_ptrs");
-    if (depth) *depth = h->S.depth.get();
-    if (parent) *parent = h->S.parent.get();
+    need(h, "etb_result_device_ptr");
+    need(dp, "etb_result_device_ptr");
+    *dp = reinterpret_cast<uint32_t*>(h->S.dp.get());
   });
 }
 
@@ -511,13 +532,7 @@ int etb_result_download(etb_layout* h, int32_t* depth, uint32_t* parent) {
   return guarded([&] {
     need(h, "etb_result_download");
     ETB_CUDA(cudaSetDevice(h->device));
-    const uint64_t n = h->L.n;
-    if (depth && n)
-      ETB_CUDA(cudaMemcpyAsync(depth, h->S.depth.get(), n * 4, cudaMemcpyDeviceToHost, h->stream));
-    if (parent && n)
-      ETB_CUDA(cudaMemcpyAsync(parent, h->S.parent.get(), n * 4, cudaMemcpyDeviceToHost,
-                               h->stream));
-    ETB_CUDA(cudaStreamSynchronize(h->stream));
+    download_result(h, depth, parent, nullptr);
   });
 }
 
@@ -528,7 +543,7 @@ int etb_result_traversed_edges(etb_layout* h, uint64_t* te) {
     ETB_CUDA(cudaSetDevice(h->device));
     etb::DevBuf<unsigned long long> acc(1);
     ETB_CUDA(cudaMemsetAsync(acc.get(), 0, 8, h->stream));
-    te_kernel<<<etb::grid_for(h->L.n, 256), 256, 0, h->stream>>>(h->S.depth.get(), h->L.degn.get(),
+    te_kernel<<<etb::grid_for(h->L.n, 256), 256, 0, h->stream>>>(h->S.dp.get(), h->L.degn.get(),
                                                                   h->L.n, acc.get());
     ETB_LAUNCH_CHECK();
     *te = etb::read_u64(reinterpret_cast<uint64_t*>(acc.get()), h->stream) / 2;

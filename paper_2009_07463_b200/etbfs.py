@@ -156,7 +156,7 @@ def lib() -> C.CDLL:
     sig("etb_bfs_device", vp, u64, C.POINTER(_BfsOptions), C.POINTER(_BfsStats))
     sig("etb_bfs", vp, u64, C.POINTER(_BfsOptions), vp, vp, C.POINTER(_BfsStats))
     sig("etb_bfs_compact", vp, u64, C.POINTER(_BfsOptions), vp, vp)
-    sig("etb_result_device_ptrs", vp, C.POINTER(vp), C.POINTER(vp))
+    sig("etb_result_device_ptr", vp, C.POINTER(vp))
     sig("etb_result_download", vp, vp, vp)
     sig("etb_result_traversed_edges", vp, P64)
     sig("etb_host_register", vp, u64)
