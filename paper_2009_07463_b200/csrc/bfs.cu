@@ -180,14 +180,13 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, 
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
   const unsigned lt = (1u << lane) - 1;
-  // Chunks are handed out in batches of kGrab: first one static batch per
-  // warp, then (only when there is more work than that) from a per-level
-  // counter, so warps that draw cheap chunks keep pulling instead of idling at
-  // the barrier while others finish expensive ones.
-  const uint64_t static_units = nw * kGrab;
+  // Every warp first takes one chunk (so small levels spread over all warps);
+  // when there is more work than that, further chunks are pulled in batches
+  // of kGrab from a per-level counter, so warps that draw cheap chunks keep
+  // working instead of idling at the barrier behind expensive ones.
   uint32_t ncl = 0;
-  for (uint64_t g0 = gw * kGrab; g0 < nu;) {
-    const uint64_t g1 = min(nu, g0 + kGrab);
+  for (uint64_t g0 = gw, gn = 1; g0 < nu;) {
+    const uint64_t g1 = min(nu, g0 + gn);
     uint64_t i = find_vertex(qp, nq, g0);
     for (uint64_t unit = g0; unit < g1; ++unit) {
       while (i + 1 < nq && qp[i + 1] <= unit) ++i;
@@ -246,10 +245,11 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, 
         __syncwarp();
       }
     }
-    if (nu <= static_units) break;
+    if (nu <= nw) break;
     unsigned long long next = 0;
-    if (lane == 0) next = static_units + atomicAdd(&slot[2], (unsigned long long)kGrab);
+    if (lane == 0) next = nw + atomicAdd(&slot[2], (unsigned long long)kGrab);
     g0 = __shfl_sync(0xffffffffu, next, 0);
+    gn = kGrab;
   }
   if (ncl) flush_claims(cbuf, ncl, qv_out, qp_out, slot);
   __syncwarp();
