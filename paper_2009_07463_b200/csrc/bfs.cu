@@ -34,14 +34,34 @@ constexpr int kItemShift = 36;
 constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 
 constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down item
-constexpr int kCbuf = 2 * kTdChunk;  // staged claims per warp
+constexpr int kCbuf = 2 * kTdChunk;  // staged claims per warp (u32 vertex ids)
 constexpr int kBuU = 4;              // visited words per warp per bottom-up iteration
 constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab
 
+// Hot prefix of a bitmap staged in smem per CTA: relaid core ids are sorted by
+// degree, so the first ~0.5M ids (the hubs) absorb most probes — the first
+// neighbour a bottom-up vertex tries, and most top-down edge endpoints.
+constexpr int kHotWords = 16384;  // 64 KB = 524,288 vertices
+
 struct Smem {
-  uint64_t cbuf[kWarps][kCbuf];  // (nchunks << 32) | vertex
+  uint32_t hot[kHotWords];
+  uint32_t cbuf[kWarps][kCbuf];  // staged claims (top-down) / deferred misses (bottom-up)
   unsigned long long red[kWarps];
 };
+
+struct Hot {
+  const uint32_t* words;  // smem copy of the bitmap's first `limit` bits
+  uint32_t* mut;          // same, writable (top-down marks its own claims)
+  uint32_t limit;         // 0 = nothing staged
+};
+
+__device__ __forceinline__ uint32_t probe_word(const Hot& h, const uint32_t* bm, uint32_t v) {
+  return v < h.limit ? h.words[v >> 5] : bm[v >> 5];
+}
+
+__device__ __forceinline__ bool probe_bit(const Hot& h, const uint32_t* bm, uint32_t v) {
+  return (probe_word(h, bm, v) >> (v & 31)) & 1u;
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -127,11 +147,15 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
 // staged batch: (claims << 36) | chunks returns both positions at once.
 
 // Append the staged claims (entries (nchunks << 32) | vertex) to the next list.
-__device__ void flush_claims(const uint64_t* cbuf, uint32_t ncl, uint32_t* qv_out,
-                             uint64_t* qp_out, unsigned long long* slot) {
+__device__ __forceinline__ uint32_t row_chunks(const BfsParams& p, uint32_t v) {
+  return (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
+}
+
+__device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, uint32_t ncl,
+                             uint32_t* qv_out, uint64_t* qp_out, unsigned long long* slot) {
   const unsigned lane = threadIdx.x & 31;
   unsigned long long nch = 0;
-  for (uint32_t i = lane; i < ncl; i += 32) nch += cbuf[i] >> 32;
+  for (uint32_t i = lane; i < ncl; i += 32) nch += row_chunks(p, cbuf[i]);
   nch = warp_sum(nch);
   unsigned long long old = 0;
   if (lane == 0) old = atomicAdd(slot, ((unsigned long long)ncl << kItemShift) | nch);
@@ -139,11 +163,11 @@ __device__ void flush_claims(const uint64_t* cbuf, uint32_t ncl, uint32_t* qv_ou
   uint64_t vpos = old >> kItemShift, cpos = old & kItemMask;
   for (uint32_t i0 = 0; i0 < ncl; i0 += 32) {
     const uint32_t i = i0 + lane;
-    const uint64_t e = i < ncl ? cbuf[i] : 0ull;
-    const uint32_t c = static_cast<uint32_t>(e >> 32);
+    const uint32_t v = i < ncl ? cbuf[i] : 0u;
+    const uint32_t c = i < ncl ? row_chunks(p, v) : 0u;
     const uint32_t incl = warp_incl_scan(c);
     if (i < ncl) {
-      qv_out[vpos + i] = static_cast<uint32_t>(e);
+      qv_out[vpos + i] = v;
       qp_out[vpos + i] = cpos + incl - c;
     }
     cpos += __shfl_sync(0xffffffffu, incl, 31);
@@ -172,7 +196,8 @@ __device__ uint64_t find_vertex(const uint64_t* qp, uint64_t nq, uint64_t unit) 
 // Top-down step (bfs.cpp:61-86). Each lane owns 8 edges of the warp's current
 // chunk; their column loads, visited probes and claim atomics are issued
 // before any result is consumed.
-__device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, const uint64_t* qp,
+__device__ void td_step(const BfsParams& p, const Hot& hot, uint32_t* cbuf, const uint32_t* qv,
+                        const uint64_t* qp,
                         uint64_t nq, uint64_t nu, uint32_t* qv_out, uint64_t* qp_out,
                         uint32_t* fnext, unsigned long long* slot, int32_t dnext, bool emit,
                         unsigned long long& scout_acc, unsigned long long& claims_acc) {
@@ -201,12 +226,15 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, 
         w[j] = e < end ? p.ccol[e] : kNone32;
       }
 #pragma unroll
-      for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
+      for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? probe_word(hot, p.visited, w[j]) : ~0u;
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
         const uint32_t bit = 1u << (w[j] & 31);
         cl[j] = false;
-        if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
+        if (!(vw[j] & bit)) {
+          cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
+          if (w[j] < hot.limit) atomicOr(&hot.mut[w[j] >> 5], bit);  // this CTA skips it now
+        }
       }
       uint2 meta[kEpl];
 #pragma unroll
@@ -233,14 +261,13 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, 
         const unsigned m = __ballot_sync(0xffffffffu, cl[j]);
         if (cl[j]) {
           scout_acc += meta[j].y;
-          const uint64_t nch = (meta[j].x + kTdChunk - 1) / kTdChunk;
-          cbuf[ncl + __popc(m & lt)] = (nch << 32) | w[j];
+          cbuf[ncl + __popc(m & lt)] = w[j];
         }
         ncl += __popc(m);
       }
       __syncwarp();
       if (ncl > kCbuf - kTdChunk) {
-        flush_claims(cbuf, ncl, qv_out, qp_out, slot);
+        flush_claims(p, cbuf, ncl, qv_out, qp_out, slot);
         ncl = 0;
         __syncwarp();
       }
@@ -251,12 +278,12 @@ __device__ void td_step(const BfsParams& p, uint64_t* cbuf, const uint32_t* qv, 
     g0 = __shfl_sync(0xffffffffu, next, 0);
     gn = kGrab;
   }
-  if (ncl) flush_claims(cbuf, ncl, qv_out, qp_out, slot);
+  if (ncl) flush_claims(p, cbuf, ncl, qv_out, qp_out, slot);
   __syncwarp();
 }
 
-__device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcur, uint32_t v,
-                                         uint32_t& par) {
+__device__ __forceinline__ bool scan_row(const BfsParams& p, const Hot& hot, const uint32_t* fcur,
+                                         uint32_t v, uint32_t& par) {
   // The first (highest-degree) neighbour was already probed; the rest of the
   // row is probed four at a time (independent loads) with early exit.
   const uint64_t re = p.crow[v + 1];
@@ -266,7 +293,7 @@ __device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcu
 #pragma unroll
     for (int j = 0; j < 4; ++j) x[j] = e + j < re ? p.ccol[e + j] : kNone32;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = x[j] != kNone32 && test_bit(fcur, x[j]);
+    for (int j = 0; j < 4; ++j) b[j] = x[j] != kNone32 && probe_bit(hot, fcur, x[j]);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (b[j]) {
@@ -284,10 +311,11 @@ __device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcu
 // deferred to a per-warp smem list and scanned afterwards, one lane per vertex
 // (rows of <= kLaneScan core neighbours) or the whole warp per vertex (longer
 // rows), so one long row no longer stalls 31 idle lanes.
-constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (reuses the claim buffer)
+constexpr int kMissCap = kCbuf;  // u32 entries per warp (reuses the claim buffer)
 constexpr uint32_t kLaneScan = 64;
 
-__device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext,
+__device__ void resolve_misses(const BfsParams& p, const Hot& hot, const uint32_t* fcur,
+                               uint32_t* fnext,
                                uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
                                unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31;
@@ -300,7 +328,7 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
     uint32_t par = 0;
     if (v != kNone32) {
       if (p.cmeta[v].x > kLaneScan) lng = true;
-      else hit = scan_row(p, fcur, v, par);
+      else hit = scan_row(p, hot, fcur, v, par);
     }
     if (hit) {
       p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
@@ -322,7 +350,7 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
     for (uint64_t e0 = rb; e0 < re; e0 += 32) {
       const uint64_t e = e0 + lane;
       const uint32_t x = e < re ? p.ccol[e] : kNone32;
-      const unsigned m = __ballot_sync(0xffffffffu, x != kNone32 && test_bit(fcur, x));
+      const unsigned m = __ballot_sync(0xffffffffu, x != kNone32 && probe_bit(hot, fcur, x));
       if (m) {
         par = __shfl_sync(0xffffffffu, x, __ffs(m) - 1);
         break;
@@ -338,7 +366,7 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
   __syncwarp();
 }
 
-__device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur,
+__device__ void bu_step(const BfsParams& p, const Hot& hot, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
@@ -360,7 +388,7 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
       f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[(w0 + k) * 32 + lane];
     bool hit[kBuU];
 #pragma unroll
-    for (int k = 0; k < kBuU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
+    for (int k = 0; k < kBuU; ++k) hit[k] = f[k] != kNone32 && probe_bit(hot, fcur, f[k]);
 #pragma unroll
     for (int k = 0; k < kBuU; ++k) {
       const uint32_t v = static_cast<uint32_t>((w0 + k) * 32 + lane);
@@ -379,11 +407,11 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
       nmiss += __popc(mm);
     }
     if (nmiss > kMissCap - 32 * kBuU) {
-      resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
+      resolve_misses(p, hot, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
       nmiss = 0;
     }
   }
-  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
+  if (nmiss) resolve_misses(p, hot, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
 }
 
 // Frontier bitmap -> frontier list (when a top-down level follows one that did
@@ -463,6 +491,7 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
   uint32_t L = 0;
   if (run_core) {
     uint32_t* F[3] = {p.fb0, p.fb1, p.fb2};
+    const uint64_t nw_total = (uint64_t)gridDim.x * kWarps;
     uint32_t* qv_in = p.qv0;
     uint32_t* qv_out = p.qv1;
     uint64_t* qp_in = p.qp0;
@@ -487,10 +516,20 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
       const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
       unsigned long long claims_acc = 0, scout_acc = 0;
       bool list_valid = true;
+      // Stage the hot prefix of the bitmap this level probes: the frontier for
+      // bottom-up (read-only this level, so exact), visited for a large
+      // top-down level (a stale 0 only costs one global atomic that fails).
+      Hot hot{sm.hot, sm.hot, 0u};
+      if (bu || nu > nw_total) {
+        const uint32_t* src = bu ? fcur : p.visited;
+        const uint32_t hw = min(p.nwords, (uint32_t)kHotWords);
+        for (uint32_t i = threadIdx.x; i < hw; i += blockDim.x) sm.hot[i] = src[i];
+        hot.limit = hw * 32u;
+        __syncthreads();
+      }
       if (bu) {
         prev = awake;
-        bu_step(p, reinterpret_cast<uint32_t*>(sm.cbuf[threadIdx.x >> 5]), fcur, fnext, dnext,
-                claims_acc);
+        bu_step(p, hot, sm.cbuf[threadIdx.x >> 5], fcur, fnext, dnext, claims_acc);
         block_add(claims_acc << kItemShift, &slot[0], sm);
       } else {
         etc -= (double)scout;
@@ -499,7 +538,7 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
         // (which needs only the bitmap), else the bitmap is converted.
         const bool emit = (double)scout < p.emit_limit;
         list_valid = emit;
-        td_step(p, sm.cbuf[threadIdx.x >> 5], qv_in, qp_in, nq, nu, qv_out, qp_out, fnext, slot,
+        td_step(p, hot, sm.cbuf[threadIdx.x >> 5], qv_in, qp_in, nq, nu, qv_out, qp_out, fnext, slot,
                 dnext, emit, scout_acc, claims_acc);
         block_add(scout_acc, &slot[1], sm);
         if (!emit) block_add(claims_acc << kItemShift, &slot[0], sm);
