@@ -41,10 +41,9 @@ constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab
 // Hot prefix of a bitmap staged in smem per CTA: relaid core ids are sorted by
 // degree, so the first ~0.5M ids (the hubs) absorb most probes — the first
 // neighbour a bottom-up vertex tries, and most top-down edge endpoints.
-constexpr int kHotWords = 16384;  // 64 KB = 524,288 vertices
+constexpr int kHotWords = 0;  // staging disabled: measured slower than L1 (it shrinks L1)
 
 struct Smem {
-  uint32_t hot[kHotWords];
   uint32_t cbuf[kWarps][kCbuf];  // staged claims (top-down) / deferred misses (bottom-up)
   unsigned long long red[kWarps];
 };
@@ -491,7 +490,6 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
   uint32_t L = 0;
   if (run_core) {
     uint32_t* F[3] = {p.fb0, p.fb1, p.fb2};
-    const uint64_t nw_total = (uint64_t)gridDim.x * kWarps;
     uint32_t* qv_in = p.qv0;
     uint32_t* qv_out = p.qv1;
     uint64_t* qp_in = p.qp0;
@@ -516,17 +514,9 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
       const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
       unsigned long long claims_acc = 0, scout_acc = 0;
       bool list_valid = true;
-      // Stage the hot prefix of the bitmap this level probes: the frontier for
-      // bottom-up (read-only this level, so exact), visited for a large
-      // top-down level (a stale 0 only costs one global atomic that fails).
-      Hot hot{sm.hot, sm.hot, 0u};
-      if (bu || nu > nw_total) {
-        const uint32_t* src = bu ? fcur : p.visited;
-        const uint32_t hw = min(p.nwords, (uint32_t)kHotWords);
-        for (uint32_t i = threadIdx.x; i < hw; i += blockDim.x) sm.hot[i] = src[i];
-        hot.limit = hw * 32u;
-        __syncthreads();
-      }
+      // (A smem copy of the bitmap's hot prefix was tried and measured slower:
+      // the 64 KB it takes comes out of L1, which already caches those lines.)
+      const Hot hot{nullptr, nullptr, 0u};
       if (bu) {
         prev = awake;
         bu_step(p, hot, sm.cbuf[threadIdx.x >> 5], fcur, fnext, dnext, claims_acc);
