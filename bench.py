@@ -246,10 +246,51 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, roots[: args.cpu_roots])
+    if world == 1 and args.secondary_scale and args.secondary_scale != args.scale:
+        del cg, g
+        out["secondary"] = measure_secondary(args.secondary_scale, args.edgefactor, args.mh,
+                                             args.steps, args.warmup)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def measure_secondary(scale, ef, mh, steps, warmup):
+    """The same timed protocol at BASELINE configs[3]'s scale (s26): HM GTEPS and
+    the HBM-roofline fraction the north_star target is quoted on."""
+    import paper_2009_07463_b200 as eb
+    from paper_2009_07463_b200 import etbfs as E
+    t0 = time.perf_counter()
+    g = eb.generate_graph(scale=scale, edgefactor=ef, seed=1)
+    cg = eb.relayout_csr(g, mh=mh)
+    prep = time.perf_counter() - t0
+    roots = select_roots_from_degrees(g.degrees(), NROOTS, 1)
+    starts = cg.old2new[roots.astype(np.int64)]
+    te = np.empty(len(starts), np.uint64)
+    for i, s in enumerate(starts):
+        E.bfs_device(cg, int(s))
+        te[i] = E.result_traversed_edges(cg)
+    ms, kms = E.time_roots(cg, np.tile(starts, steps), warmup=warmup * len(starts), flush_l2=True)
+    te_rep = np.tile(te, steps).astype(np.float64)
+    hm, per = harmonic_gteps(te_rep, ms / 1e3)
+    peak, _ = measured_peak_hbm()
+    balg = b_alg(cg.core_vertex_count, cg.restricted_edge_count, cg.tree_vertex_count)
+    achieved = balg / (float(np.mean(kms)) / 1e3) / 1e9
+    roof = peak / (balg / float(te.max()))
+    return {"workload": f"kronecker-s{scale}-ef{ef}-seed1", "value": round(hm, 3), "unit": "GTEPS",
+            "ms_per_bfs_mean": round(float(np.mean(ms)), 4),
+            "min_gteps": round(float(per.min()), 3), "max_gteps": round(float(per.max()), 3),
+            "traversed_edges": int(te.max()), "core_vertices": int(cg.core_vertex_count),
+            "core_directed_edges": int(cg.restricted_edge_count),
+            "tree_vertices": int(cg.tree_vertex_count),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "algorithmic_bytes_per_bfs": int(balg),
+                         "bytes_per_te": round(balg / float(te.max()), 3),
+                         "roofline_gteps": round(roof, 1),
+                         "frac_of_roofline_gteps": round(hm / roof, 4)},
+            "preprocessing_s": round(prep, 3), "gpu_launches": int(len(ms))}
 
 
 def select_roots_from_degrees(deg, count, seed):
@@ -389,6 +430,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-roots", type=int, default=16)
     ap.add_argument("--ref-roots-per-step", type=int, default=4)
+    ap.add_argument("--secondary-scale", type=int, default=26,
+                    help="also time this scale (0 = off); reported under 'secondary'")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -594,16 +594,19 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) vis[k] = a[k] < kNone32 - 1 ? test_bit(p.visited, a[k]) : 0u;
+    // All loads of the 4 entries are issued before any store: the stores go to
+    // dp too, so the compiler would otherwise serialise load -> store pairs.
+    uint2 out[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t t = t0 + k * nthreads;
+      out[k] = make_uint2(kNone32, kNone32);
+      if (vis[k]) out[k] = make_uint2(__ldcg(&p.dp[a[k]].x) + p.tdepth[t], p.tsrc[t]);
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (a[k] == kNone32 - 1) continue;  // out of range or inside the start's tree
-      const uint64_t t = t0 + k * nthreads;
-      const uint32_t tv = static_cast<uint32_t>(p.nc + t);
-      if (vis[k]) {
-        p.dp[tv] = make_uint2(__ldcg(&p.dp[a[k]].x) + p.tdepth[t], p.tsrc[t]);
-      } else {
-        p.dp[tv] = make_uint2(kNone32, kNone32);
-      }
+      p.dp[p.nc + t0 + k * nthreads] = out[k];
     }
   }
   for (uint64_t i = tid; i < p.npatch; i += nthreads) {
