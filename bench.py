@@ -112,6 +112,16 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def captured_traffic(workload):
+    """DRAM bytes per launch of the BFS kernel from the committed ncu --set full
+    capture (profiles/traffic.json), or None when this workload was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)[workload]["mean"]
+    except Exception:
+        return None
+
+
 def b_alg(nc, ecore, ntree):
     """algorithmic bytes per BFS (relaid space, u32 core ids)."""
     return 4 * ecore + 8 * (nc + 1) + 8 * nc + 16 * ntree
@@ -220,7 +230,8 @@ def run_ours(args):
                    "parallelism": "replicas" if world > 1 else "1gpu",
                    "l2": "flushed between roots (2x L2 memset outside the timed events)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": captured_traffic(f"kronecker-s{args.scale}-ef{args.edgefactor}-seed1"),
                      "peak_source": peak_src, "algorithmic_bytes_per_bfs": int(balg),
                      "bytes_per_te": round(balg / float(te.max()), 3),
                      "roofline_gteps": round(roof_gteps, 1),
