@@ -23,10 +23,12 @@
 // CTAs (cooperative launch).
 #include <algorithm>
 
-#include "bfs.cuh"
+#include "bfs_dev.cuh"
 
 namespace etb {
 namespace {
+
+using namespace dev;
 
 constexpr int kBlock = 512;
 constexpr int kWarps = kBlock / 32;
@@ -38,74 +40,16 @@ constexpr int kCbuf = 2 * kTdChunk;  // staged claims per warp (u32 vertex ids)
 constexpr int kBuU = 4;              // visited words per warp per bottom-up iteration
 constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab
 
-// Hot prefix of a bitmap staged in smem per CTA: relaid core ids are sorted by
-// degree, so the first ~0.5M ids (the hubs) absorb most probes — the first
-// neighbour a bottom-up vertex tries, and most top-down edge endpoints.
-constexpr int kHotWords = 0;  // staging disabled: measured slower than L1 (it shrinks L1)
-
 struct Smem {
   uint32_t cbuf[kWarps][kCbuf];  // staged claims (top-down) / deferred misses (bottom-up)
   unsigned long long red[kWarps];
 };
-
-struct Hot {
-  const uint32_t* words;  // smem copy of the bitmap's first `limit` bits
-  uint32_t* mut;          // same, writable (top-down marks its own claims)
-  uint32_t limit;         // 0 = nothing staged
-};
-
-__device__ __forceinline__ uint32_t probe_word(const Hot& h, const uint32_t* bm, uint32_t v) {
-  return v < h.limit ? h.words[v >> 5] : bm[v >> 5];
-}
-
-__device__ __forceinline__ bool probe_bit(const Hot& h, const uint32_t* bm, uint32_t v) {
-  return (probe_word(h, bm, v) >> (v & 31)) & 1u;
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
-  return *reinterpret_cast<const volatile unsigned long long*>(p);
-}
-
-// Monotonic-counter grid barrier: every CTA adds 1; the barrier of a CTA that
-// saw value `old` completes at the next multiple of gridDim.x.
-__device__ void grid_sync(unsigned long long* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long nb = gridDim.x;
-    __threadfence();
-    const unsigned long long old = atomicAdd(bar, 1ull);
-    const unsigned long long target = (old / nb + 1) * nb;
-    const long long t0 = clock64();
-    while (ld_acquire(bar) < target) {
-      if (clock64() - t0 > 40000000000ll) __trap();  // ~20 s: never hang the GPU
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 // Phase timestamps for stats (block 0 / thread 0): [256] entry, [257] after
 // init, [258 + L] after level L, [511] end of the tree replay.
 __device__ __forceinline__ void stamp(const BfsParams& p, uint32_t slot) {
   if (p.level_claims && blockIdx.x == 0 && threadIdx.x == 0 && slot < 512)
     p.level_claims[slot] = gtimer();
-}
-
-__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
 }
 
 __device__ void block_add(unsigned long long v, unsigned long long* dst, Smem& sm) {
@@ -121,21 +65,8 @@ __device__ void block_add(unsigned long long v, unsigned long long* dst, Smem& s
   __syncthreads();
 }
 
-__device__ __forceinline__ bool test_bit(const uint32_t* bm, uint32_t v) {
-  return (bm[v >> 5] >> (v & 31)) & 1u;
-}
-
 __device__ __forceinline__ uint32_t nchunks(uint64_t d) {
   return static_cast<uint32_t>((d + kTdChunk - 1) / kTdChunk);
-}
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
-  const unsigned lane = threadIdx.x & 31;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  return x;
 }
 
 // Frontier list: vertex ids qv[0..nq) plus the exclusive prefix qp[] of their
@@ -173,29 +104,10 @@ __device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, uint32_t 
   }
 }
 
-// Index of the last list entry whose chunk prefix is <= unit (32-ary search).
-__device__ uint64_t find_vertex(const uint64_t* qp, uint64_t nq, uint64_t unit) {
-  const unsigned lane = threadIdx.x & 31;
-  uint64_t lo = 0, hi = nq;  // invariant: qp[lo] <= unit < qp[hi] (qp[nq] = +inf)
-  while (hi - lo > 32) {
-    const uint64_t stride = (hi - lo + 31) / 32;
-    const uint64_t idx = lo + lane * stride;
-    const bool le = idx < hi && qp[idx] <= unit;
-    const unsigned m = __ballot_sync(0xffffffffu, le);
-    const uint64_t j = 31 - __clz(m);
-    const uint64_t nlo = lo + j * stride;
-    hi = min(hi, nlo + stride);
-    lo = nlo;
-  }
-  const uint64_t idx = lo + lane;
-  const unsigned m = __ballot_sync(0xffffffffu, idx < hi && qp[idx] <= unit);
-  return lo + (31 - __clz(m));
-}
-
 // Top-down step (bfs.cpp:61-86). Each lane owns 8 edges of the warp's current
 // chunk; their column loads, visited probes and claim atomics are issued
 // before any result is consumed.
-__device__ void td_step(const BfsParams& p, const Hot& hot, uint32_t* cbuf, const uint32_t* qv,
+__device__ void td_step(const BfsParams& p, uint32_t* cbuf, const uint32_t* qv,
                         const uint64_t* qp,
                         uint64_t nq, uint64_t nu, uint32_t* qv_out, uint64_t* qp_out,
                         uint32_t* fnext, unsigned long long* slot, int32_t dnext, bool emit,
@@ -225,15 +137,12 @@ __device__ void td_step(const BfsParams& p, const Hot& hot, uint32_t* cbuf, cons
         w[j] = e < end ? p.ccol[e] : kNone32;
       }
 #pragma unroll
-      for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? probe_word(hot, p.visited, w[j]) : ~0u;
+      for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
         const uint32_t bit = 1u << (w[j] & 31);
         cl[j] = false;
-        if (!(vw[j] & bit)) {
-          cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
-          if (w[j] < hot.limit) atomicOr(&hot.mut[w[j] >> 5], bit);  // this CTA skips it now
-        }
+        if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
       }
       uint2 meta[kEpl];
 #pragma unroll
@@ -281,8 +190,8 @@ __device__ void td_step(const BfsParams& p, const Hot& hot, uint32_t* cbuf, cons
   __syncwarp();
 }
 
-__device__ __forceinline__ bool scan_row(const BfsParams& p, const Hot& hot, const uint32_t* fcur,
-                                         uint32_t v, uint32_t& par) {
+__device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcur, uint32_t v,
+                                         uint32_t& par) {
   // The first (highest-degree) neighbour was already probed; the rest of the
   // row is probed four at a time (independent loads) with early exit.
   const uint64_t re = p.crow[v + 1];
@@ -292,7 +201,7 @@ __device__ __forceinline__ bool scan_row(const BfsParams& p, const Hot& hot, con
 #pragma unroll
     for (int j = 0; j < 4; ++j) x[j] = e + j < re ? p.ccol[e + j] : kNone32;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = x[j] != kNone32 && probe_bit(hot, fcur, x[j]);
+    for (int j = 0; j < 4; ++j) b[j] = x[j] != kNone32 && test_bit(fcur, x[j]);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (b[j]) {
@@ -313,8 +222,7 @@ __device__ __forceinline__ bool scan_row(const BfsParams& p, const Hot& hot, con
 constexpr int kMissCap = kCbuf;  // u32 entries per warp (reuses the claim buffer)
 constexpr uint32_t kLaneScan = 64;
 
-__device__ void resolve_misses(const BfsParams& p, const Hot& hot, const uint32_t* fcur,
-                               uint32_t* fnext,
+__device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext,
                                uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
                                unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31;
@@ -327,7 +235,7 @@ __device__ void resolve_misses(const BfsParams& p, const Hot& hot, const uint32_
     uint32_t par = 0;
     if (v != kNone32) {
       if (p.cmeta[v].x > kLaneScan) lng = true;
-      else hit = scan_row(p, hot, fcur, v, par);
+      else hit = scan_row(p, fcur, v, par);
     }
     if (hit) {
       p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
@@ -349,7 +257,7 @@ __device__ void resolve_misses(const BfsParams& p, const Hot& hot, const uint32_
     for (uint64_t e0 = rb; e0 < re; e0 += 32) {
       const uint64_t e = e0 + lane;
       const uint32_t x = e < re ? p.ccol[e] : kNone32;
-      const unsigned m = __ballot_sync(0xffffffffu, x != kNone32 && probe_bit(hot, fcur, x));
+      const unsigned m = __ballot_sync(0xffffffffu, x != kNone32 && test_bit(fcur, x));
       if (m) {
         par = __shfl_sync(0xffffffffu, x, __ffs(m) - 1);
         break;
@@ -365,7 +273,7 @@ __device__ void resolve_misses(const BfsParams& p, const Hot& hot, const uint32_
   __syncwarp();
 }
 
-__device__ void bu_step(const BfsParams& p, const Hot& hot, uint32_t* mbuf, const uint32_t* fcur,
+__device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
@@ -387,7 +295,7 @@ __device__ void bu_step(const BfsParams& p, const Hot& hot, uint32_t* mbuf, cons
       f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[(w0 + k) * 32 + lane];
     bool hit[kBuU];
 #pragma unroll
-    for (int k = 0; k < kBuU; ++k) hit[k] = f[k] != kNone32 && probe_bit(hot, fcur, f[k]);
+    for (int k = 0; k < kBuU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
 #pragma unroll
     for (int k = 0; k < kBuU; ++k) {
       const uint32_t v = static_cast<uint32_t>((w0 + k) * 32 + lane);
@@ -406,11 +314,11 @@ __device__ void bu_step(const BfsParams& p, const Hot& hot, uint32_t* mbuf, cons
       nmiss += __popc(mm);
     }
     if (nmiss > kMissCap - 32 * kBuU) {
-      resolve_misses(p, hot, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
+      resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
       nmiss = 0;
     }
   }
-  if (nmiss) resolve_misses(p, hot, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
+  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
 }
 
 // Frontier bitmap -> frontier list (when a top-down level follows one that did
@@ -514,12 +422,11 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
       const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
       unsigned long long claims_acc = 0, scout_acc = 0;
       bool list_valid = true;
-      // (A smem copy of the bitmap's hot prefix was tried and measured slower:
-      // the 64 KB it takes comes out of L1, which already caches those lines.)
-      const Hot hot{nullptr, nullptr, 0u};
+      // (A smem copy of the probed bitmap's hot prefix was tried and measured
+      // slower: the 64 KB it takes comes out of L1, which caches those lines.)
       if (bu) {
         prev = awake;
-        bu_step(p, hot, sm.cbuf[threadIdx.x >> 5], fcur, fnext, dnext, claims_acc);
+        bu_step(p, sm.cbuf[threadIdx.x >> 5], fcur, fnext, dnext, claims_acc);
         block_add(claims_acc << kItemShift, &slot[0], sm);
       } else {
         etc -= (double)scout;
@@ -528,7 +435,7 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
         // (which needs only the bitmap), else the bitmap is converted.
         const bool emit = (double)scout < p.emit_limit;
         list_valid = emit;
-        td_step(p, hot, sm.cbuf[threadIdx.x >> 5], qv_in, qp_in, nq, nu, qv_out, qp_out, fnext, slot,
+        td_step(p, sm.cbuf[threadIdx.x >> 5], qv_in, qp_in, nq, nu, qv_out, qp_out, fnext, slot,
                 dnext, emit, scout_acc, claims_acc);
         block_add(scout_acc, &slot[1], sm);
         if (!emit) block_add(claims_acc << kItemShift, &slot[0], sm);

@@ -1,0 +1,81 @@
+// Device helpers shared by the single- and multi-partition BFS kernels.
+#pragma once
+
+#include "bfs.cuh"
+
+namespace etb {
+namespace dev {
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// Monotonic-counter grid barrier: every CTA adds 1; the barrier of a CTA that
+// saw value `old` completes at the next multiple of gridDim.x.
+inline __device__ void grid_sync(unsigned long long* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long nb = gridDim.x;
+    __threadfence();
+    const unsigned long long old = atomicAdd(bar, 1ull);
+    const unsigned long long target = (old / nb + 1) * nb;
+    const long long t0 = clock64();
+    while (ld_acquire(bar) < target) {
+      if (clock64() - t0 > 40000000000ll) __trap();  // ~20 s: never hang the GPU
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ bool test_bit(const uint32_t* bm, uint32_t v) {
+  return (bm[v >> 5] >> (v & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const unsigned lane = threadIdx.x & 31;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// Index of the last list entry whose chunk prefix is <= unit (32-ary search).
+inline __device__ uint64_t find_vertex(const uint64_t* qp, uint64_t nq, uint64_t unit) {
+  const unsigned lane = threadIdx.x & 31;
+  uint64_t lo = 0, hi = nq;  // invariant: qp[lo] <= unit < qp[hi] (qp[nq] = +inf)
+  while (hi - lo > 32) {
+    const uint64_t stride = (hi - lo + 31) / 32;
+    const uint64_t idx = lo + lane * stride;
+    const bool le = idx < hi && qp[idx] <= unit;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    const uint64_t j = 31 - __clz(m);
+    const uint64_t nlo = lo + j * stride;
+    hi = min(hi, nlo + stride);
+    lo = nlo;
+  }
+  const uint64_t idx = lo + lane;
+  const unsigned m = __ballot_sync(0xffffffffu, idx < hi && qp[idx] <= unit);
+  return lo + (31 - __clz(m));
+}
+
+}  // namespace dev
+}  // namespace etb
