@@ -157,6 +157,24 @@ int etb_result_device_ptr(etb_layout* L, uint32_t** dp);
 int etb_result_download(etb_layout* L, int32_t* depth, uint32_t* parent);
 /* ½ Σ full degree over reached vertices of the last result (validate.cpp:151-156). */
 int etb_result_traversed_edges(etb_layout* L, uint64_t* te);
+/* ---- (5) 1D core partition ------------------------------------------------ */
+/* Split the core into `parts` partitions run by one kernel on this device (the
+ * multi-GPU algorithm with the peer exchange in local memory); parts <= 1
+ * restores the single-partition kernel. */
+int etb_layout_partition(etb_layout* L, uint32_t parts);
+/* Partition k's owned ranges: bounds[6k..6k+5] = core lo, hi, tree lo, hi,
+ * isolated lo, hi (relaid ids). */
+int etb_layout_partition_bounds(const etb_layout* L, uint32_t parts, uint64_t* bounds);
+/* One GPU per process: rank `rank` of `world` builds its partition and exports
+ * an opaque blob (etb_mp_blob_size() bytes); after all blobs are exchanged
+ * (ordered by rank) etb_mp_connect opens the peers' exchange blocks over CUDA
+ * IPC. Every rank then calls etb_bfs_device with the same start; the kernels
+ * synchronise through peer memory. etb_result_traversed_edges then returns this
+ * rank's partial count. */
+int etb_mp_blob_size(void);
+int etb_mp_export(etb_layout* L, uint32_t world, uint32_t rank, void* blob_out);
+int etb_mp_connect(etb_layout* L, const void* blobs);
+
 /* Page-lock a caller buffer so result downloads run at full link speed. */
 int etb_host_register(void* ptr, uint64_t bytes);
 int etb_host_unregister(void* ptr);

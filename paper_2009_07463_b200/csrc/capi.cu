@@ -11,6 +11,7 @@
 #include <unistd.h>
 
 #include "bfs.cuh"
+#include "bfs_part.cuh"
 
 struct etb_graph {
   etb::DevGraph g;
@@ -28,6 +29,8 @@ struct etb_layout {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   etb::DevBuf<uint8_t> flush;
+  std::unique_ptr<etb::PartState> P;  // 1D core partition (null = single-partition kernel)
+  int system_scope = 0;               // peers are other GPUs
   ~etb_layout() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -132,7 +135,18 @@ etb::BfsParams run_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* o,
     ETB_CUDA(cudaMemsetAsync(p.trace, 0, 256, h->stream));
   }
   if (pre_launch) ETB_CUDA(cudaEventRecord(pre_launch, h->stream));
-  etb::bfs_launch(p, h->S, h->stream);
+  if (h->P) {
+    etb::PartParams pp{};
+    pp.base = p;
+    pp.parts = h->P->d_parts.get();
+    pp.nparts = h->P->nparts;
+    pp.first_part = h->P->first;
+    pp.local_parts = h->P->local;
+    pp.system_scope = h->system_scope;
+    etb::part_launch(pp, *h->P, h->stream);
+  } else {
+    etb::bfs_launch(p, h->S, h->stream);
+  }
   h->S.has_result = true;
   h->S.last_start = start;
   return p;
@@ -150,8 +164,10 @@ void collect_stats(etb_layout* h, etb_bfs_stats* st) {
   ETB_CUDA(cudaMemcpyAsync(ts, h->S.level_claims.get() + 256, 256 * 8, cudaMemcpyDeviceToHost,
                            h->stream));
   ETB_CUDA(cudaStreamSynchronize(h->stream));
-  for (uint32_t i = 0; i <= nl && i + 1 < 255; ++i) st->level_ns[i] = ts[1 + i] - ts[0];
-  st->total_ns = ts[255] - ts[0];
+  if (!h->P) {  // the partitioned kernel records no timestamps
+    for (uint32_t i = 0; i <= nl && i + 1 < 255; ++i) st->level_ns[i] = ts[1 + i] - ts[0];
+    st->total_ns = ts[255] - ts[0];
+  }
   st->levels = nl;
   st->direction_trace[std::min<uint32_t>(nl, 255)] = 0;
   for (uint32_t i = 0; i < nl && i < 255; ++i) st->bottom_up_levels += st->direction_trace[i] == 'b';
@@ -543,10 +559,113 @@ int etb_result_traversed_edges(etb_layout* h, uint64_t* te) {
     ETB_CUDA(cudaSetDevice(h->device));
     etb::DevBuf<unsigned long long> acc(1);
     ETB_CUDA(cudaMemsetAsync(acc.get(), 0, 8, h->stream));
-    te_kernel<<<etb::grid_for(h->L.n, 256), 256, 0, h->stream>>>(h->S.dp.get(), h->L.degn.get(),
-                                                                  h->L.n, acc.get());
+    if (h->P && h->P->local < h->P->nparts) {
+      // Multi-GPU: this device holds only its partitions' results; the caller
+      // sums the partial counts over ranks.
+      for (uint32_t j = 0; j < h->P->local; ++j) {
+        const etb::PartDev& d = h->P->h_parts[h->P->first + j];
+        const std::pair<uint64_t, uint64_t> rs[3] = {{d.lo, d.hi}, {d.tlo, d.thi}, {d.zlo, d.zhi}};
+        for (const auto& r : rs)
+          if (r.second > r.first)
+            te_kernel<<<etb::grid_for(r.second - r.first, 256), 256, 0, h->stream>>>(
+                h->S.dp.get() + r.first, h->L.degn.get() + r.first, r.second - r.first, acc.get());
+      }
+    } else {
+      te_kernel<<<etb::grid_for(h->L.n, 256), 256, 0, h->stream>>>(h->S.dp.get(), h->L.degn.get(),
+                                                                    h->L.n, acc.get());
+    }
     ETB_LAUNCH_CHECK();
     *te = etb::read_u64(reinterpret_cast<uint64_t*>(acc.get()), h->stream) / 2;
+  });
+}
+
+int etb_layout_partition(etb_layout* h, uint32_t parts) {
+  return guarded([&] {
+    need(h, "etb_layout_partition");
+    ETB_CUDA(cudaSetDevice(h->device));
+    if (parts <= 1) {
+      h->P.reset();
+      return;
+    }
+    auto P = std::make_unique<etb::PartState>();
+    etb::part_build(h->L, *P, parts, 0, parts, h->stream);
+    h->P = std::move(P);
+    h->system_scope = 0;
+  });
+}
+
+int etb_layout_partition_bounds(const etb_layout* h, uint32_t parts, uint64_t* bounds) {
+  return guarded([&] {
+    need(h, "etb_layout_partition_bounds");
+    need(bounds, "etb_layout_partition_bounds");
+    std::vector<etb::PartDev> b;
+    etb::part_bounds(h->L, parts, b);
+    for (uint32_t k = 0; k < parts; ++k) {
+      uint64_t* o = bounds + 6 * k;
+      o[0] = b[k].lo, o[1] = b[k].hi, o[2] = b[k].tlo, o[3] = b[k].thi, o[4] = b[k].zlo,
+      o[5] = b[k].zhi;
+    }
+  });
+}
+
+// Multi-process, one GPU per process. The blob a rank exports describes its
+// partition's exchange block (frontier replicas + counters) by CUDA IPC handle.
+struct MpBlob {
+  cudaIpcMemHandle_t handle;
+  uint64_t xbytes;
+  uint64_t words;
+  uint32_t rank, world;
+};
+
+int etb_mp_blob_size(void) { return static_cast<int>(sizeof(MpBlob)); }
+
+int etb_mp_export(etb_layout* h, uint32_t world, uint32_t rank, void* blob_out) {
+  return guarded([&] {
+    need(h, "etb_mp_export");
+    need(blob_out, "etb_mp_export");
+    if (world < 2 || rank >= world) throw std::invalid_argument("etb_mp_export: bad rank/world");
+    ETB_CUDA(cudaSetDevice(h->device));
+    auto P = std::make_unique<etb::PartState>();
+    etb::part_build(h->L, *P, world, rank, 1, h->stream);
+    MpBlob b{};
+    ETB_CUDA(cudaIpcGetMemHandle(&b.handle, P->xblock.get()));
+    b.xbytes = P->xbytes;
+    b.words = (h->L.nc + 31) / 32 + 1;
+    b.rank = rank;
+    b.world = world;
+    std::memcpy(blob_out, &b, sizeof b);
+    h->P = std::move(P);
+    h->system_scope = 1;
+  });
+}
+
+int etb_mp_connect(etb_layout* h, const void* blobs) {
+  return guarded([&] {
+    need(h, "etb_mp_connect");
+    need(blobs, "etb_mp_connect");
+    if (!h->P || h->P->local != 1) throw std::invalid_argument("etb_mp_connect: call etb_mp_export first");
+    ETB_CUDA(cudaSetDevice(h->device));
+    etb::PartState& P = *h->P;
+    const MpBlob* all = static_cast<const MpBlob*>(blobs);
+    for (uint32_t q = 0; q < P.nparts; ++q) {
+      if (all[q].rank != q || all[q].world != P.nparts)
+        throw std::invalid_argument("etb_mp_connect: blobs must be ordered by rank");
+      if (q == P.first) continue;
+      void* base = nullptr;
+      ETB_CUDA(cudaIpcOpenMemHandle(&base, all[q].handle, cudaIpcMemLazyEnablePeerAccess));
+      P.peer_maps.push_back(base);
+      etb::PartDev& d = P.h_parts[q];
+      const uint64_t words = all[q].words;
+      d.fb0 = static_cast<uint32_t*>(base);
+      d.fb1 = d.fb0 + words;
+      d.fb2 = d.fb1 + words;
+      d.ctr = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(base) +
+                                                    ((3 * words * 4 + 255) / 256) * 256);
+      d.arrive = d.ctr + 32;
+    }
+    ETB_CUDA(cudaMemcpyAsync(P.d_parts.get(), P.h_parts.data(), P.nparts * sizeof(etb::PartDev),
+                             cudaMemcpyHostToDevice, h->stream));
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
   });
 }
 

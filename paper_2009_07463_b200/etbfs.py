@@ -159,6 +159,11 @@ def lib() -> C.CDLL:
     sig("etb_result_device_ptr", vp, C.POINTER(vp))
     sig("etb_result_download", vp, vp, vp)
     sig("etb_result_traversed_edges", vp, P64)
+    sig("etb_layout_partition", vp, C.c_uint32)
+    sig("etb_layout_partition_bounds", vp, C.c_uint32, vp)
+    sig("etb_mp_blob_size")
+    sig("etb_mp_export", vp, C.c_uint32, C.c_uint32, vp)
+    sig("etb_mp_connect", vp, vp)
     sig("etb_host_register", vp, u64)
     sig("etb_host_unregister", vp)
     sig("etb_time_roots", vp, vp, u64, C.c_int, C.c_int, C.POINTER(_BfsOptions), vp, vp)
@@ -342,6 +347,19 @@ class EtLayout:
         col = np.empty(max(m, 1), np.uint64)
         _check(lib().etb_layout_download_graph(self._h, _ptr(row), _ptr(col)))
         return row, col[:m]
+
+
+def partition(cg: "EtLayout", parts: int) -> None:
+    """Run subsequent traversals of cg with the 1D core partition (parts >= 2) on
+    this device, or back on the single-partition kernel (parts <= 1)."""
+    _check(lib().etb_layout_partition(cg.handle, int(parts)))
+
+
+def partition_bounds(cg: "EtLayout", parts: int) -> np.ndarray:
+    """(parts, 6) u64: core lo/hi, tree lo/hi, isolated lo/hi per partition."""
+    b = np.empty(6 * parts, np.uint64)
+    _check(lib().etb_layout_partition_bounds(cg.handle, int(parts), _ptr(b)))
+    return b.reshape(parts, 6)
 
 
 def relayout_csr(g: Csr, types=None, mh: int = -1) -> EtLayout:
