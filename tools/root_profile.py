@@ -23,9 +23,12 @@ def main():
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--mh", type=int, default=-1)
     ap.add_argument("--roots", type=int, default=64)
+    ap.add_argument("--parts", type=int, default=1, help="1D core partitions on this device")
     args = ap.parse_args()
     g = eb.generate_graph(scale=args.scale, edgefactor=args.edgefactor, seed=1)
     cg = eb.relayout_csr(g, mh=args.mh)
+    if args.parts > 1:
+        E.partition(cg, args.parts)
     roots = select_roots_from_degrees(g.degrees(), 64, 1)[: args.roots]
     starts = cg.old2new[roots.astype(np.int64)]
     ms, kms = E.time_roots(cg, starts, warmup=8, flush_l2=True)
