@@ -160,9 +160,12 @@ def run_ours(args):
         dist.barrier()
 
     te = np.empty(len(starts), np.uint64)
+    valid = []
     for i, s in enumerate(starts):
         E.bfs_device(cg, int(s))
         te[i] = E.result_traversed_edges(cg)  # this rank's owned part when world > 1
+        if world == 1:  # validate_bfs_tree rules 1-5 on the device, every root (untimed)
+            valid.append(E.result_validate(cg, int(s))["passed"])
     if world > 1:
         t = torch.tensor(te.astype(np.int64), device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -250,6 +253,7 @@ def run_ours(args):
         "detail": {"mean_gteps": round(float(per.mean()), 3), "min_gteps": round(float(per.min()), 3),
                    "max_gteps": round(float(per.max()), 3),
                    "hm_gteps_giant_component": round(hm_giant, 3),
+                   "validated_roots": len(valid), "all_valid": all(valid) if valid else None,
                    "kernel_ms_mean": round(float(np.mean(kms)), 4),
                    "call_ms_mean": round(float(np.mean(ms)), 4),
                    "traversed_edges": int(te.max()),
@@ -284,9 +288,11 @@ def measure_secondary(scale, ef, mh, steps, warmup):
     roots = select_roots_from_degrees(g.degrees(), NROOTS, 1)
     starts = cg.old2new[roots.astype(np.int64)]
     te = np.empty(len(starts), np.uint64)
+    valid = []
     for i, s in enumerate(starts):
         E.bfs_device(cg, int(s))
         te[i] = E.result_traversed_edges(cg)
+        valid.append(E.result_validate(cg, int(s))["passed"])
     ms, kms = E.time_roots(cg, np.tile(starts, steps), warmup=warmup * len(starts), flush_l2=True)
     te_rep = np.tile(te, steps).astype(np.float64)
     hm, per = harmonic_gteps(te_rep, ms / 1e3)
@@ -306,7 +312,8 @@ def measure_secondary(scale, ef, mh, steps, warmup):
                          "bytes_per_te": round(balg / float(te.max()), 3),
                          "roofline_gteps": round(roof, 1),
                          "frac_of_roofline_gteps": round(hm / roof, 4)},
-            "preprocessing_s": round(prep, 3), "gpu_launches": int(len(ms))}
+            "preprocessing_s": round(prep, 3), "gpu_launches": int(len(ms)),
+            "validated_roots": len(valid), "all_valid": all(valid)}
 
 
 def select_roots_from_degrees(deg, count, seed):

@@ -179,6 +179,13 @@ int etb_mp_connect(etb_layout* L, const void* blobs);
 int etb_host_register(void* ptr, uint64_t bytes);
 int etb_host_unregister(void* ptr);
 
+/* validate_bfs_tree (validate.hpp:13-46) on the device over the whole graph for the
+ * last result from relaid `start`: counts[0..4] = violations of rules 1..5 (root
+ * parent, chains, parent edge, level span, reached set), counts[5] = reached
+ * vertices. Rules 1-5 together imply every depth is the exact BFS distance. The
+ * layout's graph must still be alive. */
+int etb_result_validate(etb_layout* L, uint64_t start, uint64_t* counts);
+
 /* ---- measurement ---------------------------------------------------------- */
 /* Times etb_bfs_device per start with CUDA events on the layout's stream, after
  * `warmup` untimed runs; flush_l2 != 0 writes a >L2 buffer between roots (outside

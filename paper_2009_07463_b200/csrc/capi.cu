@@ -579,6 +579,18 @@ int etb_result_traversed_edges(etb_layout* h, uint64_t* te) {
   });
 }
 
+int etb_result_validate(etb_layout* h, uint64_t start, uint64_t* counts) {
+  return guarded([&] {
+    need(h, "etb_result_validate");
+    need(counts, "etb_result_validate");
+    if (start >= h->L.n) throw std::invalid_argument("validate_bfs_tree: root out of range");
+    if (h->P && h->P->local < h->P->nparts)
+      throw std::invalid_argument("etb_result_validate: result is spread over several GPUs");
+    ETB_CUDA(cudaSetDevice(h->device));
+    etb::validate_result(h->L, h->S.dp.get(), start, counts, h->stream);
+  });
+}
+
 int etb_layout_partition(etb_layout* h, uint32_t parts) {
   return guarded([&] {
     need(h, "etb_layout_partition");

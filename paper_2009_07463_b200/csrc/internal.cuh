@@ -69,6 +69,11 @@ void build_layout(const DevGraph& g, const uint8_t* type_dev, int64_t mh, DevLay
 void build_full_relabelled(const DevLayout& L, DevBuf<uint64_t>& row, DevBuf<uint32_t>& col,
                            cudaStream_t s);
 
+// validate_bfs_tree rules 1-5 on the device for a relaid {depth, parent} result:
+// out[0..4] = violations of rules 1..5, out[5] = reached vertices.
+void validate_result(const DevLayout& L, const uint2* dp, uint64_t root, uint64_t out[6],
+                     cudaStream_t s);
+
 // CUB wrappers (cub_ops.cu) — library sorts/scans used only in preprocessing.
 void sort_keys_u64(DevBuf<uint64_t>& keys, DevBuf<uint64_t>& alt, uint64_t count, int end_bit,
                    cudaStream_t s);  // result left in `keys`

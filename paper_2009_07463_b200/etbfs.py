@@ -159,6 +159,7 @@ def lib() -> C.CDLL:
     sig("etb_result_device_ptr", vp, C.POINTER(vp))
     sig("etb_result_download", vp, vp, vp)
     sig("etb_result_traversed_edges", vp, P64)
+    sig("etb_result_validate", vp, u64, vp)
     sig("etb_layout_partition", vp, C.c_uint32)
     sig("etb_layout_partition_bounds", vp, C.c_uint32, vp)
     sig("etb_mp_blob_size")
@@ -293,8 +294,9 @@ def count_types(types) -> TypeCounts:
 class EtLayout:
     """A ClassifiedGraph (types.hpp:69-76) + its EdgeTreeList, BFS-ready in HBM."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, graph=None):
         self._h = handle
+        self._graph = graph  # the device CSR must outlive the layout (graph(), validate)
         info = _LayoutInfo()
         _check(lib().etb_layout_info_get(handle, C.byref(info)))
         self.vertex_count = info.vertex_count
@@ -372,7 +374,7 @@ def relayout_csr(g: Csr, types=None, mh: int = -1) -> EtLayout:
         if t.size != g.vertex_count:
             raise ValueError("relayout_csr: types length does not match vertex count")
         _check(lib().etb_layout_build_types(g.handle, _ptr(t), int(mh), C.byref(h)))
-    return EtLayout(h)
+    return EtLayout(h, g)
 
 
 def extract_edge_tree_list(cg: EtLayout):
@@ -439,6 +441,15 @@ def result_download(cg: EtLayout, depth: np.ndarray | None = None,
         parent = np.empty(max(n, 1), np.uint32)
     _check(lib().etb_result_download(cg.handle, _ptr(depth), _ptr(parent)))
     return depth[:n], parent[:n]
+
+
+def result_validate(cg: EtLayout, start: int) -> dict:
+    """validate_bfs_tree rules 1-5 on the device for the last result."""
+    c = np.zeros(6, np.uint64)
+    _check(lib().etb_result_validate(cg.handle, int(start), _ptr(c)))
+    return {"rule1": int(c[0]), "rule2": int(c[1]), "rule3": int(c[2]), "rule4": int(c[3]),
+            "rule5": int(c[4]), "reached": int(c[5]),
+            "passed": bool((c[:5] == 0).all())}
 
 
 def result_traversed_edges(cg: EtLayout) -> int:
