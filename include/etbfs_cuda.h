@@ -186,6 +186,12 @@ int etb_host_unregister(void* ptr);
  * layout's graph must still be alive. */
 int etb_result_validate(etb_layout* L, uint64_t start, uint64_t* counts);
 
+/* Diagnostics: one traversal from `start` recording, per level and CTA, the
+ * device time (ns since kernel entry) at which the CTA finished its step:
+ * out[level * grid + cta] (cap entries). */
+int etb_debug_block_stamps(etb_layout* L, uint64_t start, uint64_t* out, uint64_t cap,
+                           uint32_t* grid, uint32_t* levels);
+
 /* ---- measurement ---------------------------------------------------------- */
 /* Times etb_bfs_device per start with CUDA events on the layout's stream, after
  * `warmup` untimed runs; flush_l2 != 0 writes a >L2 buffer between roots (outside

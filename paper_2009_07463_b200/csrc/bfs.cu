@@ -30,7 +30,7 @@ namespace {
 
 using namespace dev;
 
-constexpr int kBlock = 512;
+constexpr int kBlock = 1024;  // one CTA per SM: half the grid-barrier arrivals of 2 x 512
 constexpr int kWarps = kBlock / 32;
 constexpr int kItemShift = 36;
 constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
@@ -356,7 +356,7 @@ __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t*
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
+__global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(kBlock, 2) et_bfs_kernel(BfsParams p) {
         block_add(scout_acc, &slot[1], sm);
         if (!emit) block_add(claims_acc << kItemShift, &slot[0], sm);
       }
+      if (p.bstamp && threadIdx.x == 0 && L < 64) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
       grid_sync(p.bar);
       const unsigned long long packed = ld_volatile(&slot[0]);
       const unsigned long long claims = packed >> kItemShift;
@@ -561,7 +562,7 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
                                                          sizeof(Smem)));
   if (per_sm < 1) throw CudaError("et_bfs_kernel cannot be resident");
   S.block = kBlock;
-  S.grid = sms * std::min(per_sm, 2);
+  S.grid = sms * std::min(per_sm, 2048 / kBlock);
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -594,6 +595,7 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.emit_limit = static_cast<double>(L.nc) / 4.0 + 1024.0;
   p.trace = nullptr;
   p.level_claims = nullptr;
+  p.bstamp = nullptr;
   p.nlevels = nullptr;
 }
 

@@ -48,6 +48,7 @@ struct BfsParams {
   // stats (may be null)
   char* trace;
   unsigned long long* level_claims;
+  unsigned long long* bstamp;  // diagnostics: [level][block] step-end globaltimer, or null
   uint32_t* nlevels;
 };
 

@@ -108,7 +108,8 @@ void finish_layout(etb_layout* h) {
 }
 
 etb::BfsParams run_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* o,
-                       bool want_stats, cudaEvent_t pre_launch = nullptr) {
+                       bool want_stats, cudaEvent_t pre_launch = nullptr,
+                       unsigned long long* bstamp = nullptr) {
   const etb::DevLayout& L = h->L;
   if (start >= L.n) throw std::invalid_argument("et_bfs: start out of range");
   etb_bfs_options opt{ETB_KERNEL_HYBRID, ETB_REPLAY_TEET, 14.0, 24.0};
@@ -134,6 +135,7 @@ etb::BfsParams run_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* o,
     p.nlevels = h->S.nlevels.get();
     ETB_CUDA(cudaMemsetAsync(p.trace, 0, 256, h->stream));
   }
+  p.bstamp = bstamp;
   if (pre_launch) ETB_CUDA(cudaEventRecord(pre_launch, h->stream));
   if (h->P) {
     etb::PartParams pp{};
@@ -588,6 +590,30 @@ int etb_result_validate(etb_layout* h, uint64_t start, uint64_t* counts) {
       throw std::invalid_argument("etb_result_validate: result is spread over several GPUs");
     ETB_CUDA(cudaSetDevice(h->device));
     etb::validate_result(h->L, h->S.dp.get(), start, counts, h->stream);
+  });
+}
+
+int etb_debug_block_stamps(etb_layout* h, uint64_t start, uint64_t* out, uint64_t cap,
+                           uint32_t* grid, uint32_t* levels) {
+  return guarded([&] {
+    need(h, "etb_debug_block_stamps");
+    if (h->P) throw std::invalid_argument("etb_debug_block_stamps: single-partition kernel only");
+    ETB_CUDA(cudaSetDevice(h->device));
+    const uint64_t g = static_cast<uint64_t>(h->S.grid);
+    etb::DevBuf<unsigned long long> st(64 * g);
+    ETB_CUDA(cudaMemsetAsync(st.get(), 0, 64 * g * 8, h->stream));
+    run_bfs(h, start, nullptr, true, nullptr, st.get());
+    uint64_t t0 = 0;
+    uint32_t nl = 0;
+    ETB_CUDA(cudaMemcpyAsync(&t0, h->S.level_claims.get() + 256, 8, cudaMemcpyDeviceToHost,
+                             h->stream));
+    ETB_CUDA(cudaMemcpyAsync(&nl, h->S.nlevels.get(), 4, cudaMemcpyDeviceToHost, h->stream));
+    std::vector<uint64_t> hs(64 * g);
+    ETB_CUDA(cudaMemcpyAsync(hs.data(), st.get(), 64 * g * 8, cudaMemcpyDeviceToHost, h->stream));
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
+    for (uint64_t i = 0; i < std::min<uint64_t>(cap, 64 * g); ++i) out[i] = hs[i] ? hs[i] - t0 : 0;
+    if (grid) *grid = static_cast<uint32_t>(g);
+    if (levels) *levels = nl;
   });
 }
 
