@@ -35,13 +35,18 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kItemShift = 36;
 constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 
-constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down item
-constexpr int kCbuf = 2 * kTdChunk;  // staged claims per warp (u32 vertex ids)
+constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down chunk
+constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex ids)
 constexpr int kBuU = 4;              // visited words per warp per bottom-up iteration
 constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab
 
+struct WarpSmem {
+  uint32_t cbuf[kCbuf];     // staged claims (top-down); with win: deferred misses (bottom-up)
+  int32_t win[kTdChunk];    // merge-path window: list prefix minus chunk start
+};
+
 struct Smem {
-  uint32_t cbuf[kWarps][kCbuf];  // staged claims (top-down) / deferred misses (bottom-up)
+  WarpSmem w[kWarps];
   unsigned long long red[kWarps];
 };
 
@@ -65,76 +70,115 @@ __device__ void block_add(unsigned long long v, unsigned long long* dst, Smem& s
   __syncthreads();
 }
 
-__device__ __forceinline__ uint32_t nchunks(uint64_t d) {
-  return static_cast<uint32_t>((d + kTdChunk - 1) / kTdChunk);
-}
+// Frontier list: vertices qv[0..nq) with at least one core edge, and the
+// exclusive prefix qp[] of their core degrees (ne = total edges). A top-down
+// level cuts the concatenated rows into 256-edge chunks (merge path): hub rows
+// span many chunks, tiny rows share one, and every chunk is the same work. Each
+// warp takes one chunk, then pulls batches of kGrab from a per-level counter.
+// Claims append (vertex, edge prefix) with one packed atomic per staged batch:
+// slot[0] = (list length << 36) | edges returns both positions at once.
 
-// Frontier list: vertex ids qv[0..nq) plus the exclusive prefix qp[] of their
-// row-chunk counts (a chunk = kTdChunk core edges). A top-down level splits the
-// nu = sum(chunks) chunks evenly over all warps: each warp takes a contiguous
-// chunk range, finds its first vertex with one 32-ary warp search and walks
-// forward. Claims append (vertex, chunk prefix) pairs with one packed atomic per
-// staged batch: (claims << 36) | chunks returns both positions at once.
-
-// Append the staged claims (entries (nchunks << 32) | vertex) to the next list.
-__device__ __forceinline__ uint32_t row_chunks(const BfsParams& p, uint32_t v) {
-  return (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
-}
-
+// Append the staged claims to the next list (vertices without core edges skipped).
 __device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, uint32_t ncl,
                              uint32_t* qv_out, uint64_t* qp_out, unsigned long long* slot) {
   const unsigned lane = threadIdx.x & 31;
-  unsigned long long nch = 0;
-  for (uint32_t i = lane; i < ncl; i += 32) nch += row_chunks(p, cbuf[i]);
-  nch = warp_sum(nch);
+  unsigned long long cnt = 0, edges = 0;
+  for (uint32_t i = lane; i < ncl; i += 32) {
+    const uint32_t d = p.cmeta[cbuf[i]].x;
+    cnt += d != 0;
+    edges += d;
+  }
+  cnt = warp_sum(cnt);
+  edges = warp_sum(edges);
+  if (cnt == 0) return;
   unsigned long long old = 0;
-  if (lane == 0) old = atomicAdd(slot, ((unsigned long long)ncl << kItemShift) | nch);
+  if (lane == 0) old = atomicAdd(slot, (cnt << kItemShift) | edges);
   old = __shfl_sync(0xffffffffu, old, 0);
-  uint64_t vpos = old >> kItemShift, cpos = old & kItemMask;
+  uint64_t vpos = old >> kItemShift, epos = old & kItemMask;
   for (uint32_t i0 = 0; i0 < ncl; i0 += 32) {
     const uint32_t i = i0 + lane;
     const uint32_t v = i < ncl ? cbuf[i] : 0u;
-    const uint32_t c = i < ncl ? row_chunks(p, v) : 0u;
-    const uint32_t incl = warp_incl_scan(c);
-    if (i < ncl) {
-      qv_out[vpos + i] = v;
-      qp_out[vpos + i] = cpos + incl - c;
+    const uint32_t d = i < ncl ? p.cmeta[v].x : 0u;
+    const uint32_t k = d != 0;
+    const uint32_t kin = warp_incl_scan(k), din = warp_incl_scan(d);
+    if (k) {
+      qv_out[vpos + kin - 1] = v;
+      qp_out[vpos + kin - 1] = epos + din - d;
     }
-    cpos += __shfl_sync(0xffffffffu, incl, 31);
+    vpos += __shfl_sync(0xffffffffu, kin, 31);
+    epos += __shfl_sync(0xffffffffu, din, 31);
   }
 }
 
-// Top-down step (bfs.cpp:61-86). Each lane owns 8 edges of the warp's current
-// chunk; their column loads, visited probes and claim atomics are issued
-// before any result is consumed.
-__device__ void td_step(const BfsParams& p, uint32_t* cbuf, const uint32_t* qv,
-                        const uint64_t* qp,
-                        uint64_t nq, uint64_t nu, uint32_t* qv_out, uint64_t* qp_out,
-                        uint32_t* fnext, unsigned long long* slot, int32_t dnext, bool emit,
-                        unsigned long long& scout_acc, unsigned long long& claims_acc) {
+// Largest k with win[k] <= rel (win[0] <= 0 <= rel; win is nondecreasing).
+__device__ __forceinline__ uint32_t win_search(const int32_t* win, int32_t rel) {
+  uint32_t lo = 0, hi = kTdChunk;
+  while (hi - lo > 1) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (win[m] <= rel) lo = m; else hi = m;
+  }
+  return lo;
+}
+
+// Top-down step (bfs.cpp:61-86). Each lane owns 8 edges of the warp's chunk;
+// their column loads, visited probes and claim atomics are issued before any
+// result is consumed.
+__device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const uint32_t* qv,
+                        const uint64_t* qp, uint64_t nq, uint64_t ne, uint32_t* qv_out,
+                        uint64_t* qp_out, uint32_t* fnext, unsigned long long* slot,
+                        int32_t dnext, bool emit, unsigned long long& scout_acc,
+                        unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
   const unsigned lt = (1u << lane) - 1;
-  // Every warp first takes one chunk (so small levels spread over all warps);
-  // when there is more work than that, further chunks are pulled in batches
-  // of kGrab from a per-level counter, so warps that draw cheap chunks keep
-  // working instead of idling at the barrier behind expensive ones.
-  uint32_t ncl = 0;
+  const uint64_t nu = (ne + kTdChunk - 1) / kTdChunk;
   for (uint64_t g0 = gw, gn = 1; g0 < nu;) {
     const uint64_t g1 = min(nu, g0 + gn);
-    uint64_t i = find_vertex(qp, nq, g0);
-    for (uint64_t unit = g0; unit < g1; ++unit) {
-      while (i + 1 < nq && qp[i + 1] <= unit) ++i;
-      const uint32_t u = qv[i];
-      const uint64_t beg = p.crow[u] + (unit - qp[i]) * kTdChunk;
-      const uint64_t end = min(p.crow[u + 1], beg + kTdChunk);
-      uint32_t w[kEpl], vw[kEpl];
+    uint64_t i = find_vertex(qp, nq, g0 * kTdChunk);
+    for (uint64_t c = g0; c < g1; ++c) {
+      const uint64_t e0 = c * kTdChunk, e1 = min(ne, e0 + kTdChunk);
+      const uint64_t qi = qp[i];
+      const uint64_t iend = i + 1 < nq ? qp[i + 1] : ne;
+      const bool single = iend >= e1;
+      uint64_t inext;
+      if (!single) {
+        for (uint32_t k = lane; k < kTdChunk; k += 32) {
+          const uint64_t ii = i + k;
+          int32_t wv = 0x7FFFFFFF;
+          if (ii < nq) {
+            const uint64_t q = qp[ii];
+            wv = q <= e0 ? (k == 0 ? 0 : -1) : (q - e0 > kTdChunk ? 0x7FFFFFFF : (int32_t)(q - e0));
+          }
+          win[k] = wv;
+        }
+        __syncwarp();
+        inext = i + win_search(win, kTdChunk);
+      } else {
+        inext = iend == e1 ? i + 1 : i;
+      }
+      // vertex and column position of each of the lane's 8 edges
+      uint32_t u[kEpl], w[kEpl], vw[kEpl];
       bool cl[kEpl];
+      uint32_t k = single ? 0u : win_search(win, static_cast<int32_t>(lane));
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
-        const uint64_t e = beg + lane + 32 * j;
-        w[j] = e < end ? p.ccol[e] : kNone32;
+        const uint32_t rel = lane + 32 * j;
+        if (!single)
+          while (k + 1 < kTdChunk && win[k + 1] <= static_cast<int32_t>(rel)) ++k;
+        u[j] = rel < e1 - e0 ? (single ? qv[i] : qv[i + k]) : kNone32;
+        w[j] = static_cast<uint32_t>(k);  // relative vertex index for now
+      }
+#pragma unroll
+      for (int j = 0; j < kEpl; ++j) {
+        const uint32_t rel = lane + 32 * j;
+        uint32_t col = kNone32;
+        if (u[j] != kNone32) {
+          const uint64_t qs = single ? qi : e0 + static_cast<uint64_t>(max(win[w[j]], 0));
+          const uint64_t vs = single ? qi : (w[j] == 0 ? qi : qs);
+          col = p.ccol[p.crow[u[j]] + (e0 + rel - vs)];
+        }
+        w[j] = col;
       }
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
@@ -144,41 +188,33 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, const uint32_t* qv,
         cl[j] = false;
         if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
       }
-      uint2 meta[kEpl];
+      uint32_t dg[kEpl];
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
+        dg[j] = 0;
         if (cl[j]) {
-          p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u);
+          p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u[j]);
           atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
-          meta[j] = p.cmeta[w[j]];
+          dg[j] = p.degn[w[j]];
         }
       }
-      if (!emit) {
-        // Large frontier: the next level is all but certainly bottom-up, which
-        // needs only the bitmap (otherwise the bitmap is converted); count only.
-#pragma unroll
-        for (int j = 0; j < kEpl; ++j)
-          if (cl[j]) {
-            scout_acc += meta[j].y;
-            ++claims_acc;
-          }
-        continue;
-      }
+      uint32_t ncl = 0;
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
-        const unsigned m = __ballot_sync(0xffffffffu, cl[j]);
-        if (cl[j]) {
-          scout_acc += meta[j].y;
-          cbuf[ncl + __popc(m & lt)] = w[j];
+        scout_acc += dg[j];
+        claims_acc += cl[j];
+        if (emit) {
+          const unsigned m = __ballot_sync(0xffffffffu, cl[j]);
+          if (cl[j]) cbuf[ncl + __popc(m & lt)] = w[j];
+          ncl += __popc(m);
         }
-        ncl += __popc(m);
+      }
+      if (emit && ncl) {
+        __syncwarp();
+        flush_claims(p, cbuf, ncl, qv_out, qp_out, slot);
       }
       __syncwarp();
-      if (ncl > kCbuf - kTdChunk) {
-        flush_claims(p, cbuf, ncl, qv_out, qp_out, slot);
-        ncl = 0;
-        __syncwarp();
-      }
+      i = inext;
     }
     if (nu <= nw) break;
     unsigned long long next = 0;
@@ -186,8 +222,6 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, const uint32_t* qv,
     g0 = __shfl_sync(0xffffffffu, next, 0);
     gn = kGrab;
   }
-  if (ncl) flush_claims(p, cbuf, ncl, qv_out, qp_out, slot);
-  __syncwarp();
 }
 
 __device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcur, uint32_t v,
@@ -219,7 +253,7 @@ __device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcu
 // deferred to a per-warp smem list and scanned afterwards, one lane per vertex
 // (rows of <= kLaneScan core neighbours) or the whole warp per vertex (longer
 // rows), so one long row no longer stalls 31 idle lanes.
-constexpr int kMissCap = kCbuf;  // u32 entries per warp (reuses the claim buffer)
+constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (the claim buffer + the window)
 constexpr uint32_t kLaneScan = 64;
 
 __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext,
@@ -331,27 +365,34 @@ __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t*
   for (uint64_t w0 = gw * 32; w0 < p.nwords; w0 += nw * 32) {
     const uint64_t wi = w0 + lane;
     const uint32_t bits = wi < p.nwords ? fcur[wi] : 0u;
-    uint32_t cnt = __popc(bits), nch = 0;
+    uint32_t cnt = 0, edges = 0;
     for (uint32_t b = bits; b; b &= b - 1) {
-      const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
-      nch += (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
+      const uint32_t d = p.cmeta[static_cast<uint32_t>(wi * 32 + __ffs(b) - 1)].x;
+      cnt += d != 0;
+      edges += d;
     }
     const uint32_t vin = warp_incl_scan(cnt);
-    const uint32_t cin = warp_incl_scan(nch);
     const uint32_t vtot = __shfl_sync(0xffffffffu, vin, 31);
     if (vtot == 0) continue;
-    const uint32_t ctot = __shfl_sync(0xffffffffu, cin, 31);
+    // edge prefix in 64 bits (a word of hubs can exceed 2^32 edges only in theory)
+    unsigned long long ein = edges;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, ein, o);
+      if (lane >= o) ein += y;
+    }
+    const unsigned long long etot = __shfl_sync(0xffffffffu, ein, 31);
     unsigned long long old = 0;
-    if (lane == 31)
-      old = atomicAdd(cslot, ((unsigned long long)vtot << kItemShift) | ctot);
+    if (lane == 31) old = atomicAdd(cslot, ((unsigned long long)vtot << kItemShift) | etot);
     old = __shfl_sync(0xffffffffu, old, 31);
-    uint64_t vpos = (old >> kItemShift) + vin - cnt, cpos = (old & kItemMask) + cin - nch;
+    uint64_t vpos = (old >> kItemShift) + vin - cnt, epos = (old & kItemMask) + ein - edges;
     for (uint32_t b = bits; b; b &= b - 1) {
       const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
+      const uint32_t d = p.cmeta[v].x;
+      if (!d) continue;
       qv_out[vpos] = v;
-      qp_out[vpos] = cpos;
+      qp_out[vpos] = epos;
       ++vpos;
-      cpos += (p.cmeta[v].x + kTdChunk - 1) / kTdChunk;
+      epos += d;
     }
   }
 }
@@ -381,10 +422,10 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
     p.fb2[i] = 0;
   }
   if (tid < 24) p.ctr[tid] = 0;
-  uint64_t nq = 0, nu = 0;  // frontier list length and its chunk count
+  uint64_t nq = 0, ne = 0;  // frontier list length and its edge count
   if (run_core) {
-    nq = 1;
-    nu = (p.cmeta[start].x + kTdChunk - 1) / kTdChunk;
+    ne = p.cmeta[start].x;
+    nq = ne != 0;
     if (tid == 0) {
       p.qv0[0] = start;
       p.qp0[0] = 0;
@@ -416,6 +457,7 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
         p.ctr[((L + 2) & 3) * 4 + 0] = 0;
         p.ctr[((L + 2) & 3) * 4 + 1] = 0;
         p.ctr[((L + 2) & 3) * 4 + 2] = 0;
+        p.ctr[((L + 2) & 3) * 4 + 3] = 0;
         p.ctr[16 + ((L + 1) & 1)] = 0;
         if (p.trace && L < 255) p.trace[L] = bu ? 'b' : 't';
       }
@@ -426,8 +468,8 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
       // slower: the 64 KB it takes comes out of L1, which caches those lines.)
       if (bu) {
         prev = awake;
-        bu_step(p, sm.cbuf[threadIdx.x >> 5], fcur, fnext, dnext, claims_acc);
-        block_add(claims_acc << kItemShift, &slot[0], sm);
+        bu_step(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc);
+        block_add(claims_acc, &slot[3], sm);
       } else {
         etc -= (double)scout;
         // The next frontier list is emitted only when this frontier's edge count
@@ -435,15 +477,14 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
         // (which needs only the bitmap), else the bitmap is converted.
         const bool emit = (double)scout < p.emit_limit;
         list_valid = emit;
-        td_step(p, sm.cbuf[threadIdx.x >> 5], qv_in, qp_in, nq, nu, qv_out, qp_out, fnext, slot,
-                dnext, emit, scout_acc, claims_acc);
+        td_step(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_in, qp_in, nq, ne,
+                qv_out, qp_out, fnext, slot, dnext, emit, scout_acc, claims_acc);
         block_add(scout_acc, &slot[1], sm);
-        if (!emit) block_add(claims_acc << kItemShift, &slot[0], sm);
+        block_add(claims_acc, &slot[3], sm);
       }
       if (p.bstamp && threadIdx.x == 0 && L < 64) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
       grid_sync(p.bar);
-      const unsigned long long packed = ld_volatile(&slot[0]);
-      const unsigned long long claims = packed >> kItemShift;
+      const unsigned long long claims = ld_volatile(&slot[3]);
       if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = claims;
       ++L;
       stamp(p, 257 + L);
@@ -458,8 +499,9 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
       } else {
         frontier = claims;
         scout = ld_volatile(&slot[1]);
-        nq = claims;
-        nu = packed & kItemMask;
+        const unsigned long long packed = ld_volatile(&slot[0]);
+        nq = packed >> kItemShift;
+        ne = packed & kItemMask;
         uint32_t* tv = qv_in;
         qv_in = qv_out;
         qv_out = tv;
@@ -478,7 +520,7 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
           grid_sync(p.bar);
           const unsigned long long cp = ld_volatile(cslot);
           nq = cp >> kItemShift;
-          nu = cp & kItemMask;
+          ne = cp & kItemMask;
         }
       }
     }
