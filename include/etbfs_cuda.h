@@ -191,6 +191,10 @@ int etb_result_validate(etb_layout* L, uint64_t start, uint64_t* counts);
  * out[level * grid + cta] (cap entries). */
 int etb_debug_block_stamps(etb_layout* L, uint64_t start, uint64_t* out, uint64_t cap,
                            uint32_t* grid, uint32_t* levels);
+/* Diagnostics: the raw globaltimer stamps of the last stats run ([0] entry, [1]
+ * init end, [2 + L] level L end, [128 + L] conversion before level L end,
+ * [255] replay end). */
+int etb_debug_phase_stamps(etb_layout* L, uint64_t* out256);
 
 /* ---- measurement ---------------------------------------------------------- */
 /* Times etb_bfs_device per start with CUDA events on the layout's stream, after

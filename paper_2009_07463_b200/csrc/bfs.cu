@@ -518,6 +518,7 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
           unsigned long long* cslot = p.ctr + 16 + (L & 1);
           convert_step(p, F[L % 3], qv_in, qp_in, cslot);
           grid_sync(p.bar);
+          stamp(p, 384 + L);  // diagnostics: end of the bitmap -> list conversion
           const unsigned long long cp = ld_volatile(cslot);
           nq = cp >> kItemShift;
           ne = cp & kItemMask;

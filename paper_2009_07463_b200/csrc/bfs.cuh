@@ -6,7 +6,7 @@
 namespace etb {
 
 // Chunk of a core row one warp expands in a top-down step.
-constexpr uint32_t kTdChunk = 256;
+constexpr uint32_t kTdChunk = 128;
 
 struct BfsParams {
   // core graph (relaid ids)

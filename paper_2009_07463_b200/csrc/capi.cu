@@ -593,6 +593,16 @@ int etb_result_validate(etb_layout* h, uint64_t start, uint64_t* counts) {
   });
 }
 
+int etb_debug_phase_stamps(etb_layout* h, uint64_t* out256) {
+  return guarded([&] {
+    need(h, "etb_debug_phase_stamps");
+    need(out256, "etb_debug_phase_stamps");
+    ETB_CUDA(cudaMemcpyAsync(out256, h->S.level_claims.get() + 256, 256 * 8,
+                             cudaMemcpyDeviceToHost, h->stream));
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
 int etb_debug_block_stamps(etb_layout* h, uint64_t start, uint64_t* out, uint64_t cap,
                            uint32_t* grid, uint32_t* levels) {
   return guarded([&] {

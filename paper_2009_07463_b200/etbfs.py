@@ -160,6 +160,7 @@ def lib() -> C.CDLL:
     sig("etb_result_download", vp, vp, vp)
     sig("etb_result_traversed_edges", vp, P64)
     sig("etb_result_validate", vp, u64, vp)
+    sig("etb_debug_phase_stamps", vp, vp)
     sig("etb_debug_block_stamps", vp, u64, vp, u64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32))
     sig("etb_layout_partition", vp, C.c_uint32)
     sig("etb_layout_partition_bounds", vp, C.c_uint32, vp)

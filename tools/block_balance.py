@@ -39,14 +39,20 @@ def main():
                                                  C.byref(levels)))
         r = eb.et_bfs(cg, s, stats=True, want_parent=False, want_depth=False)
         G = grid.value
+        ph = np.zeros(256, np.uint64)
+        E._check(E.lib().etb_debug_phase_stamps(cg.handle, ph.ctypes.data))
+        conv = {L: (int(ph[128 + L]) - int(ph[0])) / 1e3 for L in range(1, 64) if ph[128 + L]}
         print(f"root index {idx} trace {r.stats.direction_trace} claims {r.stats.level_claims}")
         for L in range(levels.value):
-            t = out[L * G:(L + 1) * G].astype(np.float64) / 1e3
-            t = t[t > 0]
+            t_all = out[L * G:(L + 1) * G].astype(np.float64) / 1e3
+            t = t_all[t_all > 0]
             if t.size:
+                slow = np.argsort(-t_all)[:3]
                 print(f"  L{L} {r.stats.direction_trace[L]} step-end us: min {t.min():8.1f} "
                       f"med {np.median(t):8.1f} p90 {np.percentile(t, 90):8.1f} max {t.max():8.1f}"
-                      f"   level_end {r.stats.level_ns[L + 1] / 1e3:8.1f}")
+                      f"   level_end {r.stats.level_ns[L + 1] / 1e3:8.1f}"
+                      + (f"   (list ready at {conv[L]:8.1f})" if L in conv else "")
+                      + f"   slowest CTAs {slow.tolist()}")
 
 
 if __name__ == "__main__":
