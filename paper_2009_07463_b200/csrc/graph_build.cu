@@ -12,6 +12,8 @@
 // slot becomes one 64-bit key (src << b | dst); one radix sort + one unique
 // produce all rows at once, canonical and identical to the reference.
 #include <cmath>
+#include <cstdlib>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -185,6 +187,172 @@ void finish_csr(DevBuf<uint64_t>& keys, uint64_t nkeys, uint64_t loops, uint64_t
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 
+// ---- bucketed build (large scales) --------------------------------------------
+// The key array of a whole graph is 16 B per tuple; at scale 28 that is 69 GB,
+// twice with the sort's double buffer. The generator is counter based, so the
+// tuples are cheap to regenerate: one pass histograms the directed slots by
+// source, then every bucket of source ids regenerates the tuples, keeps only its
+// slots, sorts and dedups them and appends its rows to the CSR.
+constexpr int kHistBins = 1024;
+
+__global__ void kron_hist_kernel(KronDev k, uint64_t t, int shift, unsigned long long* hist,
+                                 unsigned long long* loops) {
+  __shared__ unsigned int sh[kHistBins];
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  unsigned long long myloops = 0;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < t;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t s, d;
+    kron_tuple(k, j, s, d);
+    if (s == d) {
+      ++myloops;
+    } else {
+      atomicAdd(&sh[s >> shift], 1u);
+      atomicAdd(&sh[d >> shift], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
+  for (int o = 16; o; o >>= 1) myloops += __shfl_xor_sync(0xffffffffu, myloops, o);
+  if ((threadIdx.x & 31) == 0 && myloops) atomicAdd(loops, myloops);
+}
+
+// Keys of the directed slots whose source lies in [lo, hi), appended with one
+// atomic per CTA iteration (block-level scan).
+__global__ void __launch_bounds__(1024) kron_bucket_kernel(KronDev k, uint64_t t, uint64_t lo,
+                                                            uint64_t hi, int b, uint64_t* keys,
+                                                            unsigned long long* cnt) {
+  __shared__ unsigned int wsum[32];
+  __shared__ unsigned long long base_sh;
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < t;
+       base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = base + threadIdx.x;
+    uint64_t k0 = 0, k1 = 0;
+    unsigned c = 0;
+    if (j < t) {
+      uint64_t s, d;
+      kron_tuple(k, j, s, d);
+      if (s != d) {
+        if (s >= lo && s < hi) k0 = (s << b) | d, ++c;
+        if (d >= lo && d < hi) (c ? k1 : k0) = (d << b) | s, ++c;
+      }
+    }
+    unsigned incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wib] = incl;
+    __syncthreads();
+    if (wib == 0) {
+      unsigned x = lane < (blockDim.x >> 5) ? wsum[lane] : 0u, xi = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, xi, o);
+        if (lane >= o) xi += y;
+      }
+      wsum[lane] = xi - x;  // exclusive warp offsets
+      if (lane == 31) base_sh = xi ? atomicAdd(cnt, (unsigned long long)xi) : 0ull;
+    }
+    __syncthreads();
+    const uint64_t pos = base_sh + wsum[wib] + incl - c;
+    if (c > 0) keys[pos] = k0;
+    if (c > 1) keys[pos + 1] = k1;
+    __syncthreads();
+  }
+}
+
+// row[v] for v in [lo, hi] from a sorted unique bucket, offset by `base`.
+__global__ void bucket_rows_kernel(const uint64_t* keys, uint64_t nkeys, int b, uint64_t lo,
+                                   uint64_t hi, uint64_t base, uint64_t* row) {
+  for (uint64_t v = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= hi;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t target = v << b;
+    uint64_t a = 0, e = nkeys;
+    while (a < e) {
+      const uint64_t m = (a + e) >> 1;
+      if (keys[m] < target) a = m + 1; else e = m;
+    }
+    row[v] = base + a;
+  }
+}
+
+void build_csr_bucketed(const etb_kron_params& p, uint64_t cap_keys, DevGraph& out,
+                        uint64_t* self_loops, uint64_t* dups, cudaStream_t s) {
+  const uint64_t n = uint64_t{1} << p.scale;
+  const uint64_t t = n * p.edgefactor;
+  const int b = bits_for(n);
+  const int shift = p.scale > 10 ? static_cast<int>(p.scale) - 10 : 0;
+  const KronDev k = to_dev(p);
+  DevBuf<unsigned long long> hist(kHistBins + 2);
+  ETB_CUDA(cudaMemsetAsync(hist.get(), 0, (kHistBins + 2) * 8, s));
+  kron_hist_kernel<<<grid_for(t, 256), 256, 0, s>>>(k, t, shift, hist.get(), hist.get() + kHistBins);
+  ETB_LAUNCH_CHECK();
+  std::vector<unsigned long long> h(kHistBins + 1);
+  ETB_CUDA(cudaMemcpyAsync(h.data(), hist.get(), (kHistBins + 1) * 8, cudaMemcpyDeviceToHost, s));
+  ETB_CUDA(cudaStreamSynchronize(s));
+  const uint64_t loops = h[kHistBins];
+  if (self_loops) *self_loops = loops;
+  const uint64_t slots = 2 * (t - loops);
+  out.n = n;
+  out.row.alloc(n + 1);
+  out.col.alloc(slots ? slots : 1);
+  out.deg.alloc(n ? n : 1);
+  // buckets of whole histogram bins, each within cap_keys (a single bin may exceed it)
+  std::vector<std::pair<uint64_t, uint64_t>> buckets;  // bin ranges
+  uint64_t acc = 0, first = 0;
+  const uint64_t nbins = std::min<uint64_t>(kHistBins, (n + (uint64_t{1} << shift) - 1) >> shift);
+  for (uint64_t i = 0; i < nbins; ++i) {
+    if (acc && acc + h[i] > cap_keys) {
+      buckets.emplace_back(first, i);
+      first = i;
+      acc = 0;
+    }
+    acc += h[i];
+  }
+  buckets.emplace_back(first, nbins);
+  uint64_t maxb = 0;
+  for (auto& bk : buckets) {
+    uint64_t c = 0;
+    for (uint64_t i = bk.first; i < bk.second; ++i) c += h[i];
+    maxb = std::max(maxb, c);
+  }
+  DevBuf<uint64_t> keys(maxb ? maxb : 1), alt(maxb ? maxb : 1);
+  DevBuf<unsigned long long> cnt(1);
+  uint64_t base = 0, dropped = 0;
+  for (auto& bk : buckets) {
+    const uint64_t lo = bk.first << shift, hi = std::min(n, bk.second << shift);
+    ETB_CUDA(cudaMemsetAsync(cnt.get(), 0, 8, s));
+    kron_bucket_kernel<<<grid_for(t, 1024, 148u * 8u), 1024, 0, s>>>(k, t, lo, hi, b, keys.get(),
+                                                                    cnt.get());
+    ETB_LAUNCH_CHECK();
+    const uint64_t nk = read_u64(reinterpret_cast<uint64_t*>(cnt.get()), s);
+    sort_keys_u64(keys, alt, nk, 2 * b, s);
+    const uint64_t uniq = unique_u64(keys.get(), alt.get(), nk, s);
+    dropped += nk - uniq;
+    if (hi > lo) {
+      bucket_rows_kernel<<<grid_for(hi - lo + 1, 256), 256, 0, s>>>(alt.get(), uniq, b, lo, hi, base,
+                                                                    out.row.get());
+      ETB_LAUNCH_CHECK();
+    }
+    if (uniq) {
+      cols_kernel<<<grid_for(uniq, 256), 256, 0, s>>>(alt.get(), uniq, (uint64_t{1} << b) - 1,
+                                                       out.col.get() + base);
+      ETB_LAUNCH_CHECK();
+    }
+    base += uniq;
+  }
+  out.nnz = base;
+  if (dups) *dups = dropped / 2;
+  if (n) {
+    degree_kernel<<<grid_for(n, 256), 256, 0, s>>>(out.row.get(), n, out.deg.get());
+    ETB_LAUNCH_CHECK();
+  }
+  ETB_CUDA(cudaStreamSynchronize(s));
+}
+
 void check_n(uint64_t n) {
   if (n > kMaxDeviceVertices)
     throw std::invalid_argument("build_csr: vertex count exceeds the 32-bit device id range");
@@ -223,6 +391,18 @@ void build_csr_from_generator(const etb_kron_params& p, DevGraph& out, uint64_t*
   const uint64_t n = uint64_t{1} << p.scale;
   check_n(n);
   const uint64_t t = n * p.edgefactor;
+  // Whole-graph key sort needs ~32 B per tuple (keys + sort buffer); bucket when
+  // that does not fit comfortably (ETB_CSR_BUCKET_KEYS forces a bucket size).
+  size_t free_b = 0, total_b = 0;
+  ETB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  uint64_t cap = 0;
+  if (const char* e = std::getenv("ETB_CSR_BUCKET_KEYS")) cap = std::strtoull(e, nullptr, 10);
+  if (!cap && 2 * t * 16 + 2 * t * 4 > static_cast<uint64_t>(free_b * 0.7))
+    cap = static_cast<uint64_t>((free_b - 2 * t * 4) * 0.7) / 16;
+  if (cap) {
+    build_csr_bucketed(p, cap, out, self_loops, dups, s);
+    return;
+  }
   const int b = bits_for(n);
   DevBuf<uint64_t> keys(2 * t);
   DevBuf<unsigned long long> loops(1);

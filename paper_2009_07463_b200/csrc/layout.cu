@@ -16,6 +16,7 @@
 // Finally the core-only CSR (the core prefix of every core row) is rebuilt in
 // the new ids with one key sort; that is all the traversal reads.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -364,13 +365,15 @@ __global__ void core_count_kernel(const uint64_t* row, const uint32_t* col, cons
 
 __global__ void core_edge_keys_kernel(const uint64_t* row, const uint32_t* col, const uint8_t* type,
                                       const uint32_t* new2old, const uint32_t* old2new,
-                                      const uint64_t* crow, uint64_t nc, int b, uint64_t* keys) {
+                                      const uint64_t* crow, uint64_t lo, uint64_t hi, int b,
+                                      uint64_t* keys) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = warp; i < nc; i += nwarps) {
+  const uint64_t kbase = crow[lo];
+  for (uint64_t i = lo + warp; i < hi; i += nwarps) {
     const uint32_t o = new2old[i];
-    uint64_t pos = crow[i];
+    uint64_t pos = crow[i] - kbase;
     for (uint64_t k0 = row[o]; k0 < row[o + 1]; k0 += 32) {
       const uint64_t k = k0 + lane;
       bool keep = false;
@@ -640,17 +643,40 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
   L.cfirst.alloc(nc ? nc : 1);
   L.cmeta.alloc(nc ? nc : 1);
   if (L.ecore) {
+    // Rows sorted by one key sort of (new src << b | new dst), in buckets of
+    // consecutive rows when the whole key array (x2 for the sort) would not fit.
     const int b = bits_for(nc);
-    DevBuf<uint64_t> keys(L.ecore), alt;
-    core_edge_keys_kernel<<<wgrid(nc), 256, 0, s>>>(g.row.get(), g.col.get(), type,
-                                                    L.new2old.get(), L.old2new.get(),
-                                                    L.crow.get(), nc, b, keys.get());
-    ETB_LAUNCH_CHECK();
-    sort_keys_u64(keys, alt, L.ecore, 2 * b, s);
-    alt.release();
-    key_cols_kernel<<<grid_for(L.ecore, 256), 256, 0, s>>>(keys.get(), L.ecore,
-                                                           (uint64_t{1} << b) - 1, L.ccol.get());
-    ETB_LAUNCH_CHECK();
+    size_t free_b = 0, total_b = 0;
+    ETB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t cap = L.ecore;
+    if (const char* e = std::getenv("ETB_CSR_BUCKET_KEYS")) cap = std::strtoull(e, nullptr, 10);
+    else if (L.ecore * 16 > static_cast<uint64_t>(free_b * 0.7))
+      cap = static_cast<uint64_t>(free_b * 0.7) / 16;
+    auto crow_at = [&](uint64_t i) { return read_u64(L.crow.get() + i, s); };
+    DevBuf<uint64_t> keys, alt;
+    for (uint64_t lo = 0; lo < nc;) {
+      // largest hi with crow[hi] - crow[lo] <= cap (at least one row)
+      const uint64_t base = crow_at(lo);
+      uint64_t a = lo + 1, e = nc;
+      while (a < e) {
+        const uint64_t m = (a + e + 1) / 2;
+        if (crow_at(m) - base <= cap) a = m; else e = m - 1;
+      }
+      const uint64_t hi = a;
+      const uint64_t nk = crow_at(hi) - base;
+      if (nk) {
+        if (keys.size() < nk) keys.alloc(nk);
+        core_edge_keys_kernel<<<wgrid(hi - lo), 256, 0, s>>>(g.row.get(), g.col.get(), type,
+                                                             L.new2old.get(), L.old2new.get(),
+                                                             L.crow.get(), lo, hi, b, keys.get());
+        ETB_LAUNCH_CHECK();
+        sort_keys_u64(keys, alt, nk, 2 * b, s);
+        key_cols_kernel<<<grid_for(nk, 256), 256, 0, s>>>(keys.get(), nk, (uint64_t{1} << b) - 1,
+                                                          L.ccol.get() + base);
+        ETB_LAUNCH_CHECK();
+      }
+      lo = hi;
+    }
   }
   if (nc) {
     first_nbr_kernel<<<grid_for(nc, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), L.degn.get(),

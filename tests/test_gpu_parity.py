@@ -295,3 +295,20 @@ def test_timing_api_and_result_download(kron16):
     depth, parent = result_download(cg)
     assert depth.dtype == np.int32 and parent.dtype == np.uint32
     assert depth[int(starts[-1])] == 0 or cg.vertex_type[int(starts[-1])] >= 2
+
+
+def test_bucketed_builds_match(kron16, monkeypatch):
+    """The large-scale path (CSR and core CSR built in source buckets, as used at
+    scale 28) forced on s16 with small buckets: identical graph and layout."""
+    monkeypatch.setenv("ETB_CSR_BUCKET_KEYS", "150000")
+    csr = eb.generate_graph(scale=16, edgefactor=16, seed=1)
+    row, col, _ = csr.download()
+    assert O.fnv1a64(row) == kron16["row_fnv"] and O.fnv1a64(col) == kron16["col_fnv"]
+    assert (csr.dropped_self_loops, csr.dropped_duplicates) == (kron16["self_loops"],
+                                                                kron16["duplicates"])
+    cg = eb.relayout_csr(csr, mh=-1)
+    lay = kron16["layout"]["-1"]
+    assert O.fnv1a64(cg.new2old) == lay["new2old_fnv"]
+    ocsr = O.OracleCsr(1 << 16, O.oracle_generate(16, 16, 1))
+    for root in kron16["roots"][:8]:
+        check_root(cg, ocsr, int(root))
