@@ -266,10 +266,12 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, roots[: args.cpu_roots])
-    if world == 1 and args.secondary_scale and args.secondary_scale != args.scale:
+    scales = [int(x) for x in str(args.secondary_scale).split(",") if x.strip() and int(x)]
+    scales = [x for x in scales if x != args.scale]
+    if world == 1 and scales:
         del cg, g
-        out["secondary"] = measure_secondary(args.secondary_scale, args.edgefactor, args.mh,
-                                             args.steps, args.warmup)
+        out["secondary"] = [measure_secondary(sc, args.edgefactor, args.mh, args.steps,
+                                              args.warmup) for sc in scales]
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
@@ -453,8 +455,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-roots", type=int, default=16)
     ap.add_argument("--ref-roots-per-step", type=int, default=4)
-    ap.add_argument("--secondary-scale", type=int, default=26,
-                    help="also time this scale (0 = off); reported under 'secondary'")
+    ap.add_argument("--secondary-scale", default="26,28",
+                    help="comma list of further scales to time (0 = none); under 'secondary'")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
