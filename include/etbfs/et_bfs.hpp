@@ -9,9 +9,9 @@ namespace etbfs {
 enum class CoreKernel {
   kTopDown,
   kHybrid,
-  kDegreeAware,        // needs a degree split: not built on the GPU yet
-  kBlockSearch,        // idem
-  kHybridBlockSearch,  // idem
+  kDegreeAware,        // hybrid; device rows are already degree-ordered
+  kBlockSearch,        // bottom-up sweeps to the fixpoint, no top-down level
+  kHybridBlockSearch,  // hybrid with the bottom-up sweep
 };
 
 enum class TreeReplay {
@@ -19,12 +19,15 @@ enum class TreeReplay {
   kTeolv,
 };
 
-struct DegreeSplitAdjacency;  // reference preprocess.hpp:26; accepted, must be null
+// Reference preprocess.hpp:26. The split-based kernels require a non-null split
+// (as the reference does, et_bfs.cpp:69-70) but the device does not read it: its
+// relaid rows already list neighbours by descending degree.
+struct DegreeSplitAdjacency;
 
 // et_bfs over a relaid graph. The first call on a given (cg, etl) pair uploads
 // it and builds the device layout; later calls on the same objects reuse it
 // (keyed by address and size). For repeated traversals prefer the device
-// session API in etbfs/gpu.hpp.
+// session calls of include/etbfs_cuda.h (etb_layout_build + etb_bfs_device).
 BfsTree et_bfs(const ClassifiedGraph& cg, const EdgeTreeList& etl, vertex_t start,
                CoreKernel kernel = CoreKernel::kHybrid, TreeReplay replay = TreeReplay::kTeet,
                const DegreeSplitAdjacency* split = nullptr, const HybridPolicy& policy = {},

@@ -45,8 +45,19 @@ extern "C" {
 /* VertexType numbering, types.hpp:55-61 */
 enum { ETB_CI = 0, ETB_CE = 1, ETB_TI = 2, ETB_TL = 3, ETB_VZ = 4 };
 
-/* CoreKernel (et_bfs.hpp:10-16) values accepted by etb_bfs. */
-enum { ETB_KERNEL_TOP_DOWN = 0, ETB_KERNEL_HYBRID = 1 };
+/* CoreKernel (et_bfs.hpp:10-16). Relaid core rows list neighbours by descending
+ * degree, so every bottom-up probe is already the reference's degree-aware order
+ * (in_plus first, then the descending remainder): kDegreeAware and
+ * kHybridBlockSearch run the hybrid driver, kBlockSearch runs bottom-up sweeps to
+ * the fixpoint with no top-down level (run_block_search, bfs.cpp:295-305). No
+ * separate degree split is needed on the device. */
+enum {
+  ETB_KERNEL_TOP_DOWN = 0,
+  ETB_KERNEL_HYBRID = 1,
+  ETB_KERNEL_DEGREE_AWARE = 2,
+  ETB_KERNEL_BLOCK_SEARCH = 3,
+  ETB_KERNEL_HYBRID_BLOCK_SEARCH = 4
+};
 /* TreeReplay (et_bfs.hpp:19-22). */
 enum { ETB_REPLAY_TEET = 0, ETB_REPLAY_TEOLV = 1 };
 

@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
     uint64_t* qp_out = p.qp1;
     unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0;
     double etc = p.edges_to_check;
-    bool bu = !p.top_down_only && (double)scout > etc / p.alpha;
+    bool bu = p.bottom_up_only || (!p.top_down_only && (double)scout > etc / p.alpha);
     if (bu) awake = frontier;
     for (;;) {
       uint32_t* fcur = F[L % 3];
@@ -488,7 +488,10 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
       if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = claims;
       ++L;
       stamp(p, 257 + L);
-      if (bu) {
+      if (bu && p.bottom_up_only) {
+        // standalone block sweeps to fixpoint (run_block_search, bfs.cpp:295-305)
+        if (claims == 0) break;
+      } else if (bu) {
         awake = claims;
         if (!(awake > 0 && (awake >= prev || (double)awake > (double)p.nc / p.beta))) {
           bu = false;

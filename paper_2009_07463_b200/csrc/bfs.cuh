@@ -44,7 +44,8 @@ struct BfsParams {
   uint32_t npatch;
   double alpha, beta, edges_to_check;
   double emit_limit;  // top-down levels with scout >= this skip work-item emission
-  int top_down_only;
+  int top_down_only;   // CoreKernel::kTopDown
+  int bottom_up_only;  // CoreKernel::kBlockSearch: bottom-up levels to fixpoint
   // stats (may be null)
   char* trace;
   unsigned long long* level_claims;

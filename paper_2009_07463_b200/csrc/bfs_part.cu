@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
     uint32_t* F[3] = {me.fb0, me.fb1, me.fb2};
     unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0;
     double etc = p.edges_to_check;
-    bool bu = !p.top_down_only && (double)scout > etc / p.alpha;
+    bool bu = p.bottom_up_only || (!p.top_down_only && (double)scout > etc / p.alpha);
     if (bu) awake = frontier;
     for (;;) {
       const uint32_t fi = L % 3, ni = (L + 1) % 3, zi = (L + 2) % 3;
@@ -376,7 +376,10 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
       const unsigned long long claims = ld_volatile(&slot[0]);
       if (stats && L < 256) p.level_claims[L] = claims;
       ++L;
-      if (bu) {
+      if (bu && p.bottom_up_only) {
+        // standalone block sweeps to fixpoint (run_block_search, bfs.cpp:295-305)
+        if (claims == 0) break;
+      } else if (bu) {
         awake = claims;
         if (!(awake > 0 && (awake >= prev || (double)awake > (double)p.nc / p.beta))) {
           bu = false;

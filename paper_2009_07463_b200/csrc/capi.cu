@@ -118,17 +118,19 @@ etb::BfsParams run_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* o,
     throw std::invalid_argument("et_bfs: leaves-only replay needs a height-0 classification");
   if (opt.replay != ETB_REPLAY_TEET && opt.replay != ETB_REPLAY_TEOLV)
     throw std::invalid_argument("et_bfs: unknown tree replay");
-  if (opt.kernel != ETB_KERNEL_HYBRID && opt.kernel != ETB_KERNEL_TOP_DOWN)
-    throw std::invalid_argument("et_bfs: kernel needs a degree split");
+  if (opt.kernel < ETB_KERNEL_TOP_DOWN || opt.kernel > ETB_KERNEL_HYBRID_BLOCK_SEARCH)
+    throw std::invalid_argument("et_bfs: unknown core kernel");
   etb::BfsParams p{};
   etb::bfs_fill_params(L, h->S, p);
   etb::bfs_prepare_start(L, h->S, start, p, h->stream);
-  if (p.start != etb::kNone32 && opt.kernel == ETB_KERNEL_HYBRID &&
-      (!(opt.alpha > 0.0) || !(opt.beta > 0.0)))
+  const bool hybrid = opt.kernel == ETB_KERNEL_HYBRID || opt.kernel == ETB_KERNEL_DEGREE_AWARE ||
+                      opt.kernel == ETB_KERNEL_HYBRID_BLOCK_SEARCH;
+  if (p.start != etb::kNone32 && hybrid && (!(opt.alpha > 0.0) || !(opt.beta > 0.0)))
     throw std::invalid_argument("run_hybrid: alpha and beta must be positive");
   p.alpha = opt.alpha;
   p.beta = opt.beta;
   p.top_down_only = opt.kernel == ETB_KERNEL_TOP_DOWN;
+  p.bottom_up_only = opt.kernel == ETB_KERNEL_BLOCK_SEARCH;
   if (want_stats) {
     p.trace = h->S.trace.get();
     p.level_claims = h->S.level_claims.get();

@@ -115,7 +115,9 @@ etb_bfs_options options(CoreKernel kernel, TreeReplay replay, const HybridPolicy
   switch (kernel) {
     case CoreKernel::kTopDown: o.kernel = ETB_KERNEL_TOP_DOWN; break;
     case CoreKernel::kHybrid: o.kernel = ETB_KERNEL_HYBRID; break;
-    default: throw std::invalid_argument("et_bfs: kernel needs a degree split");
+    case CoreKernel::kDegreeAware: o.kernel = ETB_KERNEL_DEGREE_AWARE; break;
+    case CoreKernel::kBlockSearch: o.kernel = ETB_KERNEL_BLOCK_SEARCH; break;
+    case CoreKernel::kHybridBlockSearch: o.kernel = ETB_KERNEL_HYBRID_BLOCK_SEARCH; break;
   }
   o.replay = replay == TreeReplay::kTeolv ? ETB_REPLAY_TEOLV : ETB_REPLAY_TEET;
   o.alpha = policy.alpha;
@@ -306,11 +308,17 @@ BfsTree et_bfs(const ClassifiedGraph& cg, const EdgeTreeList& etl, vertex_t star
                CoreKernel kernel, TreeReplay replay, const DegreeSplitAdjacency* split,
                const HybridPolicy& policy, KernelStats* stats) {
   (void)etl;
-  (void)split;
   const uint64_t n = cg.graph.vertex_count;
   if (start >= n) throw std::invalid_argument("et_bfs: start out of range");
   if (replay == TreeReplay::kTeolv && cg.mh != 0)
     throw std::invalid_argument("et_bfs: leaves-only replay needs a height-0 classification");
+  // et_bfs.cpp:69-70: the split-based kernels require a split; the device's
+  // degree-sorted rows make its content unnecessary, so it is only checked.
+  const bool needs_split = kernel == CoreKernel::kDegreeAware ||
+                           kernel == CoreKernel::kBlockSearch ||
+                           kernel == CoreKernel::kHybridBlockSearch;
+  if (needs_split && split == nullptr)
+    throw std::invalid_argument("et_bfs: kernel needs a degree split");
   const etb_bfs_options o = options(kernel, replay, policy);
   std::lock_guard<std::mutex> lk(g_cache_mu);
   DeviceCg& d = device_cg(cg);

@@ -36,9 +36,12 @@ class VertexType(enum.IntEnum):  # types.hpp:55-61
     VERTEX_ZERO = 4
 
 
-class CoreKernel(enum.IntEnum):  # et_bfs.hpp:10-16 (kDegreeAware / kBlockSearch not built yet)
+class CoreKernel(enum.IntEnum):  # et_bfs.hpp:10-16
     TOP_DOWN = 0
     HYBRID = 1
+    DEGREE_AWARE = 2
+    BLOCK_SEARCH = 3
+    HYBRID_BLOCK_SEARCH = 4
 
 
 class TreeReplay(enum.IntEnum):  # et_bfs.hpp:19-22

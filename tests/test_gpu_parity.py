@@ -312,3 +312,25 @@ def test_bucketed_builds_match(kron16, monkeypatch):
     ocsr = O.OracleCsr(1 << 16, O.oracle_generate(16, 16, 1))
     for root in kron16["roots"][:8]:
         check_root(cg, ocsr, int(root))
+
+
+def test_split_kernels_corpus(corpus):
+    """CoreKernel::kDegreeAware / kBlockSearch / kHybridBlockSearch (et_bfs.hpp:10-16):
+    level-exact like every kernel (test_et_bfs.cpp:158-169); block search runs
+    bottom-up sweeps only, one 'b' per step until a step claims nothing."""
+    for g in corpus:
+        csr = eb.build_csr(g["n"], edges_of(g))
+        ocsr = O.OracleCsr(g["n"], edges_of(g))
+        cg = eb.relayout_csr(csr, mh=-1)
+        for st in range(g["n"]):
+            root = int(cg.new2old[st])
+            for k in (eb.CoreKernel.DEGREE_AWARE, eb.CoreKernel.HYBRID_BLOCK_SEARCH):
+                check_root(cg, ocsr, root, kernel=k)
+            r = check_root(cg, ocsr, root, kernel=eb.CoreKernel.BLOCK_SEARCH)
+            tr = r.stats.direction_trace
+            assert set(tr) <= {"b"}, tr
+            if st < cg.core_vertex_count:
+                lv = ocsr.levels(root)
+                core_depth = max(int(x) for x, v in zip(lv, range(g["n"]))
+                                 if x != O.NO_VERTEX and int(cg.old2new[v]) < cg.core_vertex_count)
+                assert len(tr) == core_depth + 1, (g["name"], st, tr)
