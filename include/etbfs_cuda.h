@@ -206,6 +206,9 @@ int etb_debug_block_stamps(etb_layout* L, uint64_t start, uint64_t* out, uint64_
  * init end, [2 + L] level L end, [128 + L] conversion before level L end,
  * [255] replay end). */
 int etb_debug_phase_stamps(etb_layout* L, uint64_t* out256);
+/* Diagnostics: median event-timed duration (us) of an empty kernel launched
+ * like the traversal (same grid, block, shared memory, cooperative). */
+int etb_debug_launch_floor(etb_layout* L, int iters, double* empty_us);
 
 /* ---- measurement ---------------------------------------------------------- */
 /* Times etb_bfs_device per start with CUDA events on the layout's stream, after

@@ -21,6 +21,7 @@
 //                   host and applied as a patch.
 // Levels are separated by a grid barrier; the grid is one wave of co-resident
 // CTAs (cooperative launch).
+#include <cstdlib>
 #include <algorithm>
 
 #include "bfs_dev.cuh"
@@ -30,14 +31,16 @@ namespace {
 
 using namespace dev;
 
-constexpr int kBlock = 1024;  // one CTA per SM: half the grid-barrier arrivals of 2 x 512
-constexpr int kWarps = kBlock / 32;
+// One CTA per SM, 768 or 1024 threads (et_bfs_kernel<B>): 768 leaves 80
+// registers per thread and is faster on latency-bound levels (small cores),
+// 1024 keeps more bottom-up probes in flight (large cores); see block_for().
+constexpr int kMaxWarps = 32;
 constexpr int kItemShift = 36;
 constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 
 constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down chunk
 constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex ids)
-constexpr int kBuU = 4;              // visited words per warp per bottom-up iteration
+constexpr int kBuU = 8;              // visited words per warp per bottom-up iteration
 constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab
 
 struct WarpSmem {
@@ -46,8 +49,8 @@ struct WarpSmem {
 };
 
 struct Smem {
-  WarpSmem w[kWarps];
-  unsigned long long red[kWarps];
+  WarpSmem w[kMaxWarps];
+  unsigned long long red[2][kMaxWarps];
 };
 
 // Phase timestamps for stats (block 0 / thread 0): [256] entry, [257] after
@@ -57,15 +60,29 @@ __device__ __forceinline__ void stamp(const BfsParams& p, uint32_t slot) {
     p.level_claims[slot] = gtimer();
 }
 
-__device__ void block_add(unsigned long long v, unsigned long long* dst, Smem& sm) {
+// Block-reduce a (and b), add the CTA totals to da (and db), then the grid
+// barrier: one bar.sync pair per level instead of three. Thread 0 both adds and
+// arrives, so its release add publishes the totals with the CTA's writes.
+__device__ void grid_sync_add(unsigned long long* bar, Smem& sm, unsigned long long a,
+                              unsigned long long* da, unsigned long long b,
+                              unsigned long long* db) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  v = warp_sum(v);
-  if (lane == 0) sm.red[wib] = v;
+  a = warp_sum(a);
+  if (db) b = warp_sum(b);
+  if (lane == 0) {
+    sm.red[0][wib] = a;
+    sm.red[1][wib] = b;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
-    v = lane < kWarps ? sm.red[lane] : 0ull;
-    v = warp_sum(v);
-    if (lane == 0 && v) atomicAdd(dst, v);
+    const unsigned nwb = blockDim.x >> 5;
+    a = warp_sum(lane < nwb ? sm.red[0][lane] : 0ull);
+    if (db) b = warp_sum(lane < nwb ? sm.red[1][lane] : 0ull);
+    if (lane == 0) {
+      if (a) atomicAdd(da, a);
+      if (db && b) atomicAdd(db, b);
+      grid_arrive_wait(bar);
+    }
   }
   __syncthreads();
 }
@@ -129,8 +146,8 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
                         int32_t dnext, bool emit, unsigned long long& scout_acc,
                         unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
-  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   const uint64_t nu = (ne + kTdChunk - 1) / kTdChunk;
   for (uint64_t g0 = gw, gn = 1; g0 < nu;) {
@@ -310,8 +327,8 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
 __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
-  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
   for (uint64_t w0 = gw * kBuU; w0 < p.nwords; w0 += nw * kBuU) {
@@ -360,8 +377,8 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
 __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t* qv_out,
                              uint64_t* qp_out, unsigned long long* cslot) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
-  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
   for (uint64_t w0 = gw * 32; w0 < p.nwords; w0 += nw * 32) {
     const uint64_t wi = w0 + lane;
     const uint32_t bits = wi < p.nwords ? fcur[wi] : 0u;
@@ -397,7 +414,7 @@ __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t*
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
+__device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -469,7 +486,6 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
       if (bu) {
         prev = awake;
         bu_step(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc);
-        block_add(claims_acc, &slot[3], sm);
       } else {
         etc -= (double)scout;
         // The next frontier list is emitted only when this frontier's edge count
@@ -479,11 +495,9 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
         list_valid = emit;
         td_step(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_in, qp_in, nq, ne,
                 qv_out, qp_out, fnext, slot, dnext, emit, scout_acc, claims_acc);
-        block_add(scout_acc, &slot[1], sm);
-        block_add(claims_acc, &slot[3], sm);
       }
       if (p.bstamp && threadIdx.x == 0 && L < 64) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
-      grid_sync(p.bar);
+      grid_sync_add(p.bar, sm, claims_acc, &slot[3], scout_acc, bu ? nullptr : &slot[1]);
       const unsigned long long claims = ld_volatile(&slot[3]);
       if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = claims;
       ++L;
@@ -532,10 +546,18 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
   if (tid == 0 && p.nlevels) *p.nlevels = L;
 
   // ---- unreached core vertices + tree replay + start-tree patch ----------------
-  for (uint64_t wi = tid; wi < p.nwords; wi += nthreads) {
-    for (uint32_t un = ~p.visited[wi]; un; un &= un - 1) {  // padding bits are set
-      const uint64_t v = wi * 32 + __ffs(un) - 1;
-      p.dp[v] = make_uint2(kNone32, kNone32);
+  {
+    // A warp reads 32 visited words, then clears the unreached vertices of each
+    // word with one coalesced 256-byte store (padding bits are set).
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t gw = tid >> 5, nw = nthreads >> 5;
+    for (uint64_t w0 = gw * 32; w0 < p.nwords; w0 += nw * 32) {
+      const uint32_t un = w0 + lane < p.nwords ? ~p.visited[w0 + lane] : 0u;
+      for (unsigned m = __ballot_sync(0xffffffffu, un != 0); m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        if ((__shfl_sync(0xffffffffu, un, j) >> lane) & 1u)
+          p.dp[(w0 + j) * 32 + lane] = make_uint2(kNone32, kNone32);
+      }
     }
   }
   for (uint64_t t0 = tid; t0 < p.nt; t0 += 4 * nthreads) {
@@ -570,7 +592,29 @@ __global__ void __launch_bounds__(kBlock, 1) et_bfs_kernel(BfsParams p) {
   stamp(p, 511);
 }
 
+template <int B>
+__global__ void __launch_bounds__(B, 1) et_bfs_kernel(BfsParams p) {
+  et_bfs_body(p);
+}
+
 }  // namespace
+
+const void* kernel_for(int block) {
+  return block == 768 ? reinterpret_cast<const void*>(et_bfs_kernel<768>)
+                      : reinterpret_cast<const void*>(et_bfs_kernel<1024>);
+}
+
+// Measured on B200 (tools/root_profile.py, 64 roots): 768 threads win at
+// scale 22 (102 vs 109 us per root), 1024 at scale 26 (632 vs 655 us); even
+// at scale 24 (core ~10M vertices).
+// ETB_BFS_BLOCK=768|1024 overrides (experiments).
+int block_for(uint64_t nc) {
+  if (const char* e = getenv("ETB_BFS_BLOCK")) {
+    const int b = atoi(e);
+    if (b == 768 || b == 1024) return b;
+  }
+  return nc < (uint64_t{1} << 23) ? 768 : 1024;
+}
 
 void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   const uint64_t n = L.n;
@@ -602,13 +646,13 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   int dev = 0, sms = 0, per_sm = 0;
   ETB_CUDA(cudaGetDevice(&dev));
   ETB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  ETB_CUDA(cudaFuncSetAttribute(et_bfs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  S.block = block_for(L.nc);
+  const void* k = kernel_for(S.block);
+  ETB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(Smem)));
-  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, et_bfs_kernel, kBlock,
-                                                         sizeof(Smem)));
+  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S.block, sizeof(Smem)));
   if (per_sm < 1) throw CudaError("et_bfs_kernel cannot be resident");
-  S.block = kBlock;
-  S.grid = sms * std::min(per_sm, 2048 / kBlock);
+  S.grid = sms;  // one CTA per SM (the level barrier's arrivals)
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -733,10 +777,21 @@ void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParam
   }
 }
 
+__global__ void __launch_bounds__(1024, 1) empty_kernel(unsigned long long* sink) {
+  if (sink && threadIdx.x == 0 && blockIdx.x == 0) *sink = 0;
+}
+
+void empty_launch(const BfsState& S, cudaStream_t s) {
+  unsigned long long* sink = nullptr;
+  void* args[] = {&sink};
+  ETB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(empty_kernel), dim3(S.grid),
+                                       dim3(S.block), args, sizeof(Smem), s));
+}
+
 void bfs_launch(const BfsParams& p, const BfsState& S, cudaStream_t s) {
   void* args[] = {const_cast<BfsParams*>(&p)};
-  ETB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(et_bfs_kernel), dim3(S.grid),
-                                       dim3(S.block), args, sizeof(Smem), s));
+  ETB_CUDA(cudaLaunchCooperativeKernel(kernel_for(S.block), dim3(S.grid), dim3(S.block), args,
+                                       sizeof(Smem), s));
 }
 
 }  // namespace etb

@@ -78,6 +78,7 @@ struct BfsState {
 };
 
 void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s);
+void empty_launch(const BfsState& S, cudaStream_t s);  // launch-cost floor (diagnostics)
 void bfs_launch(const BfsParams& p, const BfsState& S, cudaStream_t s);
 // Fills depth/parent of the start's tree on the host (traverse_return_core_edge,
 // et_bfs.cpp:34-57) and returns the core vertex to start from (kNone32 if the

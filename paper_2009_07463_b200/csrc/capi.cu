@@ -2,6 +2,7 @@
 // exceptions into status codes: std::invalid_argument -> ETB_EINVAL (the
 // reference's caller errors, same messages), std::runtime_error ->
 // ETB_ERUNTIME, CUDA failures -> ETB_ECUDA.
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -626,6 +627,26 @@ int etb_debug_block_stamps(etb_layout* h, uint64_t start, uint64_t* out, uint64_
     for (uint64_t i = 0; i < std::min<uint64_t>(cap, 64 * g); ++i) out[i] = hs[i] ? hs[i] - t0 : 0;
     if (grid) *grid = static_cast<uint32_t>(g);
     if (levels) *levels = nl;
+  });
+}
+
+int etb_debug_launch_floor(etb_layout* h, int iters, double* empty_us) {
+  return guarded([&] {
+    need(h, "etb_debug_launch_floor");
+    need(empty_us, "etb_debug_launch_floor");
+    ETB_CUDA(cudaSetDevice(h->device));
+    std::vector<float> t;
+    for (int i = 0; i < std::max(iters, 1) + 3; ++i) {
+      ETB_CUDA(cudaEventRecord(h->ev[2], h->stream));
+      etb::empty_launch(h->S, h->stream);
+      ETB_CUDA(cudaEventRecord(h->ev[1], h->stream));
+      ETB_CUDA(cudaEventSynchronize(h->ev[1]));
+      float ms = 0.f;
+      ETB_CUDA(cudaEventElapsedTime(&ms, h->ev[2], h->ev[1]));
+      if (i >= 3) t.push_back(ms);
+    }
+    std::sort(t.begin(), t.end());
+    *empty_us = t[t.size() / 2] * 1e3;
   });
 }
 

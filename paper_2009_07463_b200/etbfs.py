@@ -21,7 +21,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "lib", "libetbfs_b200.so")
+# ETB_LIB points at another build of the same library (A/B kernel experiments).
+_LIB_PATH = os.environ.get("ETB_LIB") or os.path.join(HERE, "lib", "libetbfs_b200.so")
 
 NO_VERTEX = np.uint64(0xFFFFFFFFFFFFFFFF)  # types.hpp:13 kNoVertex
 
@@ -164,6 +165,7 @@ def lib() -> C.CDLL:
     sig("etb_result_traversed_edges", vp, P64)
     sig("etb_result_validate", vp, u64, vp)
     sig("etb_debug_phase_stamps", vp, vp)
+    sig("etb_debug_launch_floor", vp, i32, C.POINTER(C.c_double))
     sig("etb_debug_block_stamps", vp, u64, vp, u64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32))
     sig("etb_layout_partition", vp, C.c_uint32)
     sig("etb_layout_partition_bounds", vp, C.c_uint32, vp)

@@ -44,6 +44,18 @@ def main():
                "claims": r.stats.level_claims, "level_us": dur}
         out.append(rec)
         print(json.dumps(rec), flush=True)
+    # Fixed cost: a start on an isolated vertex runs init + tree replay only.
+    vz = np.nonzero(np.asarray(cg.vertex_type) == 4)[0]
+    if vz.size:
+        s = int(vz[0])
+        _, fk = E.time_roots(cg, np.full(32, s, dtype=np.uint64), warmup=4, flush_l2=True)
+        r = eb.et_bfs(cg, s, stats=True, want_parent=False, want_depth=False)
+        print(json.dumps({"floor_kernel_us": round(float(np.median(fk)) * 1e3, 1),
+                          "floor_device_us": round(r.stats.total_ns / 1e3, 1)}))
+    import ctypes as C
+    eu = C.c_double()
+    E._check(E.lib().etb_debug_launch_floor(cg.handle, 32, C.byref(eu)))
+    print(json.dumps({"empty_kernel_us": round(eu.value, 1)}))
     k = np.array([o["kernel_us"] for o in out])
     print(json.dumps({"kernel_us_mean": float(k.mean()), "kernel_us_max": float(k.max()),
                       "kernel_us_min": float(k.min())}))
