@@ -41,7 +41,7 @@ constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down chunk
 constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex ids)
 constexpr int kBuU = 8;              // visited words per warp per bottom-up iteration
-constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab
+constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab on long levels
 
 struct WarpSmem {
   uint32_t cbuf[kCbuf];     // staged claims (top-down); with win: deferred misses (bottom-up)
@@ -51,6 +51,7 @@ struct WarpSmem {
 struct Smem {
   WarpSmem w[kMaxWarps];
   unsigned long long red[2][kMaxWarps];
+  unsigned long long tot[4];  // level totals read once per CTA after the barrier
 };
 
 // Phase timestamps for stats (block 0 / thread 0): [256] entry, [257] after
@@ -62,12 +63,15 @@ __device__ __forceinline__ void stamp(const BfsParams& p, uint32_t slot) {
 
 // Block-reduce a (and b), add the CTA totals to da (and db), then the grid
 // barrier: one bar.sync pair per level instead of three. Thread 0 both adds and
-// arrives, so its release add publishes the totals with the CTA's writes.
+// arrives, so its release add publishes the totals with the CTA's writes; after
+// the barrier it alone reads the n level totals at rd (one L2 request per CTA
+// instead of one per warp: same-address requests serialise in the L2 slice)
+// and hands them to the CTA in sm.tot.
 __device__ void grid_sync_add(unsigned long long* bar, Smem& sm, unsigned long long a,
                               unsigned long long* da, unsigned long long b,
-                              unsigned long long* db) {
+                              unsigned long long* db, const unsigned long long* rd, int n) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  a = warp_sum(a);
+  if (da) a = warp_sum(a);
   if (db) b = warp_sum(b);
   if (lane == 0) {
     sm.red[0][wib] = a;
@@ -76,12 +80,13 @@ __device__ void grid_sync_add(unsigned long long* bar, Smem& sm, unsigned long l
   __syncthreads();
   if (threadIdx.x < 32) {
     const unsigned nwb = blockDim.x >> 5;
-    a = warp_sum(lane < nwb ? sm.red[0][lane] : 0ull);
+    if (da) a = warp_sum(lane < nwb ? sm.red[0][lane] : 0ull);
     if (db) b = warp_sum(lane < nwb ? sm.red[1][lane] : 0ull);
     if (lane == 0) {
-      if (a) atomicAdd(da, a);
+      if (da && a) atomicAdd(da, a);
       if (db && b) atomicAdd(db, b);
       grid_arrive_wait(bar);
+      for (int k = 0; k < n; ++k) sm.tot[k] = ld_volatile(&rd[k]);
     }
   }
   __syncthreads();
@@ -91,7 +96,8 @@ __device__ void grid_sync_add(unsigned long long* bar, Smem& sm, unsigned long l
 // exclusive prefix qp[] of their core degrees (ne = total edges). A top-down
 // level cuts the concatenated rows into 256-edge chunks (merge path): hub rows
 // span many chunks, tiny rows share one, and every chunk is the same work. Each
-// warp takes one chunk, then pulls batches of kGrab from a per-level counter.
+// warp takes one chunk, then pulls more from a per-level counter: one at a
+// time on levels of at most 8 chunks per warp, kGrab at a time on longer ones.
 // Claims append (vertex, edge prefix) with one packed atomic per staged batch:
 // slot[0] = (list length << 36) | edges returns both positions at once.
 
@@ -235,9 +241,12 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
     }
     if (nu <= nw) break;
     unsigned long long next = 0;
-    if (lane == 0) next = nw + atomicAdd(&slot[2], (unsigned long long)kGrab);
+    // single chunks when the level is only a few chunks per warp (balance),
+    // batches when it is long (fewer atomics on the shared counter)
+    const uint64_t want = nu <= 8 * nw ? 1 : kGrab;
+    if (lane == 0) next = nw + atomicAdd(&slot[2], (unsigned long long)want);
     g0 = __shfl_sync(0xffffffffu, next, 0);
-    gn = kGrab;
+    gn = want;
   }
 }
 
@@ -273,9 +282,42 @@ __device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcu
 constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (the claim buffer + the window)
 constexpr uint32_t kLaneScan = 64;
 
+// Bottom-up list emission (a level predicted to hand over to top-down): the
+// warp appends its claims, up to K per lane, to the next frontier list with one
+// packed atomic, so the level after it needs no bitmap -> list conversion.
+template <int K>
+__device__ __forceinline__ void bu_append(const uint32_t (&v)[K], const uint32_t (&d)[K],
+                                          uint32_t* qv_out, uint64_t* qp_out,
+                                          unsigned long long* lslot) {
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t c = 0;
+  unsigned long long e = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    c += d[k] != 0;
+    e += d[k];
+  }
+  if (!__any_sync(0xffffffffu, c != 0)) return;
+  const uint32_t cin = warp_incl_scan(c);
+  const unsigned long long ein = warp_incl_scan64(e);
+  unsigned long long old = 0;
+  if (lane == 31) old = atomicAdd(lslot, ((unsigned long long)cin << kItemShift) | ein);
+  old = __shfl_sync(0xffffffffu, old, 31);
+  uint64_t vpos = (old >> kItemShift) + cin - c, epos = (old & kItemMask) + ein - e;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (!d[k]) continue;
+    qv_out[vpos] = v[k];
+    qp_out[vpos] = epos;
+    ++vpos;
+    epos += d[k];
+  }
+}
+
 __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext,
                                uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
-                               unsigned long long& claims_acc) {
+                               unsigned long long& claims_acc, uint32_t* qv_out,
+                               uint64_t* qp_out, unsigned long long* lslot) {
   const unsigned lane = threadIdx.x & 31;
   __syncwarp();
   uint32_t nlong = 0;
@@ -283,9 +325,10 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
     const uint32_t i = i0 + lane;
     const uint32_t v = i < nmiss ? mbuf[i] : kNone32;
     bool lng = false, hit = false;
-    uint32_t par = 0;
+    uint32_t par = 0, cd = 0;
     if (v != kNone32) {
-      if (p.cmeta[v].x > kLaneScan) lng = true;
+      cd = p.cmeta[v].x;
+      if (cd > kLaneScan) lng = true;
       else hit = scan_row(p, fcur, v, par);
     }
     if (hit) {
@@ -293,6 +336,10 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
       atomicOr(&p.visited[v >> 5], 1u << (v & 31));
       atomicOr(&fnext[v >> 5], 1u << (v & 31));
       ++claims_acc;
+    }
+    if (lslot) {
+      const uint32_t av[1] = {v}, ad[1] = {hit ? cd : 0u};
+      bu_append<1>(av, ad, qv_out, qp_out, lslot);
     }
     // compact long rows to the front of the buffer (slots < i0 are consumed)
     const unsigned lm = __ballot_sync(0xffffffffu, lng);
@@ -320,12 +367,17 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
       atomicOr(&fnext[v >> 5], 1u << (v & 31));
       ++claims_acc;
     }
+    if (lslot) {
+      const uint32_t av[1] = {v}, ad[1] = {lane == 0 && par != kNone32 ? p.cmeta[v].x : 0u};
+      bu_append<1>(av, ad, qv_out, qp_out, lslot);
+    }
   }
   __syncwarp();
 }
 
 __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur,
-                        uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc) {
+                        uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
+                        uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
@@ -364,12 +416,21 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
       if (miss) mbuf[nmiss + __popc(mm & lt)] = v;
       nmiss += __popc(mm);
     }
+    if (lslot) {
+      uint32_t av[kBuU], ad[kBuU];
+#pragma unroll
+      for (int k = 0; k < kBuU; ++k) {
+        av[k] = static_cast<uint32_t>((w0 + k) * 32 + lane);
+        ad[k] = hit[k] ? p.cmeta[av[k]].x : 0u;
+      }
+      bu_append<kBuU>(av, ad, qv_out, qp_out, lslot);
+    }
     if (nmiss > kMissCap - 32 * kBuU) {
-      resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
+      resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
       nmiss = 0;
     }
   }
-  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc);
+  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
 }
 
 // Frontier bitmap -> frontier list (when a top-down level follows one that did
@@ -460,7 +521,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     uint32_t* qv_out = p.qv1;
     uint64_t* qp_in = p.qp0;
     uint64_t* qp_out = p.qp1;
-    unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0;
+    unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0, reached = 1;
     double etc = p.edges_to_check;
     bool bu = p.bottom_up_only || (!p.top_down_only && (double)scout > etc / p.alpha);
     if (bu) awake = frontier;
@@ -483,9 +544,18 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
       bool list_valid = true;
       // (A smem copy of the probed bitmap's hot prefix was tried and measured
       // slower: the 64 KB it takes comes out of L1, which caches those lines.)
+      bool bu_list = false;
       if (bu) {
         prev = awake;
-        bu_step(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc);
+        // Emit the next list when this level is all but certain to be the last
+        // bottom-up one: the vertices it can still claim (core minus reached)
+        // already fit under the beta bound, so only awake >= prev keeps it.
+        // (Measured: limiting it to levels with few claims left, to spare the
+        // list-counter atomics, was slower overall at scales 22 and 26.)
+        bu_list = !p.bottom_up_only && !p.top_down_only &&
+                  (double)(p.nc - reached) <= (double)p.nc / p.beta;
+        bu_step(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in, qp_in,
+                bu_list ? &slot[0] : nullptr);
       } else {
         etc -= (double)scout;
         // The next frontier list is emitted only when this frontier's edge count
@@ -497,8 +567,11 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
                 qv_out, qp_out, fnext, slot, dnext, emit, scout_acc, claims_acc);
       }
       if (p.bstamp && threadIdx.x == 0 && L < 64) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
-      grid_sync_add(p.bar, sm, claims_acc, &slot[3], scout_acc, bu ? nullptr : &slot[1]);
-      const unsigned long long claims = ld_volatile(&slot[3]);
+      grid_sync_add(p.bar, sm, claims_acc, &slot[3], scout_acc, bu ? nullptr : &slot[1], slot, 4);
+      const unsigned long long packed = sm.tot[0];
+      const unsigned long long scout_tot = sm.tot[1];
+      const unsigned long long claims = sm.tot[3];
+      reached += claims;
       if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = claims;
       ++L;
       stamp(p, 257 + L);
@@ -511,12 +584,15 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           bu = false;
           frontier = awake;
           scout = 1;
-          list_valid = false;
+          list_valid = bu_list;
+          if (bu_list) {
+            nq = packed >> kItemShift;
+            ne = packed & kItemMask;
+          }
         }
       } else {
         frontier = claims;
-        scout = ld_volatile(&slot[1]);
-        const unsigned long long packed = ld_volatile(&slot[0]);
+        scout = scout_tot;
         nq = packed >> kItemShift;
         ne = packed & kItemMask;
         uint32_t* tv = qv_in;
@@ -534,9 +610,9 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         } else if (!list_valid) {
           unsigned long long* cslot = p.ctr + 16 + (L & 1);
           convert_step(p, F[L % 3], qv_in, qp_in, cslot);
-          grid_sync(p.bar);
+          grid_sync_add(p.bar, sm, 0, nullptr, 0, nullptr, cslot, 1);
           stamp(p, 384 + L);  // diagnostics: end of the bitmap -> list conversion
-          const unsigned long long cp = ld_volatile(cslot);
+          const unsigned long long cp = sm.tot[0];
           nq = cp >> kItemShift;
           ne = cp & kItemMask;
         }

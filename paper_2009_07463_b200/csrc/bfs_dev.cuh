@@ -68,6 +68,15 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   return x;
 }
 
+__device__ __forceinline__ unsigned long long warp_incl_scan64(unsigned long long x) {
+  const unsigned lane = threadIdx.x & 31;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
 // Index of the last list entry whose chunk prefix is <= unit (32-ary search).
 inline __device__ uint64_t find_vertex(const uint64_t* qp, uint64_t nq, uint64_t unit) {
   const unsigned lane = threadIdx.x & 31;
