@@ -150,7 +150,7 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
                         const uint64_t* qp, uint64_t nq, uint64_t ne, uint32_t* qv_out,
                         uint64_t* qp_out, uint32_t* fnext, unsigned long long* slot,
                         int32_t dnext, bool emit, unsigned long long& scout_acc,
-                        unsigned long long& claims_acc) {
+                        unsigned long long& claims_acc, uint32_t root) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
@@ -158,11 +158,12 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
   const uint64_t nu = (ne + kTdChunk - 1) / kTdChunk;
   for (uint64_t g0 = gw, gn = 1; g0 < nu;) {
     const uint64_t g1 = min(nu, g0 + gn);
-    uint64_t i = find_vertex(qp, nq, g0 * kTdChunk);
+    // root != kNone32: the first level, whose list is the start alone (not stored)
+    uint64_t i = root != kNone32 ? 0 : find_vertex(qp, nq, g0 * kTdChunk);
     for (uint64_t c = g0; c < g1; ++c) {
       const uint64_t e0 = c * kTdChunk, e1 = min(ne, e0 + kTdChunk);
-      const uint64_t qi = qp[i];
-      const uint64_t iend = i + 1 < nq ? qp[i + 1] : ne;
+      const uint64_t qi = root != kNone32 ? 0 : qp[i];
+      const uint64_t iend = root != kNone32 ? ne : (i + 1 < nq ? qp[i + 1] : ne);
       const bool single = iend >= e1;
       uint64_t inext;
       if (!single) {
@@ -189,7 +190,7 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
         const uint32_t rel = lane + 32 * j;
         if (!single)
           while (k + 1 < kTdChunk && win[k + 1] <= static_cast<int32_t>(rel)) ++k;
-        u[j] = rel < e1 - e0 ? (single ? qv[i] : qv[i + k]) : kNone32;
+        u[j] = rel < e1 - e0 ? (single ? (root != kNone32 ? root : qv[i]) : qv[i + k]) : kNone32;
         w[j] = static_cast<uint32_t>(k);  // relative vertex index for now
       }
 #pragma unroll
@@ -483,34 +484,28 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
   const uint32_t start = p.start;
   const bool run_core = start != kNone32;
   stamp(p, 256);
+  // diagnostics: per-CTA entry (slot 62) and exit (slot 63) times
+  if (p.bstamp && threadIdx.x == 0) p.bstamp[62 * gridDim.x + blockIdx.x] = gtimer();
 
-  // ---- init: core-sized state only (the reference allocates n-sized state,
-  // et_bfs.cpp:82,96) --------------------------------------------------------
-  const uint32_t tail = p.nc & 31u;
-  for (uint64_t i = tid; i < p.nwords; i += nthreads) {
-    uint32_t vis = 0, f0 = 0;
-    if (i == p.nwords - 1 && tail) vis = ~0u << tail;  // padding reads as visited
-    if (run_core && i == (start >> 5)) {
-      vis |= 1u << (start & 31);
-      f0 = 1u << (start & 31);
-    }
-    p.visited[i] = vis;
-    p.fb0[i] = f0;
-    p.fb1[i] = 0;
-    p.fb2[i] = 0;
-  }
-  if (tid < 24) p.ctr[tid] = 0;
+  // ---- start: the state halves were cleaned by the previous traversal (or at
+  // layout setup); only the start's bits are set. Core-sized state only (the
+  // reference allocates n-sized state, et_bfs.cpp:82,96) --------------------------
   uint64_t nq = 0, ne = 0;  // frontier list length and its edge count
   if (run_core) {
     ne = p.cmeta[start].x;
     nq = ne != 0;
     if (tid == 0) {
-      p.qv0[0] = start;
-      p.qp0[0] = 0;
+      atomicOr(&p.visited[start >> 5], 1u << (start & 31));
+      p.fb0[start >> 5] = 1u << (start & 31);
       p.dp[start] = make_uint2(static_cast<uint32_t>(p.base_depth), p.start_parent);
     }
   }
-  grid_sync(p.bar);
+  const bool bu0 = run_core && (p.bottom_up_only ||
+                                (!p.top_down_only &&
+                                 (double)p.degn[start] > p.edges_to_check / p.alpha));
+  // A top-down first level reads only the start's row (no list, no start bit);
+  // a bottom-up one probes fb0, so it waits for the start bit.
+  if (bu0) grid_sync(p.bar);
   stamp(p, 257);
 
   // ---- level loop: run_hybrid (bfs.cpp:232-293) ---------------------------------
@@ -523,7 +518,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     uint64_t* qp_out = p.qp1;
     unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0, reached = 1;
     double etc = p.edges_to_check;
-    bool bu = p.bottom_up_only || (!p.top_down_only && (double)scout > etc / p.alpha);
+    bool bu = bu0;
     if (bu) awake = frontier;
     for (;;) {
       uint32_t* fcur = F[L % 3];
@@ -564,9 +559,10 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         const bool emit = (double)scout < p.emit_limit;
         list_valid = emit;
         td_step(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_in, qp_in, nq, ne,
-                qv_out, qp_out, fnext, slot, dnext, emit, scout_acc, claims_acc);
+                qv_out, qp_out, fnext, slot, dnext, emit, scout_acc, claims_acc,
+                L == 0 ? start : kNone32);
       }
-      if (p.bstamp && threadIdx.x == 0 && L < 64) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
+      if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
       grid_sync_add(p.bar, sm, claims_acc, &slot[3], scout_acc, bu ? nullptr : &slot[1], slot, 4);
       const unsigned long long packed = sm.tot[0];
       const unsigned long long scout_tot = sm.tot[1];
@@ -665,7 +661,21 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     const uint32_t v = p.patch[3 * i];
     p.dp[v] = make_uint2(p.patch[3 * i + 1], p.patch[3 * i + 2]);
   }
+  // ---- clean the other state half for the next traversal --------------------
+  {
+    const uint32_t tail = p.nc & 31u;
+    for (uint64_t i = tid; i < p.nwords; i += nthreads) {
+      p.visited_next[i] = (i == p.nwords - 1 && tail) ? ~0u << tail : 0u;  // padding: visited
+      p.fb0_next[i] = 0;
+      p.fb1_next[i] = 0;
+    }
+    if (tid < 32) p.ctr_next[tid] = 0;
+  }
   stamp(p, 511);
+  if (p.bstamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) p.bstamp[63 * gridDim.x + blockIdx.x] = gtimer();
+  }
 }
 
 template <int B>
@@ -696,16 +706,31 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   const uint64_t n = L.n;
   S.n = n;
   const uint64_t words = (L.nc + 31) / 32 + 1;
-  S.visited.alloc(words);
-  S.fb0.alloc(words);
-  S.fb1.alloc(words);
+  S.words = words;
+  S.visited.alloc(2 * words);
+  S.fb0.alloc(2 * words);
+  S.fb1.alloc(2 * words);
   S.fb2.alloc(words);
   const uint64_t cap = L.nc + 2;
   S.qv0.alloc(cap);
   S.qv1.alloc(cap);
   S.qp0.alloc(cap);
   S.qp1.alloc(cap);
-  S.ctr.alloc(32);
+  S.ctr.alloc(64);
+  // both halves clean: visited zero but the last word's padding bits
+  ETB_CUDA(cudaMemsetAsync(S.visited.get(), 0, 2 * words * 4, s));
+  ETB_CUDA(cudaMemsetAsync(S.fb0.get(), 0, 2 * words * 4, s));
+  ETB_CUDA(cudaMemsetAsync(S.fb1.get(), 0, 2 * words * 4, s));
+  ETB_CUDA(cudaMemsetAsync(S.fb2.get(), 0, words * 4, s));
+  ETB_CUDA(cudaMemsetAsync(S.ctr.get(), 0, 64 * 8, s));
+  if (const uint32_t tail = static_cast<uint32_t>(L.nc & 31u)) {
+    const uint32_t pad = ~0u << tail;
+    const uint64_t last = (L.nc + 31) / 32 - 1;
+    for (int h = 0; h < 2; ++h)
+      ETB_CUDA(cudaMemcpyAsync(S.visited.get() + h * words + last, &pad, 4,
+                               cudaMemcpyHostToDevice, s));
+  }
+  S.parity = 0;
   S.bar.alloc(1);
   ETB_CUDA(cudaMemsetAsync(S.bar.get(), 0, 8, s));
   S.dp.alloc(n ? n : 1);
@@ -744,15 +769,20 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.tanchor = L.tanchor.get();
   p.tdepth = L.tdepth.get();
   p.nt = static_cast<uint32_t>(L.nt);
-  p.visited = S.visited.get();
-  p.fb0 = S.fb0.get();
-  p.fb1 = S.fb1.get();
+  const uint64_t cur = S.parity * S.words, nxt = (S.parity ^ 1u) * S.words;
+  p.visited = S.visited.get() + cur;
+  p.fb0 = S.fb0.get() + cur;
+  p.fb1 = S.fb1.get() + cur;
   p.fb2 = S.fb2.get();
+  p.visited_next = S.visited.get() + nxt;
+  p.fb0_next = S.fb0.get() + nxt;
+  p.fb1_next = S.fb1.get() + nxt;
   p.qv0 = S.qv0.get();
   p.qv1 = S.qv1.get();
   p.qp0 = S.qp0.get();
   p.qp1 = S.qp1.get();
-  p.ctr = S.ctr.get();
+  p.ctr = S.ctr.get() + 32 * S.parity;
+  p.ctr_next = S.ctr.get() + 32 * (S.parity ^ 1u);
   p.bar = S.bar.get();
   p.dp = S.dp.get();
   p.patch = S.patch.get();
@@ -864,10 +894,11 @@ void empty_launch(const BfsState& S, cudaStream_t s) {
                                        dim3(S.block), args, sizeof(Smem), s));
 }
 
-void bfs_launch(const BfsParams& p, const BfsState& S, cudaStream_t s) {
+void bfs_launch(const BfsParams& p, BfsState& S, cudaStream_t s) {
   void* args[] = {const_cast<BfsParams*>(&p)};
   ETB_CUDA(cudaLaunchCooperativeKernel(kernel_for(S.block), dim3(S.grid), dim3(S.block), args,
                                        sizeof(Smem), s));
+  S.parity ^= 1u;  // this launch cleans the other half; the next one uses it
 }
 
 }  // namespace etb

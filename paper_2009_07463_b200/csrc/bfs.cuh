@@ -33,6 +33,13 @@ struct BfsParams {
   uint64_t* qp1;
   unsigned long long* ctr;  // 4 level slots x 4 + conversion counters
   unsigned long long* bar;  // grid barrier counter (monotonic)
+  // The other half of the double-buffered visited / fb0 / fb1 / ctr: this
+  // traversal cleans it for the next one, so a traversal starts on clean state
+  // without an init pass and its grid barrier.
+  uint32_t* visited_next;
+  uint32_t* fb0_next;
+  uint32_t* fb1_next;
+  unsigned long long* ctr_next;
   // outputs (relaid ids, all n vertices)
   uint2* dp;  // {depth (i32 bits, -1 unreached), parent (kNone32 unreached)} per vertex
   // per call
@@ -73,13 +80,15 @@ struct BfsState {
   }
   uint32_t last_isolated = kNone32;  // isolated start to reset on the next call
   int grid = 0, block = 0;
+  uint32_t parity = 0;  // which half of visited / fb0 / fb1 / ctr the next launch uses
+  uint64_t words = 0;   // per half
   bool has_result = false;
   uint64_t last_start = ~uint64_t{0};
 };
 
 void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s);
 void empty_launch(const BfsState& S, cudaStream_t s);  // launch-cost floor (diagnostics)
-void bfs_launch(const BfsParams& p, const BfsState& S, cudaStream_t s);
+void bfs_launch(const BfsParams& p, BfsState& S, cudaStream_t s);
 // Fills depth/parent of the start's tree on the host (traverse_return_core_edge,
 // et_bfs.cpp:34-57) and returns the core vertex to start from (kNone32 if the
 // start's component is a pure tree or the start is isolated).

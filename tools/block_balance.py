@@ -43,6 +43,10 @@ def main():
         E._check(E.lib().etb_debug_phase_stamps(cg.handle, ph.ctypes.data))
         conv = {L: (int(ph[128 + L]) - int(ph[0])) / 1e3 for L in range(1, 64) if ph[128 + L]}
         print(f"root index {idx} trace {r.stats.direction_trace} claims {r.stats.level_claims}")
+        ent = out[62 * G:63 * G].view(np.int64).astype(np.float64) / 1e3
+        ext = out[63 * G:64 * G].view(np.int64).astype(np.float64) / 1e3
+        print(f"  CTA entry us: min {ent.min():6.1f} max {ent.max():6.1f}   exit: min {ext.min():6.1f} "
+              f"med {np.median(ext):6.1f} max {ext.max():6.1f}   (device total {r.stats.total_ns / 1e3:.1f})")
         for L in range(levels.value):
             t_all = out[L * G:(L + 1) * G].astype(np.float64) / 1e3
             t = t_all[t_all > 0]
