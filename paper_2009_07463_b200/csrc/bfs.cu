@@ -106,10 +106,16 @@ __device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, uint32_t 
                              uint32_t* qv_out, uint64_t* qp_out, unsigned long long* slot) {
   const unsigned lane = threadIdx.x & 31;
   unsigned long long cnt = 0, edges = 0;
-  for (uint32_t i = lane; i < ncl; i += 32) {
-    const uint32_t d = p.cmeta[cbuf[i]].x;
-    cnt += d != 0;
-    edges += d;
+  uint32_t d[kCbuf / 32];  // all loads in flight before any is summed
+#pragma unroll
+  for (int k = 0; k < kCbuf / 32; ++k) {
+    const uint32_t i = lane + 32 * k;
+    d[k] = i < ncl ? p.cmeta[cbuf[i]].x : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < kCbuf / 32; ++k) {
+    cnt += d[k] != 0;
+    edges += d[k];
   }
   cnt = warp_sum(cnt);
   edges = warp_sum(edges);
@@ -118,15 +124,16 @@ __device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, uint32_t 
   if (lane == 0) old = atomicAdd(slot, (cnt << kItemShift) | edges);
   old = __shfl_sync(0xffffffffu, old, 0);
   uint64_t vpos = old >> kItemShift, epos = old & kItemMask;
-  for (uint32_t i0 = 0; i0 < ncl; i0 += 32) {
-    const uint32_t i = i0 + lane;
+#pragma unroll
+  for (int k = 0; k < kCbuf / 32; ++k) {
+    if (32u * k >= ncl) break;  // warp-uniform
+    const uint32_t i = lane + 32 * k;
     const uint32_t v = i < ncl ? cbuf[i] : 0u;
-    const uint32_t d = i < ncl ? p.cmeta[v].x : 0u;
-    const uint32_t k = d != 0;
-    const uint32_t kin = warp_incl_scan(k), din = warp_incl_scan(d);
-    if (k) {
+    const uint32_t take = d[k] != 0;
+    const uint32_t kin = warp_incl_scan(take), din = warp_incl_scan(d[k]);
+    if (take) {
       qv_out[vpos + kin - 1] = v;
-      qp_out[vpos + kin - 1] = epos + din - d;
+      qp_out[vpos + kin - 1] = epos + din - d[k];
     }
     vpos += __shfl_sync(0xffffffffu, kin, 31);
     epos += __shfl_sync(0xffffffffu, din, 31);
