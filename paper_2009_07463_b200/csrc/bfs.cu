@@ -102,15 +102,19 @@ __device__ void grid_sync_add(unsigned long long* bar, Smem& sm, unsigned long l
 // slot[0] = (list length << 36) | edges returns both positions at once.
 
 // Append the staged claims to the next list (vertices without core edges skipped).
-__device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, uint32_t ncl,
-                             uint32_t* qv_out, uint64_t* qp_out, unsigned long long* slot) {
+// kStaged: the claims' core degrees are staged in cdeg (else read from cmeta,
+// all loads of the batch in flight at once).
+template <bool kStaged>
+__device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, const int32_t* cdeg,
+                             uint32_t ncl, uint32_t* qv_out, uint64_t* qp_out,
+                             unsigned long long* slot) {
   const unsigned lane = threadIdx.x & 31;
   unsigned long long cnt = 0, edges = 0;
-  uint32_t d[kCbuf / 32];  // all loads in flight before any is summed
+  uint32_t d[kCbuf / 32];
 #pragma unroll
   for (int k = 0; k < kCbuf / 32; ++k) {
     const uint32_t i = lane + 32 * k;
-    d[k] = i < ncl ? p.cmeta[cbuf[i]].x : 0u;
+    d[k] = i >= ncl ? 0u : (kStaged ? static_cast<uint32_t>(cdeg[i]) : p.cmeta[cbuf[i]].x);
   }
 #pragma unroll
   for (int k = 0; k < kCbuf / 32; ++k) {
@@ -153,10 +157,14 @@ __device__ __forceinline__ uint32_t win_search(const int32_t* win, int32_t rel) 
 // Top-down step (bfs.cpp:61-86). Each lane owns 8 edges of the warp's chunk;
 // their column loads, visited probes and claim atomics are issued before any
 // result is consumed.
+// kMode: 0 no list, 1 list (flush reads the degrees), 2 list with every
+// target's degrees fetched alongside its visited word (early levels, where most
+// targets are unvisited; after bottom-up most are visited and mode 1 is used).
+template <int kMode>
 __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const uint32_t* qv,
                         const uint64_t* qp, uint64_t nq, uint64_t ne, uint32_t* qv_out,
                         uint64_t* qp_out, uint32_t* fnext, unsigned long long* slot,
-                        int32_t dnext, bool emit, unsigned long long& scout_acc,
+                        int32_t dnext, unsigned long long& scout_acc,
                         unsigned long long& claims_acc, uint32_t root) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
@@ -211,8 +219,16 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
         }
         w[j] = col;
       }
+      // With a list to emit (small frontiers) every target's {core, full}
+      // degree is fetched with its visited word, off the claim's critical path;
+      // without one only the claimed targets' full degree is read.
+      constexpr bool kEmit = kMode != 0, kPre = kMode == 2;
+      uint2 mt[kPre ? kEpl : 1];
 #pragma unroll
-      for (int j = 0; j < kEpl; ++j) vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
+      for (int j = 0; j < kEpl; ++j) {
+        vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
+        if (kPre) mt[j] = w[j] != kNone32 ? p.cmeta[w[j]] : make_uint2(0u, 0u);
+      }
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
         const uint32_t bit = 1u << (w[j] & 31);
@@ -226,23 +242,27 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
         if (cl[j]) {
           p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u[j]);
           atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
-          dg[j] = p.degn[w[j]];
+          dg[j] = kPre ? mt[j].y : p.degn[w[j]];
         }
       }
       uint32_t ncl = 0;
+      if (kPre) __syncwarp();  // the window is free: it stages the claims' core degrees
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
         scout_acc += dg[j];
         claims_acc += cl[j];
-        if (emit) {
+        if (kEmit) {
           const unsigned m = __ballot_sync(0xffffffffu, cl[j]);
-          if (cl[j]) cbuf[ncl + __popc(m & lt)] = w[j];
+          if (cl[j]) {
+            cbuf[ncl + __popc(m & lt)] = w[j];
+            if (kPre) win[ncl + __popc(m & lt)] = static_cast<int32_t>(mt[kPre ? j : 0].x);
+          }
           ncl += __popc(m);
         }
       }
-      if (emit && ncl) {
+      if (kEmit && ncl) {
         __syncwarp();
-        flush_claims(p, cbuf, ncl, qv_out, qp_out, slot);
+        flush_claims<kPre>(p, cbuf, win, ncl, qv_out, qp_out, slot);
       }
       __syncwarp();
       i = inext;
@@ -525,7 +545,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     uint64_t* qp_out = p.qp1;
     unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0, reached = 1;
     double etc = p.edges_to_check;
-    bool bu = bu0;
+    bool bu = bu0, saw_bu = bu0;
     if (bu) awake = frontier;
     for (;;) {
       uint32_t* fcur = F[L % 3];
@@ -565,9 +585,18 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         // (which needs only the bitmap), else the bitmap is converted.
         const bool emit = (double)scout < p.emit_limit;
         list_valid = emit;
-        td_step(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_in, qp_in, nq, ne,
-                qv_out, qp_out, fnext, slot, dnext, emit, scout_acc, claims_acc,
-                L == 0 ? start : kNone32);
+        uint32_t* cb = sm.w[threadIdx.x >> 5].cbuf;
+        int32_t* wn = sm.w[threadIdx.x >> 5].win;
+        const uint32_t root = L == 0 ? start : kNone32;
+        if (!emit)
+          td_step<0>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
+                     scout_acc, claims_acc, root);
+        else if (saw_bu)
+          td_step<1>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
+                     scout_acc, claims_acc, root);
+        else
+          td_step<2>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
+                     scout_acc, claims_acc, root);
       }
       if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
       grid_sync_add(p.bar, sm, claims_acc, &slot[3], scout_acc, bu ? nullptr : &slot[1], slot, 4);
@@ -609,6 +638,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         if (frontier == 0) break;
         if (!p.top_down_only && (double)scout > etc / p.alpha) {
           bu = true;
+          saw_bu = true;
           awake = frontier;
         } else if (!list_valid) {
           unsigned long long* cslot = p.ctr + 16 + (L & 1);
