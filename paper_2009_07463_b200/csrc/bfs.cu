@@ -278,12 +278,11 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
   }
 }
 
-__device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcur, uint32_t v,
-                                         uint32_t& par) {
+__device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcur, uint64_t rb,
+                                         uint64_t re, uint32_t& par) {
   // The first (highest-degree) neighbour was already probed; the rest of the
-  // row is probed four at a time (independent loads) with early exit.
-  const uint64_t re = p.crow[v + 1];
-  for (uint64_t e = p.crow[v] + 1; e < re; e += 4) {
+  // row [rb, re) is probed four at a time (independent loads) with early exit.
+  for (uint64_t e = rb + 1; e < re; e += 4) {
     uint32_t x[4];
     bool b[4];
 #pragma unroll
@@ -355,9 +354,11 @@ __device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_
     bool lng = false, hit = false;
     uint32_t par = 0, cd = 0;
     if (v != kNone32) {
-      cd = p.cmeta[v].x;
+      // the row bounds give the degree too: one round trip before the scan
+      const uint64_t rb = p.crow[v], re = p.crow[v + 1];
+      cd = static_cast<uint32_t>(re - rb);
       if (cd > kLaneScan) lng = true;
-      else hit = scan_row(p, fcur, v, par);
+      else hit = scan_row(p, fcur, rb, re, par);
     }
     if (hit) {
       p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
