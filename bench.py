@@ -122,6 +122,19 @@ def captured_traffic(workload):
         return None
 
 
+def dram_block(workload, kernel_s, peak):
+    """Measured DRAM efficiency beside the B_alg normalisation (SURVEY.md §8(d):
+    B_alg counts every core edge once, a direction-optimizing BFS reads ~2% of
+    them, so the B_alg fraction may exceed 1 and is not a DRAM figure)."""
+    t = captured_traffic(workload)
+    if not t:
+        return None
+    gbs = t / kernel_s / 1e9
+    return {"bytes_per_launch": int(t), "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+            "source": "profiles/traffic.json (ncu dram__bytes_read+write per launch, caches "
+                      "flushed per replay) / the mean CUDA-event kernel time of this run"}
+
+
 def b_alg(nc, ecore, ntree):
     """algorithmic bytes per BFS (relaid space, u32 core ids)."""
     return 4 * ecore + 8 * (nc + 1) + 8 * nc + 16 * ntree
@@ -243,7 +256,9 @@ def run_ours(args):
                      "peak_source": peak_src, "algorithmic_bytes_per_bfs": int(balg),
                      "bytes_per_te": round(balg / float(te.max()), 3),
                      "roofline_gteps": round(roof_gteps, 1),
-                     "frac_of_roofline_gteps": round(hm_giant / roof_gteps, 4)},
+                     "frac_of_roofline_gteps": round(hm_giant / roof_gteps, 4),
+                     "dram": dram_block(f"kronecker-s{args.scale}-ef{args.edgefactor}-seed1",
+                                        kern_s, peak)},
         "e2e": {"value": round(e2e_hm, 3), "unit": "GTEPS",
                 "h2d_bytes_per_step": 8 * len(starts),
                 "d2h_bytes_per_step": 4 * n * len(starts),
@@ -313,7 +328,10 @@ def measure_secondary(scale, ef, mh, steps, warmup):
                          "algorithmic_bytes_per_bfs": int(balg),
                          "bytes_per_te": round(balg / float(te.max()), 3),
                          "roofline_gteps": round(roof, 1),
-                         "frac_of_roofline_gteps": round(hm / roof, 4)},
+                         "frac_of_roofline_gteps": round(hm / roof, 4),
+                         "traffic": captured_traffic(f"kronecker-s{scale}-ef{ef}-seed1"),
+                         "dram": dram_block(f"kronecker-s{scale}-ef{ef}-seed1",
+                                            float(np.mean(kms)) / 1e3, peak)},
             "preprocessing_s": round(prep, 3), "gpu_launches": int(len(ms)),
             "validated_roots": len(valid), "all_valid": all(valid)}
 
