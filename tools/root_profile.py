@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--mh", type=int, default=-1)
     ap.add_argument("--roots", type=int, default=64)
     ap.add_argument("--parts", type=int, default=1, help="1D core partitions on this device")
+    ap.add_argument("--cold", action="store_true", help="per-level stats on a flushed L2")
     args = ap.parse_args()
     g = eb.generate_graph(scale=args.scale, edgefactor=args.edgefactor, seed=1)
     cg = eb.relayout_csr(g, mh=args.mh)
@@ -33,8 +34,14 @@ def main():
     starts = cg.old2new[roots.astype(np.int64)]
     ms, kms = E.time_roots(cg, starts, warmup=8, flush_l2=True)
     out = []
+    import torch
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for i, s in enumerate(starts):
-        E.time_roots(cg, starts[i:i + 1], warmup=0, flush_l2=True)  # flush before the stats run
+        if args.cold:  # the stats run on a flushed L2, like the timed runs
+            flush.zero_()
+            torch.cuda.synchronize()
+        else:
+            E.time_roots(cg, starts[i:i + 1], warmup=0, flush_l2=True)  # warms this root
         r = eb.et_bfs(cg, int(s), stats=True, want_parent=False, want_depth=False)
         ns = r.stats.level_ns
         dur = [round((ns[j + 1] - ns[j]) / 1e3, 1) for j in range(len(ns) - 1)]
