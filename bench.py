@@ -279,6 +279,17 @@ def run_ours(args):
                    "generate_build_csr_s": round(t_csr, 3), "classify_relayout_s": round(t_layout, 3),
                    "timeline_root0": timeline},
     }
+    if rank == 0 and args.report_json:
+        write_report_v1(args, roots, te, sec[: len(starts)], valid, preprocessing_s,
+                        g.vertex_count, g.undirected_edge_count())
+    if rank == 0 and world == 1 and args.tree_out:
+        # BenchConfig::tree_out (bench.hpp:45): the first root's tree, original ids, ETT1
+        r0t = eb.et_bfs(cg, int(starts[0]), want_depth=False)
+        new2old = np.asarray(cg.new2old, np.uint64)
+        par = np.full(cg.vertex_count, np.uint64(0xFFFFFFFFFFFFFFFF), np.uint64)
+        ok = r0t.parent != np.uint64(0xFFFFFFFFFFFFFFFF)
+        par[new2old[ok]] = new2old[r0t.parent[ok].astype(np.int64)]
+        eb.write_tree(args.tree_out, int(roots[0]), par)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, roots[: args.cpu_roots])
     scales = [int(x) for x in str(args.secondary_scale).split(",") if x.strip() and int(x)]
@@ -291,6 +302,31 @@ def run_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def write_report_v1(args, roots, te, seconds, valid, prep_s, n, m):
+    """The reference's JSON report, schema v1 (report_to_json, bench.cpp:301-343),
+    for the first timed pass over the roots, so GPU runs drop into the same
+    tooling as `etbfs_bench --json` output."""
+    gteps = [float(t) / s / 1e9 for t, s in zip(te, seconds)]
+    rep = {
+        "schema_version": 1,
+        "config": {"kernel": "et-bfs", "mh": args.mh, "roots": len(roots), "seed": 1,
+                   "threads": 0, "alpha": 14.0, "beta": 24.0, "replay": "teet",
+                   "rm_zero": False, "round_robin": False, "degree_aware": False,
+                   "block_search": False, "et": True, "segments": 0},
+        "graph": {"vertex_count": int(n), "undirected_edge_count": int(m)},
+        "aggregate": {"mean_gteps": float(np.mean(gteps)), "min_gteps": float(np.min(gteps)),
+                      "max_gteps": float(np.max(gteps)),
+                      "harmonic_mean_seconds": float(len(seconds) / np.sum(1.0 / seconds)),
+                      "preprocessing_seconds": float(prep_s),
+                      "all_valid": bool(all(valid)) if valid else False},
+        "per_root": [{"root": int(r), "seconds": float(s), "traversed_edges": int(t),
+                      "gteps": g, "valid": bool(valid[i]) if valid else False}
+                     for i, (r, s, t, g) in enumerate(zip(roots, seconds, te, gteps))],
+    }
+    with open(args.report_json, "w") as f:
+        json.dump(rep, f, indent=2)
 
 
 def measure_secondary(scale, ef, mh, steps, warmup):
@@ -473,6 +509,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-roots", type=int, default=16)
     ap.add_argument("--ref-roots-per-step", type=int, default=4)
+    ap.add_argument("--report-json", default=None,
+                    help="also write the reference's JSON report (schema v1, bench.cpp:301-343)")
+    ap.add_argument("--tree-out", default=None,
+                    help="write the first root's BFS tree (original ids) as an ETT1 file")
     ap.add_argument("--secondary-scale", default="26,28",
                     help="comma list of further scales to time (0 = none); under 'secondary'")
     args = ap.parse_args()

@@ -18,6 +18,8 @@
  *   etb_layout_download_etl     include/etbfs/relayout.hpp:52   extract_edge_tree_list
  *   etb_bfs / etb_bfs_device    include/etbfs/et_bfs.hpp:53     et_bfs (CoreKernel::kHybrid)
  *   etb_layout_restricted_edges include/etbfs/bfs.hpp:123       restricted_edge_count
+ *   etb_graph_file_read/_write  include/etbfs/io.hpp:23-24      read_graph / write_graph
+ *   etb_tree_file_read/_write   include/etbfs/io.hpp:30-31      read_tree / write_tree
  *
  * Index spaces: "original" ids are the input graph's; "relaid" ids are the
  * relayout_csr space (core block [0, core), then edge trees, then isolated
@@ -218,6 +220,29 @@ int etb_debug_launch_floor(etb_layout* L, int iters, double* empty_us);
 int etb_time_roots(etb_layout* L, const uint64_t* starts, uint64_t count, int warmup,
                    int flush_l2, const etb_bfs_options* opts, double* ms_out,
                    double* kernel_ms_out);
+
+/* ---- graph and parent-tree files (io.hpp:9-45, io.cpp:47-181) ------------- */
+/* Byte-identical to the reference's ETG1 / text graph and ETT1 tree files, with
+ * its validation order and messages (runtime errors name the path and the byte
+ * offset or line). Host-only: no GPU needed. */
+#define ETB_FORMAT_BINARY 0 /* GraphFormat::kBinary (ETG1) */
+#define ETB_FORMAT_TEXT 1   /* GraphFormat::kText */
+typedef struct etb_edgefile etb_edgefile; /* a loaded edge list (host memory) */
+
+int etb_graph_file_read(const char* path, int format, etb_edgefile** out);
+/* Any output may be NULL; *pairs stays valid until etb_graph_file_free. */
+int etb_graph_file_info(const etb_edgefile* f, uint64_t* vertex_count, uint64_t* edge_count,
+                        const uint64_t** pairs);
+void etb_graph_file_free(etb_edgefile* f);
+int etb_graph_file_write(const char* path, int format, uint64_t vertex_count,
+                         const uint64_t* pairs, uint64_t edge_count);
+/* A graph file straight to a device CSR (read + etb_graph_from_edges). */
+int etb_graph_from_file(const char* path, int format, etb_graph** out);
+int etb_tree_file_write(const char* path, uint64_t vertex_count, uint64_t root,
+                        const uint64_t* parent);
+/* parent == NULL: only *vertex_count / *root (either may be NULL); else cap >= n. */
+int etb_tree_file_read(const char* path, uint64_t* vertex_count, uint64_t* root,
+                       uint64_t* parent, uint64_t cap);
 
 #ifdef __cplusplus
 }

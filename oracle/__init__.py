@@ -95,6 +95,11 @@ def ref() -> C.CDLL:
         L = C.CDLL(REF_SO)
         vp, u64, i64, u32, d = C.c_void_p, C.c_uint64, C.c_int64, C.c_uint32, C.c_double
         _sig(L.ref_last_error, C.c_char_p)
+        cp = C.c_char_p
+        _sig(L.ref_write_graph, C.c_int, cp, C.c_int, u64, vp, u64)
+        _sig(L.ref_read_graph, C.c_int, cp, C.c_int, C.POINTER(u64), C.POINTER(u64), vp)
+        _sig(L.ref_write_tree, C.c_int, cp, u64, u64, vp)
+        _sig(L.ref_read_tree, C.c_int, cp, C.POINTER(u64), C.POINTER(u64), vp)
         _sig(L.ref_set_threads, None, C.c_int)
         _sig(L.ref_generate_kronecker, C.c_int, u32, u64, d, d, d, d, u64, U64P)
         _sig(L.ref_build_csr, vp, u64, U64P, u64, C.POINTER(u64), C.POINTER(u64))

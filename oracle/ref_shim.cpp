@@ -12,6 +12,7 @@
 //   et_bfs               proj/include/etbfs/et_bfs.hpp:53
 //   oracle_bfs / validate_bfs_tree  proj/include/etbfs/validate.hpp:37-46
 //   select_roots / run_benchmark    proj/include/etbfs/bench.hpp:78-84
+//   write_graph / read_graph / write_tree / read_tree  proj/include/etbfs/io.hpp:23-31
 // Nothing here re-implements reference logic; it only marshals vectors.
 #include <chrono>
 #include <cstdint>
@@ -29,6 +30,7 @@
 #include "etbfs/build.hpp"
 #include "etbfs/classify.hpp"
 #include "etbfs/et_bfs.hpp"
+#include "etbfs/io.hpp"
 #include "etbfs/kronecker.hpp"
 #include "etbfs/relayout.hpp"
 #include "etbfs/validate.hpp"
@@ -57,6 +59,54 @@ EdgeList make_list(uint64_t n, const uint64_t* pairs, uint64_t count) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// ---- graph / tree files (io.hpp) ------------------------------------------------
+int ref_write_graph(const char* path, int text, uint64_t n, const uint64_t* pairs, uint64_t count) {
+  try {
+    write_graph(path, make_list(n, pairs, count), text ? GraphFormat::kText : GraphFormat::kBinary);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+// pairs == nullptr: sizes only (the file is read twice).
+int ref_read_graph(const char* path, int text, uint64_t* n, uint64_t* count, uint64_t* pairs) {
+  try {
+    const EdgeList el = read_graph(path, text ? GraphFormat::kText : GraphFormat::kBinary);
+    *n = el.vertex_count;
+    *count = el.edges.size();
+    if (pairs)
+      for (uint64_t i = 0; i < el.edges.size(); ++i) {
+        pairs[2 * i] = el.edges[i].src;
+        pairs[2 * i + 1] = el.edges[i].dst;
+      }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+int ref_write_tree(const char* path, uint64_t n, uint64_t root, const uint64_t* parent) {
+  try {
+    BfsTree t;
+    t.root = root;
+    t.parent.assign(parent, parent + n);
+    write_tree(path, t);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+int ref_read_tree(const char* path, uint64_t* n, uint64_t* root, uint64_t* parent) {
+  try {
+    const BfsTree t = read_tree(path);
+    *n = t.parent.size();
+    *root = t.root;
+    if (parent) std::memcpy(parent, t.parent.data(), t.parent.size() * 8);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
 
 void ref_set_threads(int t) {
 #ifdef _OPENMP

@@ -20,6 +20,7 @@ from .etbfs import (  # noqa: F401
     TypeCounts,
     VertexType,
     build_csr,
+    build_csr_from_file,
     classify_vertices,
     compute_peak_height,
     count_types,
@@ -28,6 +29,11 @@ from .etbfs import (  # noqa: F401
     generate_graph,
     generate_kronecker,
     lib,
+    parse_graph_format,
+    read_graph,
+    read_tree,
+    write_graph,
+    write_tree,
     lib_path,
     relayout_csr,
 )

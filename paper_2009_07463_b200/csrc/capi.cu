@@ -73,6 +73,14 @@ void need(const void* p, const char* what) {
   if (!p) throw std::invalid_argument(std::string(what) + ": null argument");
 }
 
+}  // namespace
+
+namespace etb {
+void set_last_error(const char* msg) { g_err = msg; }  // for the host-only entry points
+}  // namespace etb
+
+namespace {
+
 cudaStream_t new_stream() {
   cudaStream_t s;
   ETB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));

@@ -175,6 +175,15 @@ def lib() -> C.CDLL:
     sig("etb_host_register", vp, u64)
     sig("etb_host_unregister", vp)
     sig("etb_time_roots", vp, vp, u64, C.c_int, C.c_int, C.POINTER(_BfsOptions), vp, vp)
+    cp = C.c_char_p
+    sig("etb_graph_file_read", cp, i32, C.POINTER(vp))
+    sig("etb_graph_file_info", vp, P64, P64, C.POINTER(C.POINTER(C.c_uint64)))
+    L.etb_graph_file_free.restype = None
+    L.etb_graph_file_free.argtypes = [vp]
+    sig("etb_graph_file_write", cp, i32, u64, vp, u64)
+    sig("etb_graph_from_file", cp, i32, C.POINTER(vp))
+    sig("etb_tree_file_write", cp, u64, u64, vp)
+    sig("etb_tree_file_read", cp, P64, P64, vp, u64)
     _lib = L
     return L
 
@@ -481,3 +490,62 @@ def device_count() -> int:
     c = C.c_int()
     _check(lib().etb_device_count(C.byref(c)))
     return c.value
+
+
+# ---- graph and parent-tree files (io.hpp:9-45) ---------------------------------
+GRAPH_FORMATS = {"binary": 0, "text": 1}  # GraphFormat (io.hpp:11)
+
+
+def parse_graph_format(name: str) -> str:
+    """parse_graph_format (io.hpp:44): "binary" / "text", else ValueError."""
+    if name not in GRAPH_FORMATS:
+        raise ValueError(f'unknown graph format "{name}" (binary or text)')
+    return name
+
+
+def write_graph(path: str, vertex_count: int, pairs: np.ndarray, fmt: str = "binary") -> None:
+    """write_graph (io.hpp:23): ETG1 or text, byte-identical to the reference."""
+    pairs = np.ascontiguousarray(pairs, dtype=np.uint64).reshape(-1, 2)
+    _check(lib().etb_graph_file_write(os.fsencode(path), GRAPH_FORMATS[parse_graph_format(fmt)],
+                                      int(vertex_count), _ptr(pairs), pairs.shape[0]))
+
+
+def read_graph(path: str, fmt: str = "binary"):
+    """read_graph (io.hpp:24) -> (vertex_count, pairs u64[m, 2]); RuntimeError names
+    the path and the byte offset or line, as the reference's."""
+    h = C.c_void_p()
+    _check(lib().etb_graph_file_read(os.fsencode(path), GRAPH_FORMATS[parse_graph_format(fmt)],
+                                     C.byref(h)))
+    try:
+        n, m = C.c_uint64(), C.c_uint64()
+        p = C.POINTER(C.c_uint64)()
+        _check(lib().etb_graph_file_info(h, C.byref(n), C.byref(m), C.byref(p)))
+        pairs = (np.ctypeslib.as_array(p, shape=(2 * m.value,)).copy() if m.value
+                 else np.empty(0, np.uint64))
+        return n.value, pairs.reshape(-1, 2)
+    finally:
+        lib().etb_graph_file_free(h)
+
+
+def build_csr_from_file(path: str, fmt: str = "binary") -> Csr:
+    """read_graph + build_csr with the tuples going straight to the device."""
+    h = C.c_void_p()
+    _check(lib().etb_graph_from_file(os.fsencode(path), GRAPH_FORMATS[parse_graph_format(fmt)],
+                                     C.byref(h)))
+    return _finish_csr(h, C.c_uint64(0), C.c_uint64(0))
+
+
+def write_tree(path: str, root: int, parent: np.ndarray) -> None:
+    """write_tree (io.hpp:30): ETT1 {n, root, parent u64[n]} (kNoVertex unreached)."""
+    parent = np.ascontiguousarray(parent, dtype=np.uint64)
+    _check(lib().etb_tree_file_write(os.fsencode(path), parent.size, int(root), _ptr(parent)))
+
+
+def read_tree(path: str):
+    """read_tree (io.hpp:31) -> (root, parent u64[n])."""
+    n, root = C.c_uint64(), C.c_uint64()
+    _check(lib().etb_tree_file_read(os.fsencode(path), C.byref(n), C.byref(root), None, 0))
+    parent = np.empty(n.value, np.uint64)
+    _check(lib().etb_tree_file_read(os.fsencode(path), C.byref(n), C.byref(root), _ptr(parent),
+                                    n.value))
+    return root.value, parent

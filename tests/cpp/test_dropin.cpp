@@ -16,6 +16,7 @@
 #include "etbfs/build.hpp"
 #include "etbfs/classify.hpp"
 #include "etbfs/et_bfs.hpp"
+#include "etbfs/io.hpp"
 #include "etbfs/kronecker.hpp"
 #include "etbfs/relayout.hpp"
 
@@ -180,6 +181,28 @@ void run_case(const char* name, const std::function<void()>& f) {
 }  // namespace
 
 int main() {
+  run_case("graph / tree files (test_io.cpp cases) feeding a GPU traversal", [] {
+    const std::string gpath = "/tmp/etbfs_dropin_io.etg", tpath = "/tmp/etbfs_dropin_io.ett";
+    const EdgeList el = random_tuples(300, 900, 4);
+    write_graph(gpath, el, GraphFormat::kBinary);
+    const EdgeList back = read_graph(gpath, parse_graph_format("binary"));
+    EXPECT(back.vertex_count == el.vertex_count && back.edges == el.edges);
+    write_graph(gpath, el, GraphFormat::kText);
+    EXPECT(read_graph(gpath, GraphFormat::kText).edges == el.edges);
+    const CsrGraph g = build_csr(back);
+    const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, -1), -1);
+    const EdgeTreeList etl = extract_edge_tree_list(cg);
+    const BfsTree t = et_bfs(cg, etl, cg.old2new[7]);
+    write_tree(tpath, t);
+    const BfsTree t2 = read_tree(tpath);
+    EXPECT(t2.root == t.root && t2.parent == t.parent);
+    EXPECT(throws_with<std::invalid_argument>([] { parse_graph_format("csv"); },
+                                              "unknown graph format \"csv\""));
+    EXPECT(throws_with<std::runtime_error>([&] { read_tree(gpath); }, "bad magic, expected ETT1"));
+    std::remove(gpath.c_str());
+    std::remove(tpath.c_str());
+  });
+
   run_case("build_csr KAT (test_graph_core.cpp:17-36)", [] {
     BuildStats st;
     const CsrGraph g = build_csr(
