@@ -157,7 +157,8 @@ __device__ __forceinline__ uint32_t win_search(const int32_t* win, int32_t rel) 
 // Top-down step (bfs.cpp:61-86). Each lane owns 8 edges of the warp's chunk;
 // their column loads, visited probes and claim atomics are issued before any
 // result is consumed.
-// kMode: 0 no list, 1 list (flush reads the degrees), 2 list with every
+// kMode: 0 no list, 3 no list and no scout (summed after the level by
+// scout_pass), 1 list (flush reads the degrees), 2 list with every
 // target's degrees fetched alongside its visited word (early levels, where most
 // targets are unvisited; after bottom-up most are visited and mode 1 is used).
 template <int kMode>
@@ -222,7 +223,7 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
       // With a list to emit (small frontiers) every target's {core, full}
       // degree is fetched with its visited word, off the claim's critical path;
       // without one only the claimed targets' full degree is read.
-      constexpr bool kEmit = kMode != 0, kPre = kMode == 2;
+      constexpr bool kEmit = kMode == 1 || kMode == 2, kPre = kMode == 2;
       uint2 mt[kPre ? kEpl : 1];
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
@@ -242,7 +243,9 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
         if (cl[j]) {
           p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u[j]);
           atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
-          dg[j] = kPre ? mt[j].y : p.degn[w[j]];
+          // mode 3 (huge levels): the scout is summed after the level from the
+          // new frontier bitmap, a streaming pass (scout_pass)
+          dg[j] = kPre ? mt[j].y : (kMode == 3 ? 0u : p.degn[w[j]]);
         }
       }
       uint32_t ncl = 0;
@@ -504,6 +507,32 @@ __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t*
   }
 }
 
+// Σ full degree over the frontier bitmap f: a warp takes 4 words per
+// iteration, lane = vertex, coalesced degree loads. For levels that claim a
+// large share of the core this streams the degree array instead of one random
+// 32-byte sector per claim.
+__device__ unsigned long long scout_pass(const BfsParams& p, const uint32_t* f) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long s = 0;
+  for (uint64_t w0 = gw * 4; w0 < p.nwords; w0 += nw * 4) {
+    uint32_t d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t wi = w0 + k;
+      const uint32_t bits = wi < p.nwords ? f[wi] : 0u;
+      d[k] = ((bits >> lane) & 1u) ? p.degn[wi * 32 + lane] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += d[k];
+  }
+  return s;
+}
+
+// kLarge: the 1024-thread instantiation (cores of >= 2^23 vertices), the only
+// one whose top-down levels can claim a large share of the core at once.
+template <bool kLarge>
 __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -564,7 +593,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
       }
       const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
       unsigned long long claims_acc = 0, scout_acc = 0;
-      bool list_valid = true;
+      bool list_valid = true, defer_scout = false;
       // (A smem copy of the probed bitmap's hot prefix was tried and measured
       // slower: the 64 KB it takes comes out of L1, which caches those lines.)
       bool bu_list = false;
@@ -589,7 +618,13 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         uint32_t* cb = sm.w[threadIdx.x >> 5].cbuf;
         int32_t* wn = sm.w[threadIdx.x >> 5].win;
         const uint32_t root = L == 0 ? start : kNone32;
-        if (!emit)
+        // a frontier with more edges than the core has vertices claims a large share of
+        // it: its scout is summed afterwards by a streaming pass (mode 3)
+        defer_scout = kLarge && !emit && (double)scout > (double)p.nc;
+        if (kLarge && defer_scout)
+          td_step<3>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
+                     scout_acc, claims_acc, root);
+        else if (!emit)
           td_step<0>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
                      scout_acc, claims_acc, root);
         else if (saw_bu)
@@ -626,6 +661,11 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
       } else {
         frontier = claims;
         scout = scout_tot;
+        if (kLarge && defer_scout && claims) {  // this level deferred its scout
+          const unsigned long long ds = scout_pass(p, F[L % 3]);
+          grid_sync_add(p.bar, sm, ds, &slot[1], 0, nullptr, slot, 4);
+          scout = sm.tot[1];
+        }
         nq = packed >> kItemShift;
         ne = packed & kItemMask;
         uint32_t* tv = qv_in;
@@ -718,7 +758,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
 
 template <int B>
 __global__ void __launch_bounds__(B, 1) et_bfs_kernel(BfsParams p) {
-  et_bfs_body(p);
+  et_bfs_body<(B > 768)>(p);
 }
 
 }  // namespace
