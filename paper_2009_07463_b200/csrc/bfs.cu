@@ -681,7 +681,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           bu = true;
           saw_bu = true;
           awake = frontier;
-        } else if (!list_valid) {
+        } else if (!list_valid && reached < p.nc) {
           unsigned long long* cslot = p.ctr + 16 + (L & 1);
           convert_step(p, F[L % 3], qv_in, qp_in, cslot);
           grid_sync_add(p.bar, sm, 0, nullptr, 0, nullptr, cslot, 1);
@@ -690,6 +690,16 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           nq = cp >> kItemShift;
           ne = cp & kItemMask;
         }
+      }
+      // Every core vertex is visited: the level the reference would run next
+      // (bfs.cpp:240-292; either direction) claims nothing and ends the loop.
+      // Record it with its direction and no claims, without running it.
+      if (reached == p.nc) {
+        if (tid == 0 && p.trace && L < 255) p.trace[L] = bu ? 'b' : 't';
+        if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = 0;
+        ++L;
+        stamp(p, 257 + L);
+        break;
       }
     }
   }
