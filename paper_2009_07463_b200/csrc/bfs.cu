@@ -749,6 +749,12 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     const uint32_t v = p.patch[3 * i];
     p.dp[v] = make_uint2(p.patch[3 * i + 1], p.patch[3 * i + 2]);
   }
+  // inline patch entries: constant indices keep them in the parameter bank
+#pragma unroll
+  for (int k = 0; k < kInlinePatch; ++k)
+    if (tid == static_cast<uint64_t>(k) && static_cast<uint32_t>(k) < p.nipatch)
+      p.dp[p.ipatch[3 * k]] = make_uint2(p.ipatch[3 * k + 1], p.ipatch[3 * k + 2]);
+
   // ---- clean the other state half for the next traversal --------------------
   {
     const uint32_t tail = p.nc & 31u;
@@ -875,6 +881,7 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.dp = S.dp.get();
   p.patch = S.patch.get();
   p.npatch = 0;
+  p.nipatch = 0;
   p.edges_to_check = static_cast<double>(L.ecore);
   p.emit_limit = static_cast<double>(L.nc) / 4.0 + 1024.0;
   p.trace = nullptr;
@@ -964,8 +971,13 @@ void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParam
     ++np;
     S.last_isolated = static_cast<uint32_t>(start);
   }
-  p.npatch = np;
-  if (np) {
+  p.npatch = 0;
+  p.nipatch = 0;
+  if (np <= static_cast<uint32_t>(kInlinePatch)) {
+    std::copy(ph, ph + 3 * np, p.ipatch);
+    p.nipatch = np;
+  } else {
+    p.npatch = np;
     ETB_CUDA(cudaMemcpyAsync(S.patch.get(), ph, np * 12, cudaMemcpyHostToDevice, s));
     ETB_CUDA(cudaEventRecord(S.patch_done, s));
   }

@@ -7,6 +7,8 @@ namespace etb {
 
 // Chunk of a core row one warp expands in a top-down step.
 constexpr uint32_t kTdChunk = 128;
+// Start-tree patch entries carried inline in the kernel parameters.
+constexpr int kInlinePatch = 4;
 
 struct BfsParams {
   // core graph (relaid ids)
@@ -49,6 +51,10 @@ struct BfsParams {
   uint32_t skip_lo, skip_hi;  // tree range filled by the start-side walk
   const uint32_t* patch;  // (vertex, depth, parent) triples
   uint32_t npatch;
+  // Small patches travel in the launch parameters (no host-to-device copy in
+  // the per-root sequence); ipatch[3 k .. 3 k + 2] for k < nipatch.
+  uint32_t nipatch;
+  uint32_t ipatch[3 * kInlinePatch];
   double alpha, beta, edges_to_check;
   double emit_limit;  // top-down levels with scout >= this skip work-item emission
   int top_down_only;   // CoreKernel::kTopDown

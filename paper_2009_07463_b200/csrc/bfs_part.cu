@@ -422,6 +422,11 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
     const uint32_t v = p.patch[3 * i];
     if (owns(me, v)) p.dp[v] = make_uint2(p.patch[3 * i + 1], p.patch[3 * i + 2]);
   }
+#pragma unroll
+  for (int k = 0; k < kInlinePatch; ++k)
+    if (gtid == static_cast<uint64_t>(k) && static_cast<uint32_t>(k) < p.nipatch &&
+        owns(me, p.ipatch[3 * k]))
+      p.dp[p.ipatch[3 * k]] = make_uint2(p.ipatch[3 * k + 1], p.ipatch[3 * k + 2]);
 }
 
 // seg[u] = {offset, length} of u's neighbours inside [lo, hi) (rows ascend).

@@ -475,15 +475,18 @@ def result_traversed_edges(cg: EtLayout) -> int:
 
 
 def time_roots(cg: EtLayout, starts, warmup=3, flush_l2=True, kernel=CoreKernel.HYBRID,
-               replay=TreeReplay.TEET, policy: HybridPolicy | None = None):
-    """Per-root CUDA-event times (ms): (whole call incl. start-side walk, kernel only)."""
+               replay=TreeReplay.TEET, policy: HybridPolicy | None = None,
+               kernel_times: bool = True):
+    """Per-root CUDA-event times (ms): (whole call incl. start-side walk, kernel only).
+    kernel_times=False leaves out the pre-launch event (kernel times None): the
+    whole-call times then carry no third event."""
     s = np.ascontiguousarray(starts, np.uint64)
     ms = np.empty(max(s.size, 1), np.float64)
-    kms = np.empty(max(s.size, 1), np.float64)
+    kms = np.empty(max(s.size, 1), np.float64) if kernel_times else None
     o = _opts(kernel, replay, policy)
     _check(lib().etb_time_roots(cg.handle, _ptr(s), s.size, int(warmup), int(bool(flush_l2)),
                                 C.byref(o), _ptr(ms), _ptr(kms)))
-    return ms[: s.size], kms[: s.size]
+    return ms[: s.size], (kms[: s.size] if kms is not None else None)
 
 
 def device_count() -> int:

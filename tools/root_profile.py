@@ -46,7 +46,7 @@ def main():
         ns = r.stats.level_ns
         dur = [round((ns[j + 1] - ns[j]) / 1e3, 1) for j in range(len(ns) - 1)]
         rec = {"root": int(roots[i]), "start": int(s), "type": int(cg.vertex_type[int(s)]),
-               "kernel_us": round(float(kms[i]) * 1e3, 1), "device_us": round(r.stats.total_ns / 1e3, 1),
+               "kernel_us": round(float(kms[i]) * 1e3, 1), "call_us": round(float(ms[i]) * 1e3, 1), "device_us": round(r.stats.total_ns / 1e3, 1),
                "init_us": round(ns[0] / 1e3, 1) if ns else None, "trace": r.stats.direction_trace,
                "claims": r.stats.level_claims, "level_us": dur}
         out.append(rec)
