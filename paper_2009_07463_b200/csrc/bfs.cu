@@ -705,7 +705,34 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
   }
   if (tid == 0 && p.nlevels) *p.nlevels = L;
 
-  // ---- unreached core vertices + tree replay + start-tree patch ----------------
+  // ---- tree replay + unreached core vertices + start-tree patch ----------------
+  // Replay (TEET/TEOLV, et_bfs.cpp:14-32): the tree arrays and, per anchor, its
+  // visited bit and depth are fetched together (two dependent round trips;
+  // an unreached anchor's stale depth is simply ignored).
+  for (uint64_t t0 = tid; t0 < p.nt; t0 += 4 * nthreads) {
+    uint32_t a[4], td[4], ts[4], vis[4], da[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t t = t0 + k * nthreads;
+      const uint32_t tv = static_cast<uint32_t>(p.nc + t);
+      const bool in = t < p.nt && !(tv >= p.skip_lo && tv < p.skip_hi);
+      a[k] = in ? p.tanchor[t] : kNone32 - 1;
+      td[k] = in ? p.tdepth[t] : 0u;
+      ts[k] = in ? p.tsrc[t] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool ok = a[k] < kNone32 - 1;
+      vis[k] = ok ? test_bit(p.visited, a[k]) : 0u;
+      da[k] = ok ? __ldcg(&p.dp[a[k]].x) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (a[k] == kNone32 - 1) continue;  // out of range or inside the start's tree
+      p.dp[p.nc + t0 + k * nthreads] =
+          vis[k] ? make_uint2(da[k] + td[k], ts[k]) : make_uint2(kNone32, kNone32);
+    }
+  }
   {
     // A warp reads 32 visited words, then clears the unreached vertices of each
     // word with one coalesced 256-byte store (padding bits are set).
@@ -718,31 +745,6 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         if ((__shfl_sync(0xffffffffu, un, j) >> lane) & 1u)
           p.dp[(w0 + j) * 32 + lane] = make_uint2(kNone32, kNone32);
       }
-    }
-  }
-  for (uint64_t t0 = tid; t0 < p.nt; t0 += 4 * nthreads) {
-    uint32_t a[4], vis[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t t = t0 + k * nthreads;
-      const uint32_t tv = static_cast<uint32_t>(p.nc + t);
-      a[k] = (t < p.nt && !(tv >= p.skip_lo && tv < p.skip_hi)) ? p.tanchor[t] : kNone32 - 1;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) vis[k] = a[k] < kNone32 - 1 ? test_bit(p.visited, a[k]) : 0u;
-    // All loads of the 4 entries are issued before any store: the stores go to
-    // dp too, so the compiler would otherwise serialise load -> store pairs.
-    uint2 out[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t t = t0 + k * nthreads;
-      out[k] = make_uint2(kNone32, kNone32);
-      if (vis[k]) out[k] = make_uint2(__ldcg(&p.dp[a[k]].x) + p.tdepth[t], p.tsrc[t]);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (a[k] == kNone32 - 1) continue;  // out of range or inside the start's tree
-      p.dp[p.nc + t0 + k * nthreads] = out[k];
     }
   }
   for (uint64_t i = tid; i < p.npatch; i += nthreads) {
