@@ -206,7 +206,7 @@ int etb_debug_block_stamps(etb_layout* L, uint64_t start, uint64_t* out, uint64_
                            uint32_t* grid, uint32_t* levels);
 /* Diagnostics: the raw globaltimer stamps of the last stats run ([0] entry, [1]
  * init end, [2 + L] level L end, [128 + L] conversion before level L end,
- * [255] replay end). */
+ * [255] replay end) and, at [192 + L], top-down level L's frontier edge count. */
 int etb_debug_phase_stamps(etb_layout* L, uint64_t* out256);
 /* Diagnostics: median event-timed duration (us) of an empty kernel launched
  * like the traversal (same grid, block, shared memory, cooperative). */

@@ -614,6 +614,8 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         // is small; a large one is all but certain to hand over to bottom-up
         // (which needs only the bitmap), else the bitmap is converted.
         const bool emit = (double)scout < p.emit_limit;
+        // diagnostics: this top-down level's frontier edges (phase stamp 192 + L)
+        if (p.level_claims && tid == 0 && L < 64) p.level_claims[448 + L] = ne;
         list_valid = emit;
         uint32_t* cb = sm.w[threadIdx.x >> 5].cbuf;
         int32_t* wn = sm.w[threadIdx.x >> 5].win;

@@ -44,11 +44,16 @@ def main():
             E.time_roots(cg, starts[i:i + 1], warmup=0, flush_l2=True)  # warms this root
         r = eb.et_bfs(cg, int(s), stats=True, want_parent=False, want_depth=False)
         ns = r.stats.level_ns
+        import ctypes as C
+        ph = np.zeros(256, np.uint64)
+        E._check(E.lib().etb_debug_phase_stamps(cg.handle, ph.ctypes.data))
+        td_edges = [int(ph[192 + L]) if r.stats.direction_trace[L:L + 1] == "t" else None
+                    for L in range(len(r.stats.direction_trace))]
         dur = [round((ns[j + 1] - ns[j]) / 1e3, 1) for j in range(len(ns) - 1)]
         rec = {"root": int(roots[i]), "start": int(s), "type": int(cg.vertex_type[int(s)]),
                "kernel_us": round(float(kms[i]) * 1e3, 1), "call_us": round(float(ms[i]) * 1e3, 1), "device_us": round(r.stats.total_ns / 1e3, 1),
                "init_us": round(ns[0] / 1e3, 1) if ns else None, "trace": r.stats.direction_trace,
-               "claims": r.stats.level_claims, "level_us": dur}
+               "claims": r.stats.level_claims, "level_us": dur, "td_edges": td_edges}
         out.append(rec)
         print(json.dumps(rec), flush=True)
     # Fixed cost: a start on an isolated vertex runs init + tree replay only.
