@@ -18,7 +18,26 @@ constexpr unsigned long long kPGrab = 4;
 
 struct PSmem {
   uint32_t mbuf[kPWarps][kPMiss];
-  unsigned long long red[kPWarps];
+  unsigned long long red[2][kPWarps];
+  unsigned long long tot[4];  // values read once per CTA after a barrier
+};
+
+// The next-frontier replicas of every partition (index ni of the ring), so a
+// claim is published to all partitions as it happens: no exchange phase.
+struct Peers {
+  uint32_t* f[kMaxParts];
+  uint32_t n;
+  uint32_t self;
+  bool sys;
+  __device__ __forceinline__ void or_bit(uint32_t v) const {
+    for (uint32_t q = 0; q < n; ++q) {
+      if (sys && q != self) atomicOr_system(&f[q][v >> 5], 1u << (v & 31));
+      else atomicOr(&f[q][v >> 5], 1u << (v & 31));
+    }
+  }
+  __device__ __forceinline__ void store_word(uint64_t w, uint32_t m) const {
+    for (uint32_t q = 0; q < n; ++q) f[q][w] = m;  // owned words: one writer
+  }
 };
 
 // ctr layout (per partition, exchange block): [0..15] four level slots of
@@ -53,39 +72,48 @@ __device__ void group_sync(unsigned long long* bar, unsigned nb, bool sys) {
   __syncthreads();
 }
 
-// Cross-partition barrier, run by each group's leader thread between two
-// group barriers: signal every partition (peers included), wait for all.
-__device__ void cross_signal_wait(const PartParams& pp, const PartDev& me,
-                                  unsigned long long target) {
+// The level barrier over every CTA of every partition. Each CTA reduces its
+// (a, b) partials, adds them into every partition's counters `off`, publishes
+// its writes (replica words, results) and arrives at every partition's
+// counter; the barrier completes when all nparts x gsize CTAs have arrived
+// (`target` counts arrivals since the counters were created). Thread 0 then
+// reads the n counters at `rd` once for the CTA (sm.tot).
+__device__ void part_sync(const PartParams& pp, const PartDev& me, PSmem& sm,
+                          unsigned long long a, unsigned long long b, uint32_t off,
+                          unsigned long long target, const unsigned long long* rd, int n) {
   const bool sys = pp.system_scope;
-  fence(sys);
-  for (uint32_t q = 0; q < pp.nparts; ++q) {
-    if (sys) atomicAdd_system(pp.parts[q].arrive, 1ull);
-    else atomicAdd(pp.parts[q].arrive, 1ull);
-  }
-  const long long t0 = clock64();
-  while ((sys ? ld_acquire_sys(me.arrive) : ld_acquire(me.arrive)) < target)
-    if (clock64() - t0 > 40000000000ll) __trap();
-  fence(sys);
-}
-
-__device__ void block_reduce2(unsigned long long a, unsigned long long b, unsigned long long& ra,
-                              unsigned long long& rb, PSmem& sm) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   a = warp_sum(a);
   b = warp_sum(b);
-  __shared__ unsigned long long red2[kPWarps];
   if (lane == 0) {
-    sm.red[wib] = a;
-    red2[wib] = b;
+    sm.red[0][wib] = a;
+    sm.red[1][wib] = b;
   }
   __syncthreads();
-  ra = rb = 0;
   if (threadIdx.x < 32) {
-    a = lane < kPWarps ? sm.red[lane] : 0ull;
-    b = lane < kPWarps ? red2[lane] : 0ull;
-    ra = warp_sum(a);
-    rb = warp_sum(b);
+    a = warp_sum(lane < kPWarps ? sm.red[0][lane] : 0ull);
+    b = warp_sum(lane < kPWarps ? sm.red[1][lane] : 0ull);
+    if (lane == 0) {
+      for (uint32_t q = 0; q < pp.nparts; ++q) {
+        unsigned long long* c = pp.parts[q].ctr + off;
+        if (sys) {
+          if (a) atomicAdd_system(&c[0], a);
+          if (b) atomicAdd_system(&c[1], b);
+        } else {
+          if (a) atomicAdd(&c[0], a);
+          if (b) atomicAdd(&c[1], b);
+        }
+      }
+      fence(sys);  // release: the CTA's writes (ordered by bar.sync) before the arrival
+      for (uint32_t q = 0; q < pp.nparts; ++q) {
+        if (sys) atomicAdd_system(pp.parts[q].arrive, 1ull);
+        else atomicAdd(pp.parts[q].arrive, 1ull);
+      }
+      const long long t0 = clock64();
+      while ((sys ? ld_acquire_sys(me.arrive) : ld_acquire(me.arrive)) < target)
+        if (clock64() - t0 > 40000000000ll) __trap();
+      for (int k = 0; k < n; ++k) sm.tot[k] = ld_volatile(&rd[k]);
+    }
   }
   __syncthreads();
 }
@@ -130,7 +158,7 @@ __device__ void part_convert(const BfsParams& p, const PartDev& me, const uint32
 
 // Top-down over the owned segments of the frontier rows.
 __device__ void part_td(const BfsParams& p, const PartDev& me, uint64_t nq, uint64_t nu,
-                        uint32_t* fnext, unsigned long long* grab, int32_t dnext, uint64_t gw,
+                        const Peers& fnext, unsigned long long* grab, int32_t dnext, uint64_t gw,
                         uint64_t nw, unsigned long long& scout_acc,
                         unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31;
@@ -165,7 +193,7 @@ __device__ void part_td(const BfsParams& p, const PartDev& me, uint64_t nq, uint
         dg[j] = 0;
         if (cl[j]) {
           p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u);
-          atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
+          fnext.or_bit(w[j]);
           dg[j] = p.degn[w[j]];
         }
       }
@@ -204,7 +232,7 @@ __device__ __forceinline__ bool part_scan_row(const BfsParams& p, const uint32_t
 }
 
 __device__ void part_misses(const BfsParams& p, const PartDev& me, const uint32_t* fcur,
-                            uint32_t* fnext, uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
+                            const Peers& fnext, uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
                             unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31;
   __syncwarp();
@@ -214,7 +242,7 @@ __device__ void part_misses(const BfsParams& p, const PartDev& me, const uint32_
     if (part_scan_row(p, fcur, v, par)) {
       p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
       atomicOr(&me.visited[v >> 5], 1u << (v & 31));
-      atomicOr(&fnext[v >> 5], 1u << (v & 31));
+      fnext.or_bit(v);
       ++claims_acc;
     }
   }
@@ -223,7 +251,7 @@ __device__ void part_misses(const BfsParams& p, const PartDev& me, const uint32_
 
 // Bottom-up over the owned visited words.
 __device__ void part_bu(const BfsParams& p, const PartDev& me, uint32_t* mbuf,
-                        const uint32_t* fcur, uint32_t* fnext, int32_t dnext, uint64_t gw,
+                        const uint32_t* fcur, const Peers& fnext, int32_t dnext, uint64_t gw,
                         uint64_t nw, unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1;
@@ -252,7 +280,7 @@ __device__ void part_bu(const BfsParams& p, const PartDev& me, uint32_t* mbuf,
       if (hit[k]) p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), f[k]);
       if (lane == 0 && m) {
         me.visited[w0 + k] = vis[k] | m;
-        fnext[w0 + k] = m;
+        fnext.store_word(w0 + k, m);
         claims_acc += __popc(m);
       }
       const bool miss = f[k] != kNone32 && !hit[k];
@@ -306,15 +334,14 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
   if (gtid < 20) me.ctr[gtid] = 0;
   if (run_core && gtid == 0 && start >= me.lo && start < me.hi)
     p.dp[start] = make_uint2(static_cast<uint32_t>(p.base_depth), p.start_parent);
-  group_sync(me.bar, gsize, sys);
+  const unsigned long long per_barrier = static_cast<unsigned long long>(pp.nparts) * gsize;
   ++xk;  // every partition initialised its replicas before any peer writes into them
-  if (leader_block && threadIdx.x == 0) cross_signal_wait(pp, me, xk * pp.nparts);
-  group_sync(me.bar, gsize, sys);
+  part_sync(pp, me, sm, 0, 0, 0, xk * per_barrier, nullptr, 0);
 
   uint32_t L = 0;
   if (run_core) {
     uint32_t* F[3] = {me.fb0, me.fb1, me.fb2};
-    unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0;
+    unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0, reached = 1;
     double etc = p.edges_to_check;
     bool bu = p.bottom_up_only || (!p.top_down_only && (double)scout > etc / p.alpha);
     if (bu) awake = frontier;
@@ -334,46 +361,35 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
       if (stats && L < 255) p.trace[L] = bu ? 'b' : 't';
       const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
       unsigned long long claims_acc = 0, scout_acc = 0;
+      Peers fn;  // this level's next-frontier replicas, ours and the peers'
+      fn.n = pp.nparts;
+      fn.self = part;
+      fn.sys = sys;
+      for (uint32_t q = 0; q < pp.nparts; ++q) {
+        const PartDev& pq = pp.parts[q];
+        fn.f[q] = q == part ? fnext : (ni == 0 ? pq.fb0 : (ni == 1 ? pq.fb1 : pq.fb2));
+      }
       if (bu) {
         prev = awake;
-        part_bu(p, me, sm.mbuf[threadIdx.x >> 5], fcur, fnext, dnext, gw, nw, claims_acc);
+        part_bu(p, me, sm.mbuf[threadIdx.x >> 5], fcur, fn, dnext, gw, nw, claims_acc);
       } else {
         etc -= (double)scout;
         unsigned long long* cslot = me.ctr + 16 + (L & 1);
         part_convert(p, me, fcur, cslot, gw, nw);
         group_sync(me.bar, gsize, sys);
-        const unsigned long long cp = ld_volatile(cslot);
-        part_td(p, me, cp >> kShift, cp & kMask, fnext, &slot[2], dnext, gw, nw, scout_acc,
+        if (threadIdx.x == 0) sm.tot[2] = ld_volatile(cslot);  // once per CTA
+        __syncthreads();
+        const unsigned long long cp = sm.tot[2];
+        part_td(p, me, cp >> kShift, cp & kMask, fn, &slot[2], dnext, gw, nw, scout_acc,
                 claims_acc);
       }
-      // partials into every partition's slot, owned next-frontier slice into every replica
-      unsigned long long bc = 0, bs = 0;
-      block_reduce2(claims_acc, scout_acc, bc, bs, sm);
-      if (threadIdx.x == 0 && (bc || bs)) {
-        for (uint32_t q = 0; q < pp.nparts; ++q) {
-          unsigned long long* qs = pp.parts[q].ctr + (L & 3) * 4;
-          if (sys) {
-            if (bc) atomicAdd_system(&qs[0], bc);
-            if (bs) atomicAdd_system(&qs[1], bs);
-          } else {
-            if (bc) atomicAdd(&qs[0], bc);
-            if (bs) atomicAdd(&qs[1], bs);
-          }
-        }
-      }
-      group_sync(me.bar, gsize, sys);  // owned fnext words final
-      const uint64_t wlo = me.lo >> 5, whi = (static_cast<uint64_t>(me.hi) + 31) >> 5;
-      for (uint32_t q = 0; q < pp.nparts; ++q) {
-        if (q == part) continue;
-        const PartDev& pq = pp.parts[q];
-        uint32_t* dst = ni == 0 ? pq.fb0 : (ni == 1 ? pq.fb1 : pq.fb2);
-        for (uint64_t i = wlo + gtid; i < whi; i += gthreads) dst[i] = fnext[i];
-      }
-      group_sync(me.bar, gsize, sys);
+      // one barrier over all partitions: partials added everywhere, claims already
+      // published into every replica
       ++xk;
-      if (leader_block && threadIdx.x == 0) cross_signal_wait(pp, me, xk * pp.nparts);
-      group_sync(me.bar, gsize, sys);
-      const unsigned long long claims = ld_volatile(&slot[0]);
+      part_sync(pp, me, sm, claims_acc, scout_acc, (L & 3) * 4, xk * per_barrier, slot, 2);
+      const unsigned long long claims = sm.tot[0];
+      const unsigned long long scout_tot = sm.tot[1];
+      reached += claims;
       if (stats && L < 256) p.level_claims[L] = claims;
       ++L;
       if (bu && p.bottom_up_only) {
@@ -388,7 +404,7 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
         }
       } else {
         frontier = claims;
-        scout = ld_volatile(&slot[1]);
+        scout = scout_tot;
       }
       if (!bu) {
         if (frontier == 0) break;
@@ -396,6 +412,13 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
           bu = true;
           awake = frontier;
         }
+      }
+      // every core vertex visited: the next level claims nothing (see bfs.cu)
+      if (reached == p.nc) {
+        if (stats && L < 255) p.trace[L] = bu ? 'b' : 't';
+        if (stats && L < 256) p.level_claims[L] = 0;
+        ++L;
+        break;
       }
     }
   }
