@@ -42,7 +42,7 @@ struct Peers {
 
 // ctr layout (per partition, exchange block): [0..15] four level slots of
 // {claims, scout, top-down grab counter, unused}; [16], [17] conversion
-// counters (packed list length << 36 | chunks); [30] cross barriers completed by
+// counters (packed list length << 36 | owned edges); [30] cross barriers completed by
 // earlier launches.
 constexpr int kShift = 36;
 constexpr unsigned long long kMask = (1ull << kShift) - 1;
@@ -118,10 +118,6 @@ __device__ void part_sync(const PartParams& pp, const PartDev& me, PSmem& sm,
   __syncthreads();
 }
 
-__device__ __forceinline__ uint32_t seg_chunks(const uint2* seg, uint32_t u) {
-  return (seg[u].y + kTdChunk - 1) / kTdChunk;
-}
-
 // Replicated frontier bitmap -> this partition's list of frontier vertices
 // with a non-empty owned segment.
 __device__ void part_convert(const BfsParams& p, const PartDev& me, const uint32_t* fcur,
@@ -130,9 +126,9 @@ __device__ void part_convert(const BfsParams& p, const PartDev& me, const uint32
   for (uint64_t w0 = gw * 32; w0 < p.nwords; w0 += nw * 32) {
     const uint64_t wi = w0 + lane;
     const uint32_t bits = wi < p.nwords ? fcur[wi] : 0u;
-    uint32_t cnt = 0, nch = 0;
+    uint32_t cnt = 0, nch = 0;  // vertices with an owned segment, their owned edges
     for (uint32_t b = bits; b; b &= b - 1) {
-      const uint32_t c = seg_chunks(me.seg, static_cast<uint32_t>(wi * 32 + __ffs(b) - 1));
+      const uint32_t c = me.seg[static_cast<uint32_t>(wi * 32 + __ffs(b) - 1)].y;
       cnt += c != 0;
       nch += c;
     }
@@ -146,7 +142,7 @@ __device__ void part_convert(const BfsParams& p, const PartDev& me, const uint32
     uint64_t vpos = (old >> kShift) + vin - cnt, cpos = (old & kMask) + cin - nch;
     for (uint32_t b = bits; b; b &= b - 1) {
       const uint32_t v = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
-      const uint32_t c = seg_chunks(me.seg, v);
+      const uint32_t c = me.seg[v].y;
       if (!c) continue;
       me.qv[vpos] = v;
       me.qp[vpos] = cpos;
@@ -156,28 +152,84 @@ __device__ void part_convert(const BfsParams& p, const PartDev& me, const uint32
   }
 }
 
-// Top-down over the owned segments of the frontier rows.
-__device__ void part_td(const BfsParams& p, const PartDev& me, uint64_t nq, uint64_t nu,
+// Top-down over the owned segments of the frontier rows, merge path: the list
+// holds the frontier vertices with a non-empty owned segment and the exclusive
+// prefix of the segment lengths; the concatenated segments are cut into
+// kTdChunk-edge chunks (long segments span many, short ones share one), a
+// warp's chunk window of list entries staged in shared memory (as td_step in
+// bfs.cu, without the list emission: partitions rebuild their lists from the
+// replicated bitmap).
+__device__ __forceinline__ uint32_t pwin_search(const int32_t* win, int32_t rel) {
+  uint32_t lo = 0, hi = kTdChunk;
+  while (hi - lo > 1) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (win[m] <= rel) lo = m; else hi = m;
+  }
+  return lo;
+}
+
+__device__ void part_td(const BfsParams& p, const PartDev& me, uint64_t nq, uint64_t ne,
                         const Peers& fnext, unsigned long long* grab, int32_t dnext, uint64_t gw,
-                        uint64_t nw, unsigned long long& scout_acc,
+                        uint64_t nw, int32_t* win, unsigned long long& scout_acc,
                         unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31;
+  const uint64_t nu = (ne + kTdChunk - 1) / kTdChunk;
+  const uint32_t* qv = me.qv;
+  const uint64_t* qp = me.qp;
   for (uint64_t g0 = gw, gn = 1; g0 < nu;) {
     const uint64_t g1 = min(nu, g0 + gn);
-    uint64_t i = find_vertex(me.qp, nq, g0);
-    for (uint64_t unit = g0; unit < g1; ++unit) {
-      while (i + 1 < nq && me.qp[i + 1] <= unit) ++i;
-      const uint32_t u = me.qv[i];
-      const uint2 sg = me.seg[u];
-      const uint64_t sb = p.crow[u] + sg.x;
-      const uint64_t beg = sb + (unit - me.qp[i]) * kTdChunk;
-      const uint64_t end = min(sb + sg.y, beg + kTdChunk);
-      uint32_t w[kPEpl], vw[kPEpl];
+    uint64_t i = find_vertex(qp, nq, g0 * kTdChunk);
+    for (uint64_t c = g0; c < g1; ++c) {
+      const uint64_t e0 = c * kTdChunk, e1 = min(ne, e0 + kTdChunk);
+      const uint64_t qi = qp[i];
+      const uint64_t iend = i + 1 < nq ? qp[i + 1] : ne;
+      const bool single = iend >= e1;
+      uint64_t inext;
+      if (!single) {
+        for (uint32_t k = lane; k < kTdChunk; k += 32) {
+          const uint64_t ii = i + k;
+          int32_t wv = 0x7FFFFFFF;
+          if (ii < nq) {
+            const uint64_t q = qp[ii];
+            wv = q <= e0 ? (k == 0 ? 0 : -1) : (q - e0 > kTdChunk ? 0x7FFFFFFF : (int32_t)(q - e0));
+          }
+          win[k] = wv;
+        }
+        __syncwarp();
+        inext = i + pwin_search(win, kTdChunk);
+      } else {
+        inext = iend == e1 ? i + 1 : i;
+      }
+      uint32_t u[kPEpl], w[kPEpl], vw[kPEpl];
       bool cl[kPEpl];
+      if (single) {  // one segment: its vertex and start once for the chunk
+        const uint32_t uu = qv[i];
+        const uint64_t base = p.crow[uu] + me.seg[uu].x + (e0 - qi);
 #pragma unroll
-      for (int j = 0; j < kPEpl; ++j) {
-        const uint64_t e = beg + lane + 32 * j;
-        w[j] = e < end ? p.ccol[e] : kNone32;
+        for (int j = 0; j < kPEpl; ++j) {
+          const uint32_t rel = lane + 32 * j;
+          u[j] = rel < e1 - e0 ? uu : kNone32;
+          w[j] = u[j] != kNone32 ? p.ccol[base + rel] : kNone32;
+        }
+      } else {
+        uint32_t k = pwin_search(win, static_cast<int32_t>(lane));
+#pragma unroll
+        for (int j = 0; j < kPEpl; ++j) {
+          const uint32_t rel = lane + 32 * j;
+          while (k + 1 < kTdChunk && win[k + 1] <= static_cast<int32_t>(rel)) ++k;
+          u[j] = rel < e1 - e0 ? qv[i + k] : kNone32;
+          w[j] = static_cast<uint32_t>(k);
+        }
+#pragma unroll
+        for (int j = 0; j < kPEpl; ++j) {
+          const uint32_t rel = lane + 32 * j;
+          uint32_t col = kNone32;
+          if (u[j] != kNone32) {
+            const uint64_t vs = w[j] == 0 ? qi : e0 + static_cast<uint64_t>(max(win[w[j]], 0));
+            col = p.ccol[p.crow[u[j]] + me.seg[u[j]].x + (e0 + rel - vs)];
+          }
+          w[j] = col;
+        }
       }
 #pragma unroll
       for (int j = 0; j < kPEpl; ++j) vw[j] = w[j] != kNone32 ? me.visited[w[j] >> 5] : ~0u;
@@ -192,7 +244,7 @@ __device__ void part_td(const BfsParams& p, const PartDev& me, uint64_t nq, uint
       for (int j = 0; j < kPEpl; ++j) {
         dg[j] = 0;
         if (cl[j]) {
-          p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u);
+          p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u[j]);
           fnext.or_bit(w[j]);
           dg[j] = p.degn[w[j]];
         }
@@ -202,12 +254,15 @@ __device__ void part_td(const BfsParams& p, const PartDev& me, uint64_t nq, uint
         scout_acc += dg[j];
         claims_acc += cl[j];
       }
+      __syncwarp();
+      i = inext;
     }
     if (nu <= nw) break;
     unsigned long long next = 0;
-    if (lane == 0) next = nw + atomicAdd(grab, kPGrab);
+    const uint64_t want = nu <= 8 * nw ? 1 : kPGrab;
+    if (lane == 0) next = nw + atomicAdd(grab, (unsigned long long)want);
     g0 = __shfl_sync(0xffffffffu, next, 0);
-    gn = kPGrab;
+    gn = want;
   }
 }
 
@@ -316,6 +371,11 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
   const uint32_t start = p.start;
   const bool run_core = start != kNone32;
   unsigned long long xk = me.ctr[30];  // cross barriers completed by earlier launches
+  // phase timestamps as the single-partition kernel's (partition 0, block 0)
+  auto pstamp = [&](uint32_t slot) {
+    if (stats && slot < 512) p.level_claims[slot] = gtimer();
+  };
+  pstamp(256);
 
   // ---- init (own replicas) ----------------------------------------------------
   const uint32_t tail = p.nc & 31u;
@@ -337,6 +397,7 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
   const unsigned long long per_barrier = static_cast<unsigned long long>(pp.nparts) * gsize;
   ++xk;  // every partition initialised its replicas before any peer writes into them
   part_sync(pp, me, sm, 0, 0, 0, xk * per_barrier, nullptr, 0);
+  pstamp(257);
 
   uint32_t L = 0;
   if (run_core) {
@@ -380,8 +441,8 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
         if (threadIdx.x == 0) sm.tot[2] = ld_volatile(cslot);  // once per CTA
         __syncthreads();
         const unsigned long long cp = sm.tot[2];
-        part_td(p, me, cp >> kShift, cp & kMask, fn, &slot[2], dnext, gw, nw, scout_acc,
-                claims_acc);
+        part_td(p, me, cp >> kShift, cp & kMask, fn, &slot[2], dnext, gw, nw,
+                reinterpret_cast<int32_t*>(sm.mbuf[threadIdx.x >> 5]), scout_acc, claims_acc);
       }
       // one barrier over all partitions: partials added everywhere, claims already
       // published into every replica
@@ -390,6 +451,7 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
       const unsigned long long claims = sm.tot[0];
       const unsigned long long scout_tot = sm.tot[1];
       reached += claims;
+      pstamp(258 + L);
       if (stats && L < 256) p.level_claims[L] = claims;
       ++L;
       if (bu && p.bottom_up_only) {
@@ -418,6 +480,7 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
         if (stats && L < 255) p.trace[L] = bu ? 'b' : 't';
         if (stats && L < 256) p.level_claims[L] = 0;
         ++L;
+        pstamp(258 + L - 1);
         break;
       }
     }
@@ -450,6 +513,7 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
     if (gtid == static_cast<uint64_t>(k) && static_cast<uint32_t>(k) < p.nipatch &&
         owns(me, p.ipatch[3 * k]))
       p.dp[p.ipatch[3 * k]] = make_uint2(p.ipatch[3 * k + 1], p.ipatch[3 * k + 2]);
+  pstamp(511);
 }
 
 // seg[u] = {offset, length} of u's neighbours inside [lo, hi) (rows ascend).

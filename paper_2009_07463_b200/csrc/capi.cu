@@ -177,8 +177,11 @@ void collect_stats(etb_layout* h, etb_bfs_stats* st) {
   ETB_CUDA(cudaMemcpyAsync(ts, h->S.level_claims.get() + 256, 256 * 8, cudaMemcpyDeviceToHost,
                            h->stream));
   ETB_CUDA(cudaStreamSynchronize(h->stream));
-  if (!h->P) {  // the partitioned kernel records no timestamps
-    for (uint32_t i = 0; i <= nl && i + 1 < 255; ++i) st->level_ns[i] = ts[1 + i] - ts[0];
+  // both kernels stamp (partition 0's first block when partitioned); a rank
+  // that does not run partition 0 has no stamps
+  if (ts[0] && ts[255] >= ts[0]) {
+    for (uint32_t i = 0; i <= nl && i + 1 < 255; ++i)
+      st->level_ns[i] = ts[1 + i] >= ts[0] ? ts[1 + i] - ts[0] : 0;
     st->total_ns = ts[255] - ts[0];
   }
   st->levels = nl;
