@@ -200,25 +200,34 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
       // vertex and column position of each of the lane's 8 edges
       uint32_t u[kEpl], w[kEpl], vw[kEpl];
       bool cl[kEpl];
-      uint32_t k = single ? 0u : win_search(win, static_cast<int32_t>(lane));
+      if (single) {  // one row: its vertex and row start once for the chunk
+        const uint32_t uu = root != kNone32 ? root : qv[i];
+        const uint64_t base = p.crow[uu] + (e0 - qi);
 #pragma unroll
-      for (int j = 0; j < kEpl; ++j) {
-        const uint32_t rel = lane + 32 * j;
-        if (!single)
-          while (k + 1 < kTdChunk && win[k + 1] <= static_cast<int32_t>(rel)) ++k;
-        u[j] = rel < e1 - e0 ? (single ? (root != kNone32 ? root : qv[i]) : qv[i + k]) : kNone32;
-        w[j] = static_cast<uint32_t>(k);  // relative vertex index for now
-      }
-#pragma unroll
-      for (int j = 0; j < kEpl; ++j) {
-        const uint32_t rel = lane + 32 * j;
-        uint32_t col = kNone32;
-        if (u[j] != kNone32) {
-          const uint64_t qs = single ? qi : e0 + static_cast<uint64_t>(max(win[w[j]], 0));
-          const uint64_t vs = single ? qi : (w[j] == 0 ? qi : qs);
-          col = p.ccol[p.crow[u[j]] + (e0 + rel - vs)];
+        for (int j = 0; j < kEpl; ++j) {
+          const uint32_t rel = lane + 32 * j;
+          u[j] = rel < e1 - e0 ? uu : kNone32;
+          w[j] = u[j] != kNone32 ? p.ccol[base + rel] : kNone32;
         }
-        w[j] = col;
+      } else {
+        uint32_t k = win_search(win, static_cast<int32_t>(lane));
+#pragma unroll
+        for (int j = 0; j < kEpl; ++j) {
+          const uint32_t rel = lane + 32 * j;
+          while (k + 1 < kTdChunk && win[k + 1] <= static_cast<int32_t>(rel)) ++k;
+          u[j] = rel < e1 - e0 ? qv[i + k] : kNone32;
+          w[j] = static_cast<uint32_t>(k);  // relative vertex index for now
+        }
+#pragma unroll
+        for (int j = 0; j < kEpl; ++j) {
+          const uint32_t rel = lane + 32 * j;
+          uint32_t col = kNone32;
+          if (u[j] != kNone32) {
+            const uint64_t vs = w[j] == 0 ? qi : e0 + static_cast<uint64_t>(max(win[w[j]], 0));
+            col = p.ccol[p.crow[u[j]] + (e0 + rel - vs)];
+          }
+          w[j] = col;
+        }
       }
       // With a list to emit (small frontiers) every target's {core, full}
       // degree is fetched with its visited word, off the claim's critical path;
