@@ -1,26 +1,33 @@
 // (3)+(4) The ET-BFS traversal on sm_100a: one persistent cooperative kernel
 // per root runs the whole of et_bfs (src/et_bfs.cpp:59-124) —
-//   init            visited/frontier bitmaps sized to the CORE (not n), seeded
-//                   with the effective start (et_bfs.cpp:96-98);
+//   start           visited/frontier bitmaps sized to the CORE (not n), double
+//                   buffered: this launch runs on a half the previous one
+//                   cleaned and cleans the other; only the start bits are set
+//                   (et_bfs.cpp:96-98);
 //   level loop      the reference's α/β direction-optimizing driver
 //                   (src/bfs.cpp:232-293), decided redundantly by every thread
 //                   from grid-reduced counters, with no host round trip;
-//                     top-down  (bfs.cpp:61-86): the frontier's rows are cut in
-//                               256-edge chunks spread evenly over all warps,
-//                               8 edges per lane in flight, check-then-atomicOr
-//                               claims staged in smem and appended in batches;
-//                     bottom-up (bfs.cpp:88-111): one warp per 32-vertex visited
-//                               word, first probe on the contiguous first-
+//                     top-down  (bfs.cpp:61-86): merge path — the frontier's
+//                               rows concatenated and cut into 128-edge chunks,
+//                               4 edges per lane in flight, check-then-atomicOr
+//                               claims staged in smem and appended to the next
+//                               list in batches (td_step);
+//                     bottom-up (bfs.cpp:88-111): 8 visited words per warp, lane
+//                               = vertex, first probe on the contiguous first-
 //                               neighbour array (the highest-degree neighbour,
-//                               since relaid ids are degree sorted), early exit,
-//                               one word write-back per warp;
+//                               since relaid ids are degree sorted), deferred
+//                               scans for misses, one word write-back per word
+//                               (bu_step);
+//                   and stops once every core vertex is visited (the level the
+//                   reference would run next claims nothing);
 //   tree replay     TEET/TEOLV (et_bfs.cpp:14-32) as one streaming pass giving
 //                   every tree vertex parent = src and depth = depth(anchor) +
 //                   tree depth; unreached core vertices get -1 in the same phase;
 //   start tree      the start-side walk (et_bfs.cpp:34-57) is precomputed on the
-//                   host and applied as a patch.
-// Levels are separated by a grid barrier; the grid is one wave of co-resident
-// CTAs (cooperative launch).
+//                   host and applied as a patch (in the launch parameters when
+//                   small).
+// Levels are separated by a grid barrier; the grid is one CTA per SM
+// (cooperative launch). DESIGN.md §4 lists the measured choices.
 #include <cstdlib>
 #include <algorithm>
 
@@ -94,7 +101,7 @@ __device__ void grid_sync_add(unsigned long long* bar, Smem& sm, unsigned long l
 
 // Frontier list: vertices qv[0..nq) with at least one core edge, and the
 // exclusive prefix qp[] of their core degrees (ne = total edges). A top-down
-// level cuts the concatenated rows into 256-edge chunks (merge path): hub rows
+// level cuts the concatenated rows into 128-edge chunks (merge path): hub rows
 // span many chunks, tiny rows share one, and every chunk is the same work. Each
 // warp takes one chunk, then pulls more from a per-level counter: one at a
 // time on levels of at most 8 chunks per warp, kGrab at a time on longer ones.
@@ -154,7 +161,7 @@ __device__ __forceinline__ uint32_t win_search(const int32_t* win, int32_t rel) 
   return lo;
 }
 
-// Top-down step (bfs.cpp:61-86). Each lane owns 8 edges of the warp's chunk;
+// Top-down step (bfs.cpp:61-86). Each lane owns 4 edges of the warp's chunk;
 // their column loads, visited probes and claim atomics are issued before any
 // result is consumed.
 // kMode: 0 no list, 3 no list and no scout (summed after the level by
