@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <string>
 
+#include "etbfs/preprocess.hpp"
 #include "etbfs/types.hpp"
 
 namespace etbfs {
@@ -27,6 +28,13 @@ BfsTree bfs_top_down(const CsrGraph& graph, vertex_t root, KernelStats* stats = 
 
 BfsTree bfs_hybrid(const CsrGraph& graph, vertex_t root, const HybridPolicy& policy = {},
                    KernelStats* stats = nullptr);
+
+// Hybrid driver with the degree-aware bottom-up phase / the standalone
+// block-search sweep (bfs.hpp:57-65). The split must cover the whole graph.
+BfsTree bfs_degree_aware(const CsrGraph& graph, const DegreeSplitAdjacency& split, vertex_t root,
+                         const HybridPolicy& policy = {}, KernelStats* stats = nullptr);
+BfsTree bfs_block_search(const CsrGraph& graph, const DegreeSplitAdjacency& split, vertex_t root,
+                         KernelStats* stats = nullptr);
 
 std::uint64_t restricted_edge_count(const CsrGraph& graph, vertex_t limit);
 

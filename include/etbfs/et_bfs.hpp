@@ -2,6 +2,7 @@
 #pragma once
 
 #include "etbfs/bfs.hpp"
+#include "etbfs/preprocess.hpp"
 #include "etbfs/types.hpp"
 
 namespace etbfs {
@@ -19,10 +20,9 @@ enum class TreeReplay {
   kTeolv,
 };
 
-// Reference preprocess.hpp:26. The split-based kernels require a non-null split
-// (as the reference does, et_bfs.cpp:69-70) but the device does not read it: its
+// The split-based kernels require a split matching the core block (as the
+// reference checks, et_bfs.cpp:69-78) but the device does not read it: its
 // relaid rows already list neighbours by descending degree.
-struct DegreeSplitAdjacency;
 
 // et_bfs over a relaid graph. The first call on a given (cg, etl) pair uploads
 // it and builds the device layout; later calls on the same objects reuse it

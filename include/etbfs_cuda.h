@@ -20,6 +20,9 @@
  *   etb_layout_restricted_edges include/etbfs/bfs.hpp:123       restricted_edge_count
  *   etb_graph_file_read/_write  include/etbfs/io.hpp:23-24      read_graph / write_graph
  *   etb_tree_file_read/_write   include/etbfs/io.hpp:30-31      read_tree / write_tree
+ *   etb_graph_degree_split      include/etbfs/preprocess.hpp:69 split_degree_aware
+ *   etb_graph_levels            include/etbfs/validate.hpp:37   oracle_bfs
+ *   etb_graph_validate_tree     include/etbfs/validate.hpp:46   validate_bfs_tree
  *
  * Index spaces: "original" ids are the input graph's; "relaid" ids are the
  * relayout_csr space (core block [0, core), then edge trees, then isolated
@@ -126,6 +129,28 @@ int etb_graph_info(const etb_graph* g, uint64_t* vertex_count, uint64_t* directe
 int etb_graph_download(const etb_graph* g, uint64_t* row_offsets, uint64_t* cols,
                        uint64_t* degrees);
 void etb_graph_free(etb_graph* g);
+
+/* ---- checker-side and preprocessing helpers on a device graph ------------- */
+/* split_degree_aware (preprocess.hpp:69): per vertex the highest-degree
+ * neighbour below `limit` (in_plus, ETB_NO_VERTEX if none; ties: smallest id)
+ * and the rest by descending degree, ascending id (minus). minus_offsets (n+1)
+ * is always written; in_plus (n) and minus_cols (minus_offsets[n]) may be NULL
+ * (sizing call). limit = ETB_NO_VERTEX keeps every neighbour. */
+int etb_graph_degree_split(const etb_graph* g, uint64_t limit, uint64_t* in_plus,
+                           uint64_t* minus_offsets, uint64_t* minus_cols);
+/* oracle_bfs (validate.hpp:37): BFS levels from root (ETB_NO_VERTEX = unreached),
+ * a plain level-synchronous device BFS independent of the ET-BFS kernels. */
+int etb_graph_levels(const etb_graph* g, uint64_t root, uint64_t* levels);
+/* validate_bfs_tree (validate.hpp:46) of a host parent array (n u64, original
+ * ids of g) rooted at root: counts[0] = 1 if every rule holds, counts[r] =
+ * failures of rule r (1..5; rule 2: bad parent chains), counts[6] reached
+ * vertices, counts[7] traversed edges (half the reached degree sum). For each
+ * rule the first (up to 25) failures in the reference's order go to
+ * where[(r-1)*25 + i] (rule 4: the edge's smaller endpoint; rule 2: bit 62 set
+ * for a dead end, clear for a cycle) with first_count[r-1] of them; both may
+ * be NULL. */
+int etb_graph_validate_tree(const etb_graph* g, uint64_t root, const uint64_t* parent,
+                            uint64_t* counts, uint64_t* where, uint32_t* first_count);
 
 /* ---- (2) edge-tree preprocessing ----------------------------------------- */
 /* types_out (n u8, may be NULL); counts_out (5 u64 CI/CE/TI/TL/VZ, may be NULL). */

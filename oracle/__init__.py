@@ -97,6 +97,8 @@ def ref() -> C.CDLL:
         _sig(L.ref_last_error, C.c_char_p)
         cp = C.c_char_p
         _sig(L.ref_write_graph, C.c_int, cp, C.c_int, u64, vp, u64)
+        _sig(L.ref_split_degree_aware, C.c_int, vp, u64, vp, vp, vp)
+        _sig(L.ref_validate_report, C.c_int, vp, u64, vp, vp, vp)
         _sig(L.ref_read_graph, C.c_int, cp, C.c_int, C.POINTER(u64), C.POINTER(u64), vp)
         _sig(L.ref_write_tree, C.c_int, cp, u64, u64, vp)
         _sig(L.ref_read_tree, C.c_int, cp, C.POINTER(u64), C.POINTER(u64), vp)

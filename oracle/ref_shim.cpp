@@ -32,6 +32,7 @@
 #include "etbfs/et_bfs.hpp"
 #include "etbfs/io.hpp"
 #include "etbfs/kronecker.hpp"
+#include "etbfs/preprocess.hpp"
 #include "etbfs/relayout.hpp"
 #include "etbfs/validate.hpp"
 
@@ -59,6 +60,47 @@ EdgeList make_list(uint64_t n, const uint64_t* pairs, uint64_t count) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// ---- degree split (preprocess.hpp:69) --------------------------------------------
+// minus_cols == nullptr: sizes only (minus_offsets, n + 1, always written).
+int ref_split_degree_aware(void* h, uint64_t limit, uint64_t* in_plus, uint64_t* minus_offsets,
+                           uint64_t* minus_cols) {
+  try {
+    const CsrGraph& g = *static_cast<CsrGraph*>(h);
+    const DegreeSplitAdjacency sp = split_degree_aware(g, limit);
+    std::memcpy(minus_offsets, sp.minus_offsets.data(), sp.minus_offsets.size() * 8);
+    if (in_plus) std::memcpy(in_plus, sp.in_plus.data(), sp.in_plus.size() * 8);
+    if (minus_cols && !sp.minus_cols.empty())
+      std::memcpy(minus_cols, sp.minus_cols.data(), sp.minus_cols.size() * 8);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// validate_bfs_tree with the report's per-rule failure counts (capped lists).
+int ref_validate_report(void* h, uint64_t root, const uint64_t* parent, uint64_t* out8,
+                        uint64_t* where125) {
+  try {
+    const CsrGraph& g = *static_cast<CsrGraph*>(h);
+    BfsTree t;
+    t.root = root;
+    t.parent.assign(parent, parent + g.vertex_count);
+    const ValidationReport rep = validate_bfs_tree(g, t);
+    std::memset(out8, 0, 64);
+    out8[0] = rep.passed;
+    uint64_t idx[6] = {};
+    for (const auto& f : rep.failures) {
+      ++out8[f.rule];
+      if (where125 && idx[f.rule] < 25) where125[(f.rule - 1) * 25 + idx[f.rule]++] = f.where;
+    }
+    out8[6] = rep.reached_count;
+    out8[7] = rep.traversed_edge_count;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
 
 // ---- graph / tree files (io.hpp) ------------------------------------------------
 int ref_write_graph(const char* path, int text, uint64_t n, const uint64_t* pairs, uint64_t count) {

@@ -366,6 +366,58 @@ int etb_graph_info(const etb_graph* g, uint64_t* n, uint64_t* nnz) {
   });
 }
 
+int etb_graph_degree_split(const etb_graph* g, uint64_t limit, uint64_t* in_plus,
+                           uint64_t* minus_offsets, uint64_t* minus_cols) {
+  return guarded([&] {
+    need(g, "etb_graph_degree_split");
+    need(minus_offsets, "etb_graph_degree_split");
+    ETB_CUDA(cudaSetDevice(g->device));
+    etb::graph_degree_split(g->g, limit, in_plus, minus_offsets, minus_cols, g->stream);
+  });
+}
+
+int etb_graph_levels(const etb_graph* g, uint64_t root, uint64_t* levels) {
+  return guarded([&] {
+    need(g, "etb_graph_levels");
+    need(levels, "etb_graph_levels");
+    if (root >= g->g.n) throw std::invalid_argument("oracle_bfs: root out of range");
+    ETB_CUDA(cudaSetDevice(g->device));
+    etb::DevBuf<uint32_t> lvl;
+    etb::graph_levels(g->g, root, lvl, g->stream);
+    std::vector<uint32_t> h(g->g.n);
+    if (g->g.n)
+      ETB_CUDA(cudaMemcpyAsync(h.data(), lvl.get(), g->g.n * 4, cudaMemcpyDeviceToHost,
+                               g->stream));
+    ETB_CUDA(cudaStreamSynchronize(g->stream));
+    for (uint64_t i = 0; i < g->g.n; ++i) levels[i] = h[i] == etb::kNone32 ? ~uint64_t{0} : h[i];
+  });
+}
+
+int etb_graph_validate_tree(const etb_graph* g, uint64_t root, const uint64_t* parent,
+                            uint64_t* counts, uint64_t* where, uint32_t* first_count) {
+  return guarded([&] {
+    need(g, "etb_graph_validate_tree");
+    need(parent, "etb_graph_validate_tree");
+    need(counts, "etb_graph_validate_tree");
+    if (root >= g->g.n) throw std::invalid_argument("validate_bfs_tree: root out of range");
+    ETB_CUDA(cudaSetDevice(g->device));
+    uint64_t out[8] = {};
+    std::vector<uint64_t> first[6];
+    etb::graph_validate_tree(g->g, root, parent, out, first, g->stream);
+    bool ok = true;
+    for (int r = 1; r <= 5; ++r) ok = ok && out[r] == 0;
+    counts[0] = ok;
+    for (int r = 1; r <= 7; ++r) counts[r] = out[r];
+    for (int r = 1; r <= 5; ++r) {
+      const size_t m = std::min<size_t>(first[r].size(), 25);
+      if (first_count) first_count[r - 1] = static_cast<uint32_t>(m);
+      if (where)
+        for (size_t i = 0; i < m; ++i)
+          where[(r - 1) * 25 + i] = r == 4 ? (first[r][i] >> 32) : first[r][i];
+    }
+  });
+}
+
 int etb_graph_download(const etb_graph* g, uint64_t* row, uint64_t* cols, uint64_t* degrees) {
   return guarded([&] {
     need(g, "etb_graph_download");

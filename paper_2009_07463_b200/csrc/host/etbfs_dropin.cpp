@@ -156,7 +156,8 @@ BfsTree run(etb_layout* l, uint64_t n, uint64_t start_dev, const etb_bfs_options
 BfsTree whole_graph(const CsrGraph& graph, vertex_t root, const etb_bfs_options& o,
                     KernelStats* stats) {
   if (root >= graph.vertex_count) throw std::invalid_argument("bfs: root out of range");
-  if (o.kernel == ETB_KERNEL_HYBRID && (!(o.alpha > 0.0) || !(o.beta > 0.0)))
+  if ((o.kernel == ETB_KERNEL_HYBRID || o.kernel == ETB_KERNEL_DEGREE_AWARE) &&
+      (!(o.alpha > 0.0) || !(o.beta > 0.0)))
     throw std::invalid_argument("run_hybrid: alpha and beta must be positive");
   GraphPtr g = upload(graph);
   std::vector<uint8_t> types(graph.vertex_count, ETB_CI);
@@ -317,8 +318,14 @@ BfsTree et_bfs(const ClassifiedGraph& cg, const EdgeTreeList& etl, vertex_t star
   const bool needs_split = kernel == CoreKernel::kDegreeAware ||
                            kernel == CoreKernel::kBlockSearch ||
                            kernel == CoreKernel::kHybridBlockSearch;
-  if (needs_split && split == nullptr)
-    throw std::invalid_argument("et_bfs: kernel needs a degree split");
+  if (needs_split) {
+    if (split == nullptr) throw std::invalid_argument("et_bfs: kernel needs a degree split");
+    const uint64_t core = cg.core_vertex_count;
+    const bool covers_core =
+        split->neighbor_limit == core || (split->neighbor_limit == kNoVertex && core == n);
+    if (split->in_plus.size() != n || !covers_core)
+      throw std::invalid_argument("et_bfs: split does not match the core block");
+  }
   const etb_bfs_options o = options(kernel, replay, policy);
   std::lock_guard<std::mutex> lk(g_cache_mu);
   DeviceCg& d = device_cg(cg);
@@ -332,6 +339,31 @@ BfsTree bfs_top_down(const CsrGraph& graph, vertex_t root, KernelStats* stats) {
 BfsTree bfs_hybrid(const CsrGraph& graph, vertex_t root, const HybridPolicy& policy,
                    KernelStats* stats) {
   return whole_graph(graph, root, options(CoreKernel::kHybrid, TreeReplay::kTeet, policy), stats);
+}
+
+namespace {
+// bfs.cpp:25-30: the whole-graph split kernels need a split of the whole graph.
+void check_full_split(const CsrGraph& graph, const DegreeSplitAdjacency& split) {
+  if (split.in_plus.size() != graph.vertex_count)
+    throw std::invalid_argument("bfs: split size does not match graph");
+  if (split.neighbor_limit != kNoVertex && split.neighbor_limit < graph.vertex_count)
+    throw std::invalid_argument("bfs: split excludes neighbors the traversal needs");
+}
+}  // namespace
+
+BfsTree bfs_degree_aware(const CsrGraph& graph, const DegreeSplitAdjacency& split, vertex_t root,
+                         const HybridPolicy& policy, KernelStats* stats) {
+  if (root >= graph.vertex_count) throw std::invalid_argument("bfs: root out of range");
+  check_full_split(graph, split);
+  return whole_graph(graph, root, options(CoreKernel::kDegreeAware, TreeReplay::kTeet, policy),
+                     stats);
+}
+
+BfsTree bfs_block_search(const CsrGraph& graph, const DegreeSplitAdjacency& split, vertex_t root,
+                         KernelStats* stats) {
+  if (root >= graph.vertex_count) throw std::invalid_argument("bfs: root out of range");
+  check_full_split(graph, split);
+  return whole_graph(graph, root, options(CoreKernel::kBlockSearch, TreeReplay::kTeet, {}), stats);
 }
 
 std::uint64_t restricted_edge_count(const CsrGraph& graph, vertex_t limit) {

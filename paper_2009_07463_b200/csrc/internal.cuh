@@ -90,4 +90,14 @@ void inclusive_max_scan_u32(const uint32_t* in, uint32_t* out, uint64_t count, c
 // Scratch device counter helpers.
 uint64_t read_u64(const uint64_t* dev, cudaStream_t s);
 
+// graph_tools.cu: split_degree_aware / oracle_bfs / validate_bfs_tree on an
+// uploaded graph (host outputs; h_minus may be null to size it from h_moff[n]).
+void graph_degree_split(const DevGraph& g, uint64_t limit, uint64_t* h_in_plus, uint64_t* h_moff,
+                        uint64_t* h_minus, cudaStream_t s);
+void graph_levels(const DevGraph& g, uint64_t root, DevBuf<uint32_t>& lvl, cudaStream_t s);
+// out[r] = failures of rule r (1..5; rule 2: bad chain representatives),
+// out[6] reached, out[7] traversed edges; first[r] = sorted failure keys.
+void graph_validate_tree(const DevGraph& g, uint64_t root, const uint64_t* h_parent,
+                         uint64_t out[8], std::vector<uint64_t> first[6], cudaStream_t s);
+
 }  // namespace etb

@@ -175,6 +175,9 @@ def lib() -> C.CDLL:
     sig("etb_host_register", vp, u64)
     sig("etb_host_unregister", vp)
     sig("etb_time_roots", vp, vp, u64, C.c_int, C.c_int, C.POINTER(_BfsOptions), vp, vp)
+    sig("etb_graph_degree_split", vp, u64, vp, vp, vp)
+    sig("etb_graph_levels", vp, u64, vp)
+    sig("etb_graph_validate_tree", vp, u64, vp, vp, vp, vp)
     cp = C.c_char_p
     sig("etb_graph_file_read", cp, i32, C.POINTER(vp))
     sig("etb_graph_file_info", vp, P64, P64, C.POINTER(C.POINTER(C.c_uint64)))
@@ -552,3 +555,48 @@ def read_tree(path: str):
     _check(lib().etb_tree_file_read(os.fsencode(path), C.byref(n), C.byref(root), _ptr(parent),
                                     n.value))
     return root.value, parent
+
+
+# ---- checker-side helpers on a device graph (preprocess.hpp / validate.hpp) ----
+def split_degree_aware(g: Csr, neighbor_limit: int | None = None):
+    """split_degree_aware (preprocess.hpp:69) on the GPU -> (in_plus u64[n],
+    minus_offsets u64[n+1], minus_cols u64[...]); None keeps every neighbour."""
+    lim = 0xFFFFFFFFFFFFFFFF if neighbor_limit is None else int(neighbor_limit)
+    n = g.vertex_count
+    moff = np.empty(n + 1, np.uint64)
+    _check(lib().etb_graph_degree_split(g.handle, lim, None, _ptr(moff), None))
+    in_plus = np.empty(max(n, 1), np.uint64)
+    minus = np.empty(max(int(moff[n]), 1), np.uint64)
+    _check(lib().etb_graph_degree_split(g.handle, lim, _ptr(in_plus), _ptr(moff), _ptr(minus)))
+    return in_plus[:n], moff, minus[: int(moff[n])]
+
+
+def oracle_bfs(g: Csr, root: int) -> np.ndarray:
+    """oracle_bfs (validate.hpp:37): BFS levels (u64, NO_VERTEX unreached) from an
+    independent level-synchronous device BFS."""
+    lv = np.empty(max(g.vertex_count, 1), np.uint64)
+    _check(lib().etb_graph_levels(g.handle, int(root), _ptr(lv)))
+    return lv[: g.vertex_count]
+
+
+RULE_MESSAGES = {1: "root is not its own parent", 4: "edge spans more than one level"}
+
+
+def validate_bfs_tree(g: Csr, root: int, parent: np.ndarray) -> dict:
+    """validate_bfs_tree (validate.hpp:46) of a parent array in g's ids, on the GPU:
+    {passed, rule_counts[1..5], reached_count, traversed_edge_count, failures}."""
+    parent = np.ascontiguousarray(parent, np.uint64)
+    if parent.size != g.vertex_count:
+        raise ValueError("validate_bfs_tree: tree does not match graph vertex count")
+    counts = np.zeros(8, np.uint64)
+    where = np.zeros(125, np.uint64)
+    first = np.zeros(5, np.uint32)
+    _check(lib().etb_graph_validate_tree(g.handle, int(root), _ptr(parent), _ptr(counts),
+                                         _ptr(where), _ptr(first)))
+    failures = []
+    for r in range(1, 6):
+        for i in range(int(first[r - 1])):
+            failures.append((r, int(where[(r - 1) * 25 + i])))
+    return {"passed": bool(counts[0]), "rule_counts": [int(x) for x in counts[1:6]],
+            "reached_count": int(counts[6]), "traversed_edge_count": int(counts[7]),
+            "failures": failures}

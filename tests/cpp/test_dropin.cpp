@@ -12,13 +12,16 @@
 #include <string>
 #include <vector>
 
+#include "etbfs/bench.hpp"
 #include "etbfs/bfs.hpp"
 #include "etbfs/build.hpp"
 #include "etbfs/classify.hpp"
 #include "etbfs/et_bfs.hpp"
 #include "etbfs/io.hpp"
 #include "etbfs/kronecker.hpp"
+#include "etbfs/preprocess.hpp"
 #include "etbfs/relayout.hpp"
+#include "etbfs/validate.hpp"
 
 using namespace etbfs;
 
@@ -122,7 +125,7 @@ std::vector<uint64_t> host_levels(const EdgeList& el, vertex_t root) {
 }
 
 // Levels implied by a parent tree, by fixpoint (shares nothing with the library).
-std::vector<uint64_t> tree_levels(const BfsTree& t) {
+std::vector<uint64_t> fixpoint_levels(const BfsTree& t) {
   const uint64_t n = t.parent.size();
   std::vector<uint64_t> lv(n, kUnreached);
   if (t.root >= n || t.parent[t.root] != t.root) return {};
@@ -151,7 +154,7 @@ EdgeList relabeled(const ClassifiedGraph& cg) {
 void check_tree_exact(const EdgeList& el, const BfsTree& t, vertex_t root) {
   EXPECT(t.root == root);
   const auto want = host_levels(el, root);
-  EXPECT(tree_levels(t) == want);
+  EXPECT(fixpoint_levels(t) == want);
   std::vector<std::set<vertex_t>> adj(el.vertex_count);
   for (const Edge& e : el.edges)
     if (e.src != e.dst) adj[e.src].insert(e.dst), adj[e.dst].insert(e.src);
@@ -181,6 +184,53 @@ void run_case(const char* name, const std::function<void()>& f) {
 }  // namespace
 
 int main() {
+  run_case("degree split, split kernels, checker side (preprocess/validate/bench.hpp)", [] {
+    // star centre 0 with a 2-path hanging off leaf 3: degrees 0:4 3:2
+    const CsrGraph g = build_csr(edges(6, {{0, 1}, {0, 2}, {0, 3}, {0, 4}, {3, 5}}));
+    const DegreeSplitAdjacency sp = split_degree_aware(g);
+    EXPECT(sp.in_plus[3] == 0 && sp.in_plus[0] == 3 && sp.in_plus[5] == 3);
+    EXPECT(std::vector<vertex_t>(sp.in_minus(0).begin(), sp.in_minus(0).end()) ==
+           (std::vector<vertex_t>{1, 2, 4}));
+    const DegreeSplitAdjacency lim = split_degree_aware(g, 3);
+    EXPECT(lim.in_plus[5] == kNoVertex && lim.in_plus[3] == 0 && lim.in_minus(0).size() == 1);
+    for (const EdgeList& el : corpus()) {
+      const CsrGraph cg = build_csr(el);
+      const DegreeSplitAdjacency full = split_degree_aware(cg);
+      for (vertex_t r = 0; r < el.vertex_count; r += 3) {
+        const auto want = host_levels(el, r);
+        EXPECT(fixpoint_levels(bfs_degree_aware(cg, full, r)) == want);
+        EXPECT(fixpoint_levels(bfs_block_search(cg, full, r)) == want);
+        EXPECT(oracle_bfs(cg, r) == want);
+        const BfsTree t = bfs_hybrid(cg, r);
+        EXPECT(tree_levels(t) == want);
+        const ValidationReport rep = validate_bfs_tree(cg, t);
+        EXPECT(rep.passed && rep.failures.empty());
+        if (el.vertex_count > 2 && t.parent[r] == r) {
+          BfsTree bad = t;
+          bad.parent[r] = kNoVertex;
+          const ValidationReport r2 = validate_bfs_tree(cg, bad);
+          EXPECT(!r2.passed && r2.failures.front().rule == kRuleRootParent &&
+                 r2.failures.front().message == "root is not its own parent");
+        }
+      }
+    }
+    EXPECT(throws_with<std::invalid_argument>(
+        [&] { bfs_degree_aware(g, lim, 0); }, "split excludes neighbors the traversal needs"));
+    KroneckerParams kp;
+    kp.scale = 16;
+    kp.seed = 1;
+    const CsrGraph s16 = build_csr(generate_kronecker(kp));
+    const auto roots = select_roots(s16, 8, 1);
+    EXPECT(roots == (std::vector<vertex_t>{23745, 51467, 640, 15525, 34165, 15784, 20321, 24000}));
+    EXPECT(compute_gteps(2000000000, 2.0) == 1.0);
+    EXPECT(throws_with<std::invalid_argument>([] { compute_gteps(1, 0.0); }, "must be positive"));
+    BfsTree tr;
+    tr.root = 1;
+    tr.parent = {1, 1, 0};
+    const BfsTree back = translate_tree(tr, {2, 0, 1});
+    EXPECT(back.root == 0 && back.parent == (std::vector<vertex_t>{0, 2, 0}));
+  });
+
   run_case("graph / tree files (test_io.cpp cases) feeding a GPU traversal", [] {
     const std::string gpath = "/tmp/etbfs_dropin_io.etg", tpath = "/tmp/etbfs_dropin_io.ett";
     const EdgeList el = random_tuples(300, 900, 4);
