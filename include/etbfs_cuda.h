@@ -246,6 +246,20 @@ int etb_time_roots(etb_layout* L, const uint64_t* starts, uint64_t count, int wa
                    int flush_l2, const etb_bfs_options* opts, double* ms_out,
                    double* kernel_ms_out);
 
+/* ---- step / driver layer (bfs.hpp:66-120) on caller-held state ------------ */
+/* op: 0 top_down_step, 1 bottom_up_step, 2 degree_aware_step, 3 block_search_step,
+ * 4 run_top_down, 5 run_hybrid (classic), 6 run_hybrid (degree-aware), 7 run_hybrid
+ * (block-search), 8 run_block_search. visited/current/next: ceil(n/64) u64 bitmap
+ * words, parent: n u64, all host, updated in place. in_plus / minus_offsets /
+ * minus_cols: the degree split (ops 2, 3, 6, 7, 8; else NULL). stats (6 u64,
+ * added to): claimed, scout, probes, skipped blocks, levels, bottom-up levels;
+ * trace (drivers, may be NULL): one 't'/'b' per level, NUL-terminated within
+ * trace_cap. */
+int etb_steps_run(const etb_graph* g, int op, uint64_t limit, uint64_t* visited,
+                  uint64_t* current, uint64_t* next, uint64_t* parent, const uint64_t* in_plus,
+                  const uint64_t* minus_offsets, const uint64_t* minus_cols, double alpha,
+                  double beta, uint64_t* stats, char* trace, uint64_t trace_cap);
+
 /* ---- graph and parent-tree files (io.hpp:9-45, io.cpp:47-181) ------------- */
 /* Byte-identical to the reference's ETG1 / text graph and ETT1 tree files, with
  * its validation order and messages (runtime errors name the path and the byte

@@ -418,6 +418,39 @@ int etb_graph_validate_tree(const etb_graph* g, uint64_t root, const uint64_t* p
   });
 }
 
+int etb_steps_run(const etb_graph* g, int op, uint64_t limit, uint64_t* visited,
+                  uint64_t* current, uint64_t* next, uint64_t* parent, const uint64_t* in_plus,
+                  const uint64_t* minus_offsets, const uint64_t* minus_cols, double alpha,
+                  double beta, uint64_t* stats, char* trace, uint64_t trace_cap) {
+  return guarded([&] {
+    need(g, "etb_steps_run");
+    if (op < 0 || op > 8) throw std::invalid_argument("etb_steps_run: unknown op");
+    const bool split = op == 2 || op == 3 || op == 6 || op == 7 || op == 8;
+    if (split && (!in_plus || !minus_offsets || (minus_offsets[g->g.n] && !minus_cols)))
+      throw std::invalid_argument("run_hybrid: bottom-up kind needs a degree split");
+    if (op >= 5 && op <= 7 && (!(alpha > 0.0) || !(beta > 0.0)))
+      throw std::invalid_argument("run_hybrid: alpha and beta must be positive");
+    if (g->g.n) {
+      need(visited, "etb_steps_run");
+      need(current, "etb_steps_run");
+      need(next, "etb_steps_run");
+      need(parent, "etb_steps_run");
+    }
+    ETB_CUDA(cudaSetDevice(g->device));
+    uint64_t out[6] = {};
+    std::string tr;
+    etb::step_run(g->g, op, limit, visited, current, next, parent, in_plus, minus_offsets,
+                  minus_cols, alpha, beta, out, trace ? &tr : nullptr, g->stream);
+    if (stats)
+      for (int i = 0; i < 6; ++i) stats[i] += out[i];
+    if (trace && trace_cap) {
+      const size_t m = std::min<size_t>(tr.size(), trace_cap - 1);
+      std::memcpy(trace, tr.data(), m);
+      trace[m] = 0;
+    }
+  });
+}
+
 int etb_graph_download(const etb_graph* g, uint64_t* row, uint64_t* cols, uint64_t* degrees) {
   return guarded([&] {
     need(g, "etb_graph_download");

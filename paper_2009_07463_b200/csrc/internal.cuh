@@ -1,6 +1,7 @@
 // Internal device data structures shared by the kernels and the C-ABI.
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include "../../include/etbfs_cuda.h"
@@ -99,5 +100,15 @@ void graph_levels(const DevGraph& g, uint64_t root, DevBuf<uint32_t>& lvl, cudaS
 // out[6] reached, out[7] traversed edges; first[r] = sorted failure keys.
 void graph_validate_tree(const DevGraph& g, uint64_t root, const uint64_t* h_parent,
                          uint64_t out[8], std::vector<uint64_t> first[6], cudaStream_t s);
+
+// steps.cu: the reference's step / driver layer on caller state (host words and
+// parents in, out). ops 0-3 steps (td, bu, degree-aware, block-search), 4
+// run_top_down, 5-7 run_hybrid (classic, degree-aware, block-search), 8
+// run_block_search; out = claimed, scout, probes, skipped blocks, levels,
+// bottom-up levels.
+void step_run(const DevGraph& g, int op, uint64_t limit, uint64_t* h_vis, uint64_t* h_cur,
+              uint64_t* h_nxt, uint64_t* h_parent, const uint64_t* h_in_plus,
+              const uint64_t* h_moff, const uint64_t* h_minus, double alpha, double beta,
+              uint64_t out[6], std::string* trace, cudaStream_t s);
 
 }  // namespace etb

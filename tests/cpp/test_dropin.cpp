@@ -183,7 +183,98 @@ void run_case(const char* name, const std::function<void()>& f) {
 
 }  // namespace
 
+// Host restatement of one bottom-up step's parent rule for the checks below:
+// the first neighbour (in the given order) present in `in`.
+vertex_t first_in(const std::vector<vertex_t>& order, const Bitmap& in) {
+  for (vertex_t x : order)
+    if (in.get(x)) return x;
+  return kNoVertex;
+}
+
 int main() {
+  run_case("step and driver layer on the GPU (bfs.hpp:66-120)", [] {
+    EXPECT(block_search_unvisited(0b1010) == (std::pair<std::uint32_t, std::uint64_t>{1, 0b1000}));
+    for (const EdgeList& el : corpus()) {
+      const CsrGraph g = build_csr(el);
+      const uint64_t n = g.vertex_count;
+      const DegreeSplitAdjacency sp = split_degree_aware(g);
+      for (vertex_t r = 0; r < n; r += 4) {
+        const auto want = host_levels(el, r);
+        auto seeded = [&](FrontierState& st, std::vector<vertex_t>& par) {
+          st = FrontierState(n);
+          par.assign(n, kNoVertex);
+          par[r] = r;
+          st.visited.set(r);
+          st.current.set(r);
+        };
+        FrontierState st;
+        std::vector<vertex_t> par;
+        // drivers: exact levels; the hybrid trace matches the persistent kernel's
+        for (int d = 0; d < 5; ++d) {
+          seeded(st, par);
+          KernelStats ks;
+          if (d == 0) run_top_down(g, st, par, n, &ks);
+          if (d == 1) run_hybrid(g, nullptr, BottomUpKind::kClassic, st, par, n, {}, &ks);
+          if (d == 2) run_hybrid(g, &sp, BottomUpKind::kDegreeAware, st, par, n, {}, &ks);
+          if (d == 3) run_hybrid(g, &sp, BottomUpKind::kBlockSearch, st, par, n, {}, &ks);
+          if (d == 4) run_block_search(g, sp, st, par, n, &ks);
+          BfsTree t;
+          t.root = r;
+          t.parent = par;
+          EXPECT(fixpoint_levels(t) == want);
+          EXPECT(ks.levels == ks.direction_trace.size());
+          if (d == 1) {
+            KernelStats ref;
+            bfs_hybrid(g, r, {}, &ref);
+            EXPECT(ks.direction_trace == ref.direction_trace);
+          }
+        }
+        // single steps: claims and the deterministic bottom-up parent rules
+        seeded(st, par);
+        const StepResult td = top_down_step(g, st, par, n);
+        uint64_t deg1 = 0, sc = 0;
+        for (vertex_t v = 0; v < n; ++v)
+          if (want[v] == 1) ++deg1, sc += g.degrees[v];
+        EXPECT(td.claimed == deg1 && td.scout == sc);
+        st.advance_level();
+        for (int kind = 0; kind < 3; ++kind) {
+          FrontierState s2 = st;
+          std::vector<vertex_t> p2 = par;
+          if (kind == 0) bottom_up_step(g, s2, p2, n);
+          if (kind == 1) degree_aware_step(g, sp, s2, p2, n);
+          if (kind == 2) block_search_step(g, sp, s2, p2, n);
+          for (vertex_t w = 0; w < n; ++w) {
+            if (st.visited.get(w)) {
+              EXPECT(p2[w] == par[w]);
+              continue;
+            }
+            std::vector<vertex_t> order;
+            if (kind == 0) {
+              order.assign(g.neighbors(w).begin(), g.neighbors(w).end());
+            } else {
+              if (sp.in_plus[w] != kNoVertex) order.push_back(sp.in_plus[w]);
+              order.insert(order.end(), sp.in_minus(w).begin(), sp.in_minus(w).end());
+            }
+            // classic / degree-aware probe the frontier, block search the
+            // pre-step visited set
+            const vertex_t want_p = first_in(order, kind == 2 ? st.visited : st.current);
+            EXPECT(p2[w] == want_p);
+            EXPECT(s2.next.get(w) == (want_p != kNoVertex));
+          }
+        }
+      }
+    }
+    const CsrGraph g = build_csr(path(4));
+    FrontierState bad(3);
+    std::vector<vertex_t> p(4, kNoVertex);
+    EXPECT(throws_with<std::invalid_argument>([&] { top_down_step(g, bad, p, 4); },
+                                              "frontier state does not match graph"));
+    FrontierState ok(4);
+    EXPECT(throws_with<std::invalid_argument>(
+        [&] { run_hybrid(g, nullptr, BottomUpKind::kDegreeAware, ok, p, 4, {}); },
+        "needs a degree split"));
+  });
+
   run_case("degree split, split kernels, checker side (preprocess/validate/bench.hpp)", [] {
     // star centre 0 with a 2-path hanging off leaf 3: degrees 0:4 3:2
     const CsrGraph g = build_csr(edges(6, {{0, 1}, {0, 2}, {0, 3}, {0, 4}, {3, 5}}));
