@@ -2,6 +2,7 @@
 #pragma once
 
 #include "etbfs/bfs.hpp"
+#include "etbfs/bitmap.hpp"
 #include "etbfs/preprocess.hpp"
 #include "etbfs/types.hpp"
 
@@ -19,6 +20,18 @@ enum class TreeReplay {
   kTeet,
   kTeolv,
 };
+
+// Tree replay over caller-held state (et_bfs.hpp:30-37), on the GPU: for every
+// entry whose guard is visited (teet: the tree's core edge vertex; teolv: the
+// entry's src, height-0 layouts) parent[dst] = src unless already set.
+void teet(const EdgeTreeList& etl, const Bitmap& visited, std::vector<vertex_t>& parent);
+void teolv(const EdgeTreeList& etl, const Bitmap& visited, std::vector<vertex_t>& parent);
+
+// The start-side walk (et_bfs.hpp:39-43): BFS inside the edge tree containing
+// start, parents oriented away from it; returns the tree's core edge vertex
+// (its parent set to the adjacent tree vertex) or kNoVertex for a pure tree.
+// O(tree size) host work here as in the product path's start patch.
+vertex_t traverse_return_core_edge(const ClassifiedGraph& cg, vertex_t start, BfsTree& tree);
 
 // The split-based kernels require a split matching the core block (as the
 // reference checks, et_bfs.cpp:69-78) but the device does not read it: its

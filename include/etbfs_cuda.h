@@ -260,6 +260,13 @@ int etb_steps_run(const etb_graph* g, int op, uint64_t limit, uint64_t* visited,
                   const uint64_t* minus_offsets, const uint64_t* minus_cols, double alpha,
                   double beta, uint64_t* stats, char* trace, uint64_t trace_cap);
 
+/* teet / teolv (et_bfs.hpp:30-37) on the current device: entry i sets
+ * parent[dst[i]] = src[i] if its guard (core_edge[i], or src[i] when leaves_only)
+ * is set in the visited words and parent[dst[i]] is ETB_NO_VERTEX. */
+int etb_tree_replay(int leaves_only, const uint64_t* src, const uint64_t* dst,
+                    const uint64_t* core_edge, uint64_t count, const uint64_t* visited_words,
+                    uint64_t words, uint64_t* parent, uint64_t n);
+
 /* ---- graph and parent-tree files (io.hpp:9-45, io.cpp:47-181) ------------- */
 /* Byte-identical to the reference's ETG1 / text graph and ETT1 tree files, with
  * its validation order and messages (runtime errors name the path and the byte

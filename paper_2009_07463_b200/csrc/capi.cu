@@ -451,6 +451,33 @@ int etb_steps_run(const etb_graph* g, int op, uint64_t limit, uint64_t* visited,
   });
 }
 
+int etb_tree_replay(int leaves_only, const uint64_t* src, const uint64_t* dst,
+                    const uint64_t* core_edge, uint64_t count, const uint64_t* visited_words,
+                    uint64_t words, uint64_t* parent, uint64_t n) {
+  return guarded([&] {
+    if (count) {
+      need(src, "etb_tree_replay");
+      need(dst, "etb_tree_replay");
+      need(core_edge, "etb_tree_replay");
+    }
+    if (n) need(parent, "etb_tree_replay");
+    if (words) need(visited_words, "etb_tree_replay");
+    for (uint64_t i = 0; i < count; ++i) {  // the host side validates the indices
+      const uint64_t guard = leaves_only ? src[i] : core_edge[i];
+      if (dst[i] >= n || (guard != ~uint64_t{0} && guard >= words * 64))
+        throw std::invalid_argument("teet: entry index out of range");
+    }
+    cudaStream_t s = nullptr;
+    ETB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamDel {
+      cudaStream_t s;
+      ~StreamDel() { cudaStreamDestroy(s); }
+    } del{s};
+    etb::tree_replay_run(leaves_only, src, dst, core_edge, count, visited_words, words, parent, n,
+                         s);
+  });
+}
+
 int etb_graph_download(const etb_graph* g, uint64_t* row, uint64_t* cols, uint64_t* degrees) {
   return guarded([&] {
     need(g, "etb_graph_download");

@@ -145,3 +145,60 @@ void run_block_search(const CsrGraph& graph, const DegreeSplitAdjacency& split,
 }
 
 }  // namespace etbfs
+
+// ---- tree replay and the start-side walk (et_bfs.hpp:30-43) -------------------
+#include "etbfs/et_bfs.hpp"
+
+namespace etbfs {
+namespace {
+
+void replay(int leaves_only, const EdgeTreeList& etl, const Bitmap& visited,
+            std::vector<vertex_t>& parent) {
+  const size_t m = etl.entries.size();
+  std::vector<uint64_t> src(m), dst(m), ce(m);
+  for (size_t i = 0; i < m; ++i) {
+    src[i] = etl.entries[i].src;
+    dst[i] = etl.entries[i].dst;
+    ce[i] = etl.entries[i].core_edge;
+  }
+  std::vector<uint64_t> words(visited.word_count());
+  for (uint64_t w = 0; w < words.size(); ++w) words[w] = visited.word(w);
+  check(etb_tree_replay(leaves_only, src.data(), dst.data(), ce.data(), m, words.data(),
+                        words.size(), parent.data(), parent.size()));
+}
+
+}  // namespace
+
+void teet(const EdgeTreeList& etl, const Bitmap& visited, std::vector<vertex_t>& parent) {
+  replay(0, etl, visited, parent);
+}
+
+void teolv(const EdgeTreeList& etl, const Bitmap& visited, std::vector<vertex_t>& parent) {
+  replay(1, etl, visited, parent);
+}
+
+vertex_t traverse_return_core_edge(const ClassifiedGraph& cg, vertex_t start, BfsTree& tree) {
+  if (start >= cg.graph.vertex_count ||
+      (cg.vertex_type[start] != VertexType::kTreeInternal &&
+       cg.vertex_type[start] != VertexType::kTreeLeaf))
+    throw std::invalid_argument("traverse_return_core_edge: start is not a tree vertex");
+  const uint64_t core = cg.core_vertex_count;
+  tree.parent[start] = start;
+  vertex_t core_edge = kNoVertex;
+  std::vector<vertex_t> frontier{start};
+  for (size_t head = 0; head < frontier.size(); ++head) {
+    const vertex_t u = frontier[head];
+    for (vertex_t w : cg.graph.neighbors(u)) {
+      if (w < core) {  // the tree's single attachment to the core
+        core_edge = w;
+        tree.parent[w] = u;
+      } else if (tree.parent[w] == kNoVertex) {
+        tree.parent[w] = u;
+        frontier.push_back(w);
+      }
+    }
+  }
+  return core_edge;
+}
+
+}  // namespace etbfs

@@ -111,4 +111,10 @@ void step_run(const DevGraph& g, int op, uint64_t limit, uint64_t* h_vis, uint64
               const uint64_t* h_moff, const uint64_t* h_minus, double alpha, double beta,
               uint64_t out[6], std::string* trace, cudaStream_t s);
 
+// steps.cu: teet / teolv (leaves_only) over a host edge tree list, visited
+// words and parents.
+void tree_replay_run(int leaves_only, const uint64_t* h_src, const uint64_t* h_dst,
+                     const uint64_t* h_ce, uint64_t count, const uint64_t* h_vis, uint64_t words,
+                     uint64_t* h_parent, uint64_t n, cudaStream_t s);
+
 }  // namespace etb

@@ -337,3 +337,47 @@ void step_run(const DevGraph& g, int op, uint64_t limit, uint64_t* h_vis, uint64
 }
 
 }  // namespace etb
+
+namespace etb {
+namespace {
+
+// teet / teolv (et_bfs.cpp:14-32): entry i writes parent[dst] = src when its
+// guard vertex (the tree's core edge vertex / the entry's src) is visited and
+// dst has no parent yet.
+__global__ void replay_kernel(int leaves_only, const uint64_t* src, const uint64_t* dst,
+                              const uint64_t* core_edge, uint64_t count,
+                              const unsigned long long* vis, uint64_t* parent) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t guard = leaves_only ? src[i] : core_edge[i];
+    if (guard == ~uint64_t{0}) continue;  // whole-component tree (TEET)
+    if (((vis[guard >> 6] >> (guard & 63)) & 1ull) && parent[dst[i]] == ~uint64_t{0})
+      parent[dst[i]] = src[i];
+  }
+}
+
+}  // namespace
+
+void tree_replay_run(int leaves_only, const uint64_t* h_src, const uint64_t* h_dst,
+                     const uint64_t* h_ce, uint64_t count, const uint64_t* h_vis, uint64_t words,
+                     uint64_t* h_parent, uint64_t n, cudaStream_t s) {
+  DevBuf<uint64_t> src(count ? count : 1), dst(count ? count : 1), ce(count ? count : 1),
+      parent(n ? n : 1);
+  DevBuf<unsigned long long> vis(words ? words : 1);
+  if (count) {
+    ETB_CUDA(cudaMemcpyAsync(src.get(), h_src, count * 8, cudaMemcpyHostToDevice, s));
+    ETB_CUDA(cudaMemcpyAsync(dst.get(), h_dst, count * 8, cudaMemcpyHostToDevice, s));
+    ETB_CUDA(cudaMemcpyAsync(ce.get(), h_ce, count * 8, cudaMemcpyHostToDevice, s));
+  }
+  if (words) ETB_CUDA(cudaMemcpyAsync(vis.get(), h_vis, words * 8, cudaMemcpyHostToDevice, s));
+  if (n) ETB_CUDA(cudaMemcpyAsync(parent.get(), h_parent, n * 8, cudaMemcpyHostToDevice, s));
+  if (count) {
+    replay_kernel<<<grid_for(count, 256), 256, 0, s>>>(leaves_only, src.get(), dst.get(),
+                                                       ce.get(), count, vis.get(), parent.get());
+    ETB_LAUNCH_CHECK();
+  }
+  if (n) ETB_CUDA(cudaMemcpyAsync(h_parent, parent.get(), n * 8, cudaMemcpyDeviceToHost, s));
+  ETB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace etb

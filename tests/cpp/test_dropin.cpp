@@ -192,6 +192,49 @@ vertex_t first_in(const std::vector<vertex_t>& order, const Bitmap& in) {
 }
 
 int main() {
+  run_case("et_bfs composed from the public pieces (et_bfs.cpp:59-124 restated)", [] {
+    for (const EdgeList& el : corpus()) {
+      const CsrGraph g = build_csr(el);
+      for (int64_t mh : {int64_t{-1}, int64_t{0}}) {
+        const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, mh), mh);
+        const EdgeTreeList etl = extract_edge_tree_list(cg);
+        const EdgeList rel = relabeled(cg);
+        const uint64_t n = cg.graph.vertex_count, core = cg.core_vertex_count;
+        for (vertex_t s = 0; s < n; ++s) {
+          BfsTree t;
+          t.root = s;
+          t.parent.assign(n, kNoVertex);
+          FrontierState st(n);
+          vertex_t cstart = s;
+          const VertexType ty = cg.vertex_type[s];
+          if (ty == VertexType::kTreeInternal || ty == VertexType::kTreeLeaf)
+            cstart = traverse_return_core_edge(cg, s, t);
+          else if (ty == VertexType::kVertexZero)
+            cstart = kNoVertex, t.parent[s] = s;
+          else
+            t.parent[s] = s;
+          if (cstart != kNoVertex && cstart < core) {
+            st.visited.set(cstart);
+            st.current.set(cstart);
+            run_hybrid(cg.graph, nullptr, BottomUpKind::kClassic, st, t.parent, core, {});
+          }
+          if (mh == 0) teolv(etl, st.visited, t.parent);
+          else teet(etl, st.visited, t.parent);
+          EXPECT(fixpoint_levels(t) == host_levels(rel, s));
+        }
+      }
+    }
+    EXPECT(throws_with<std::invalid_argument>(
+        [] {
+          const CsrGraph g = build_csr(path(3));
+          const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, 0), 0);
+          BfsTree t;
+          t.parent.assign(3, kNoVertex);
+          traverse_return_core_edge(cg, 0, t);
+        },
+        "start is not a tree vertex"));
+  });
+
   run_case("step and driver layer on the GPU (bfs.hpp:66-120)", [] {
     EXPECT(block_search_unvisited(0b1010) == (std::pair<std::uint32_t, std::uint64_t>{1, 0b1000}));
     for (const EdgeList& el : corpus()) {
