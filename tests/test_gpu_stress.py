@@ -1,0 +1,73 @@
+"""Shapes far from Kronecker, on the product kernel: a long cycle (tens of
+thousands of levels), a long path (all edge tree), a big star (one hub, every
+other vertex a leaf), a dense clique, a grid, and a mixture of components —
+depths checked against the CPU oracle, parents by the device validator."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2009_07463_b200 as eb
+from paper_2009_07463_b200 import etbfs as E
+
+pytestmark = pytest.mark.gpu
+NO = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def cycle(n):
+    v = np.arange(n, dtype=np.uint64)
+    return np.stack([v, (v + 1) % n], 1)
+
+
+def path(n):
+    v = np.arange(n - 1, dtype=np.uint64)
+    return np.stack([v, v + 1], 1)
+
+
+def star(n):
+    v = np.arange(1, n, dtype=np.uint64)
+    return np.stack([np.zeros_like(v), v], 1)
+
+
+def clique(k):
+    a, b = np.triu_indices(k, 1)
+    return np.stack([a, b], 1).astype(np.uint64)
+
+
+def grid(w, h):
+    idx = np.arange(w * h, dtype=np.uint64).reshape(h, w)
+    right = np.stack([idx[:, :-1].ravel(), idx[:, 1:].ravel()], 1)
+    down = np.stack([idx[:-1, :].ravel(), idx[1:, :].ravel()], 1)
+    return np.vstack([right, down])
+
+
+def mixture():
+    parts, off = [], 0
+    for e, n in ((cycle(500), 500), (path(300), 300), (star(200), 200), (clique(40), 40),
+                 (grid(30, 20), 600), (np.empty((0, 2), np.uint64), 50)):
+        parts.append(e + np.uint64(off))
+        off += n
+    return off, np.vstack(parts)
+
+
+CASES = [("cycle", 1 << 15, cycle(1 << 15)), ("path", 1 << 15, path(1 << 15)),
+         ("star", 1 << 18, star(1 << 18)), ("clique", 1500, clique(1500)),
+         ("grid", 300 * 200, grid(300, 200)), ("mixture",) + mixture()]
+
+
+@pytest.mark.parametrize("name,n,pairs", CASES, ids=[c[0] for c in CASES])
+def test_extreme_shapes(name, n, pairs):
+    g = eb.build_csr(n, pairs)
+    oc = O.OracleCsr(n, pairs)
+    rng = np.random.default_rng(11)
+    for mh in (-1, 0):
+        cg = eb.relayout_csr(g, mh=mh)
+        for root in [0, n - 1] + [int(x) for x in rng.integers(0, n, 3)]:
+            s = int(cg.old2new[root])
+            r = eb.et_bfs(cg, s, stats=True)
+            want = oc.levels(root)
+            got = np.full(n, NO, np.uint64)
+            ok = r.depth >= 0
+            got[np.asarray(cg.new2old, np.int64)[ok]] = r.depth[ok].astype(np.uint64)
+            assert np.array_equal(got, want), (name, mh, root)
+            E.bfs_device(cg, s)
+            assert E.result_validate(cg, s)["passed"], (name, mh, root)
