@@ -334,3 +334,32 @@ def test_split_kernels_corpus(corpus):
                 core_depth = max(int(x) for x, v in zip(lv, range(g["n"]))
                                  if x != O.NO_VERTEX and int(cg.old2new[v]) < cg.core_vertex_count)
                 assert len(tr) == core_depth + 1, (g["name"], st, tr)
+
+
+def test_bfs_compact_outputs(kron16):
+    """etb_bfs_compact (the e2e API) into pageable and pinned (registered) host
+    buffers equals that traversal's device result (parents can differ between
+    runs: top-down claims race)."""
+    from paper_2009_07463_b200 import etbfs as E
+    g = eb.generate_graph(scale=16, edgefactor=16, seed=1)
+    cg = eb.relayout_csr(g, mh=-1)
+    n = cg.vertex_count
+    L = E.lib()
+    for root in kron16["roots"][:4]:
+        s = int(cg.old2new[root])
+        for pinned in (False, True):
+            par = np.full(n, 7, np.uint32)
+            dep = np.full(n, 7, np.int32)
+            if pinned:
+                E._check(L.etb_host_register(par.ctypes.data, par.nbytes))
+                E._check(L.etb_host_register(dep.ctypes.data, dep.nbytes))
+            try:
+                E._check(L.etb_bfs_compact(cg.handle, s, None, dep.ctypes.data, par.ctypes.data))
+            finally:
+                if pinned:
+                    E._check(L.etb_host_unregister(par.ctypes.data))
+                    E._check(L.etb_host_unregister(dep.ctypes.data))
+            d2, p2 = result_download(cg)  # u32 parents, UINT32_MAX unreached
+            assert np.array_equal(par, p2), (root, pinned)
+            assert np.array_equal(dep, d2), (root, pinned)
+            assert E.result_validate(cg, s)["passed"], (root, pinned)
