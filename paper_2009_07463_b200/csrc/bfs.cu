@@ -593,6 +593,86 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     double etc = p.edges_to_check;
     bool bu = bu0, saw_bu = bu0;
     if (bu) awake = frontier;
+    bool list_from_prologue = false;
+    // ---- fused first level: when the start's core row fits one CTA, every CTA
+    // claims it redundantly (the claims are the whole row: nothing else is
+    // visited yet), sets the bits itself and builds the same level-1 list in
+    // place, so level 1 starts without level 0's chain and grid barrier. Only
+    // CTA 0 writes the results and stats.
+    const uint32_t d0 = static_cast<uint32_t>(ne);
+    // (Small-core kernel only: in the large-core instantiation the extra code
+    // costs more in register allocation elsewhere than the 3 us it saves.)
+    if (!kLarge && !bu && !p.bottom_up_only && d0 > 0 && d0 <= blockDim.x && d0 + 1 < p.nc) {
+      const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+      const uint64_t rs = p.crow[start];
+      uint32_t w = kNone32;
+      uint2 mt = make_uint2(0u, 0u);
+      // the start's bit too: CTA 0's thread 0 sets it without a barrier here
+      if (threadIdx.x == 0) atomicOr(&p.visited[start >> 5], 1u << (start & 31));
+      if (threadIdx.x < d0) {
+        w = p.ccol[rs + threadIdx.x];
+        mt = p.cmeta[w];
+        atomicOr(&p.visited[w >> 5], 1u << (w & 31));
+        if (blockIdx.x == 0)
+          p.dp[w] = make_uint2(static_cast<uint32_t>(p.base_depth + 1), start);
+      }
+      // block scans: list position and edge prefix of the neighbours with core edges
+      const uint32_t take = mt.x != 0;
+      const uint32_t cin = warp_incl_scan(take);
+      const unsigned long long ein = warp_incl_scan64(mt.x);
+      const unsigned long long sc = warp_sum(static_cast<unsigned long long>(mt.y));
+      if (lane == 31) {
+        sm.red[0][wib] = (static_cast<unsigned long long>(cin) << 40) | ein;
+        sm.red[1][wib] = sc;
+      }
+      __syncthreads();
+      unsigned long long cbase = 0, ebase = 0, ctot = 0, etot = 0, stot = 0;
+      for (unsigned k = 0; k < nwb; ++k) {
+        const unsigned long long r = sm.red[0][k];
+        if (k < wib) {
+          cbase += r >> 40;
+          ebase += r & ((1ull << 40) - 1);
+        }
+        ctot += r >> 40;
+        etot += r & ((1ull << 40) - 1);
+        stot += sm.red[1][k];
+      }
+      if (take) {
+        const uint64_t pos = cbase + cin - 1;
+        p.qv1[pos] = w;
+        p.qp1[pos] = ebase + ein - mt.x;
+      }
+      // the state after level 0
+      etc -= (double)scout;
+      frontier = d0;
+      scout = stot;
+      reached = 1 + d0;
+      nq = ctot;
+      ne = etot;
+      if (tid == 0) {
+        if (p.trace) p.trace[0] = 't';
+        if (p.level_claims) p.level_claims[0] = d0;
+      }
+      L = 1;
+      stamp(p, 258);
+      if (!p.top_down_only && (double)scout > etc / p.alpha) {
+        // a bottom-up level 1 probes the frontier bitmap: this CTA's own copy of it
+        bu = true;
+        saw_bu = true;
+        awake = frontier;
+        if (w != kNone32) atomicOr(&p.fb1[w >> 5], 1u << (w & 31));
+      }
+      list_from_prologue = true;
+      __syncthreads();  // this CTA's visited / frontier bits and list before level 1
+    }
+    if (list_from_prologue) {  // level 1 reads qv1 / qp1
+      uint32_t* tv = qv_in;
+      qv_in = qv_out;
+      qv_out = tv;
+      uint64_t* tp = qp_in;
+      qp_in = qp_out;
+      qp_out = tp;
+    }
     for (;;) {
       uint32_t* fcur = F[L % 3];
       uint32_t* fnext = F[(L + 1) % 3];
@@ -782,6 +862,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
       p.visited_next[i] = (i == p.nwords - 1 && tail) ? ~0u << tail : 0u;  // padding: visited
       p.fb0_next[i] = 0;
       p.fb1_next[i] = 0;
+      p.fb2_next[i] = 0;
     }
     if (tid < 32) p.ctr_next[tid] = 0;
   }
@@ -824,7 +905,7 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   S.visited.alloc(2 * words);
   S.fb0.alloc(2 * words);
   S.fb1.alloc(2 * words);
-  S.fb2.alloc(words);
+  S.fb2.alloc(2 * words);
   const uint64_t cap = L.nc + 2;
   S.qv0.alloc(cap);
   S.qv1.alloc(cap);
@@ -835,7 +916,7 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   ETB_CUDA(cudaMemsetAsync(S.visited.get(), 0, 2 * words * 4, s));
   ETB_CUDA(cudaMemsetAsync(S.fb0.get(), 0, 2 * words * 4, s));
   ETB_CUDA(cudaMemsetAsync(S.fb1.get(), 0, 2 * words * 4, s));
-  ETB_CUDA(cudaMemsetAsync(S.fb2.get(), 0, words * 4, s));
+  ETB_CUDA(cudaMemsetAsync(S.fb2.get(), 0, 2 * words * 4, s));
   ETB_CUDA(cudaMemsetAsync(S.ctr.get(), 0, 64 * 8, s));
   if (const uint32_t tail = static_cast<uint32_t>(L.nc & 31u)) {
     const uint32_t pad = ~0u << tail;
@@ -887,10 +968,11 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.visited = S.visited.get() + cur;
   p.fb0 = S.fb0.get() + cur;
   p.fb1 = S.fb1.get() + cur;
-  p.fb2 = S.fb2.get();
+  p.fb2 = S.fb2.get() + cur;
   p.visited_next = S.visited.get() + nxt;
   p.fb0_next = S.fb0.get() + nxt;
   p.fb1_next = S.fb1.get() + nxt;
+  p.fb2_next = S.fb2.get() + nxt;
   p.qv0 = S.qv0.get();
   p.qv1 = S.qv1.get();
   p.qp0 = S.qp0.get();

@@ -41,6 +41,7 @@ struct BfsParams {
   uint32_t* visited_next;
   uint32_t* fb0_next;
   uint32_t* fb1_next;
+  uint32_t* fb2_next;
   unsigned long long* ctr_next;
   // outputs (relaid ids, all n vertices)
   uint2* dp;  // {depth (i32 bits, -1 unreached), parent (kNone32 unreached)} per vertex
