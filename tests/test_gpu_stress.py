@@ -49,7 +49,21 @@ def mixture():
     return off, np.vstack(parts)
 
 
-CASES = [("cycle", 1 << 15, cycle(1 << 15)), ("path", 1 << 15, path(1 << 15)),
+def long_miss():
+    """A bottom-up level where a vertex with > 1024 core neighbours misses on its
+    first (highest-degree) neighbour and scans its row with the whole warp:
+    R - N_i (1500, in a ring), H - every N_i, H - Z, Z - Y_0..Y_9 (a ring)."""
+    k, y = 1500, 10
+    R, H, Z = 0, 1, 2
+    N = np.arange(3, 3 + k, dtype=np.uint64)
+    Y = np.arange(3 + k, 3 + k + y, dtype=np.uint64)
+    e = [np.stack([np.full(k, R, np.uint64), N], 1), np.stack([N, np.roll(N, 1)], 1),
+         np.stack([np.full(k, H, np.uint64), N], 1), np.array([[H, Z]], np.uint64),
+         np.stack([np.full(y, Z, np.uint64), Y], 1), np.stack([Y, np.roll(Y, 1)], 1)]
+    return 3 + k + y, np.vstack(e)
+
+
+CASES = [("longmiss",) + long_miss(), ("cycle", 1 << 15, cycle(1 << 15)), ("path", 1 << 15, path(1 << 15)),
          ("star", 1 << 18, star(1 << 18)), ("clique", 1500, clique(1500)),
          ("grid", 300 * 200, grid(300, 200)), ("mixture",) + mixture()]
 
