@@ -229,6 +229,14 @@ int etb_result_validate(etb_layout* L, uint64_t start, uint64_t* counts);
  * out[level * grid + cta] (cap entries). */
 int etb_debug_block_stamps(etb_layout* L, uint64_t start, uint64_t* out, uint64_t cap,
                            uint32_t* grid, uint32_t* levels);
+/* Diagnostics (libraries built with -DETB_WARP_STAMPS; zeros otherwise): for
+ * the top-down level that claims depth `depth`, per warp (8 entries, physical
+ * warp order): [0] ns since kernel entry at the warp's first chunk, clock64
+ * cycles from then to [1] its list position known, [2] columns loaded, [3]
+ * visited words loaded, [4] claim atomics returned, [5] chunk done; [6] chunk
+ * index, [7] 1 if the chunk lies in one row. */
+int etb_debug_warp_stamps(etb_layout* L, uint64_t start, int32_t depth, uint64_t* out,
+                          uint64_t cap, uint32_t* nwarps);
 /* Diagnostics: the raw globaltimer stamps of the last stats run ([0] entry, [1]
  * init end, [2 + L] level L end, [128 + L] conversion before level L end,
  * [255] replay end) and, at [192 + L], top-down level L's frontier edge count. */

@@ -175,19 +175,32 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
                         int32_t dnext, unsigned long long& scout_acc,
                         unsigned long long& claims_acc, uint32_t root) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const uint64_t gw = (uint64_t)wib * gridDim.x + blockIdx.x;  // CTA-minor: spread over SMs
   const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   const uint64_t nu = (ne + kTdChunk - 1) / kTdChunk;
   for (uint64_t g0 = gw, gn = 1; g0 < nu;) {
     const uint64_t g1 = min(nu, g0 + gn);
     // root != kNone32: the first level, whose list is the start alone (not stored)
+#ifdef ETB_WARP_STAMPS
+    const bool rec = p.wstamp && dnext == p.wdepth && g0 == gw;
+    unsigned long long* ws = p.wstamp + 8 * ((uint64_t)blockIdx.x * (blockDim.x >> 5) + wib);
+    const long long c0 = clock64();
+    if (rec && lane == 0) ws[0] = gtimer();
+#endif
     uint64_t i = root != kNone32 ? 0 : find_vertex(qp, nq, g0 * kTdChunk);
     for (uint64_t c = g0; c < g1; ++c) {
       const uint64_t e0 = c * kTdChunk, e1 = min(ne, e0 + kTdChunk);
       const uint64_t qi = root != kNone32 ? 0 : qp[i];
       const uint64_t iend = root != kNone32 ? ne : (i + 1 < nq ? qp[i + 1] : ne);
       const bool single = iend >= e1;
+#ifdef ETB_WARP_STAMPS
+      if (rec && c == g0 && lane == 0) {
+        ws[1] = clock_after(static_cast<uint32_t>(qi ^ iend)) - c0;
+        ws[6] = c;
+        ws[7] = single;
+      }
+#endif
       uint64_t inext;
       if (!single) {
         for (uint32_t k = lane; k < kTdChunk; k += 32) {
@@ -239,6 +252,9 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
       // With a list to emit (small frontiers) every target's {core, full}
       // degree is fetched with its visited word, off the claim's critical path;
       // without one only the claimed targets' full degree is read.
+#ifdef ETB_WARP_STAMPS
+      if (rec && c == g0 && lane == 0) ws[2] = clock_after(w[0] ^ w[1] ^ w[2] ^ w[3]) - c0;
+#endif
       constexpr bool kEmit = kMode == 1 || kMode == 2, kPre = kMode == 2;
       uint2 mt[kPre ? kEpl : 1];
 #pragma unroll
@@ -252,6 +268,12 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
         cl[j] = false;
         if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
       }
+#ifdef ETB_WARP_STAMPS
+      if (rec && c == g0 && lane == 0) {
+        ws[3] = clock_after(vw[0] ^ vw[1] ^ vw[2] ^ vw[3]) - c0;
+        ws[4] = clock_after(cl[0] | cl[1] | cl[2] | cl[3]) - c0;
+      }
+#endif
       uint32_t dg[kEpl];
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
@@ -284,6 +306,9 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
         flush_claims<kPre>(p, cbuf, win, ncl, qv_out, qp_out, slot);
       }
       __syncwarp();
+#ifdef ETB_WARP_STAMPS
+      if (rec && c == g0 && lane == 0) ws[5] = clock64() - c0;
+#endif
       i = inext;
     }
     if (nu <= nw) break;
@@ -487,7 +512,7 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
 __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t* qv_out,
                              uint64_t* qp_out, unsigned long long* cslot) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const uint64_t gw = (uint64_t)wib * gridDim.x + blockIdx.x;  // CTA-minor: spread over SMs
   const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
   for (uint64_t w0 = gw * 32; w0 < p.nwords; w0 += nw * 32) {
     const uint64_t wi = w0 + lane;
@@ -990,6 +1015,8 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.trace = nullptr;
   p.level_claims = nullptr;
   p.bstamp = nullptr;
+  p.wstamp = nullptr;
+  p.wdepth = -1;
   p.nlevels = nullptr;
 }
 

@@ -64,6 +64,8 @@ struct BfsParams {
   char* trace;
   unsigned long long* level_claims;
   unsigned long long* bstamp;  // diagnostics: [level][block] step-end globaltimer, or null
+  unsigned long long* wstamp;  // diagnostics (ETB_WARP_STAMPS builds): per-warp chunk phases
+  int32_t wdepth;              //   of the top-down level claiming this depth
   uint32_t* nlevels;
 };
 

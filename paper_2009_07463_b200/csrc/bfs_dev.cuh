@@ -44,6 +44,13 @@ inline __device__ void grid_sync(unsigned long long* bar) {
   __syncthreads();
 }
 
+// clock64 read that waits for x (diagnostics: phase boundaries after a load)
+__device__ __forceinline__ long long clock_after(uint32_t x) {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : "r"(x));
+  return t;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -118,7 +118,8 @@ void finish_layout(etb_layout* h) {
 
 etb::BfsParams run_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* o,
                        bool want_stats, cudaEvent_t pre_launch = nullptr,
-                       unsigned long long* bstamp = nullptr) {
+                       unsigned long long* bstamp = nullptr,
+                       unsigned long long* wstamp = nullptr, int32_t wdepth = -1) {
   const etb::DevLayout& L = h->L;
   if (start >= L.n) throw std::invalid_argument("et_bfs: start out of range");
   etb_bfs_options opt{ETB_KERNEL_HYBRID, ETB_REPLAY_TEET, 14.0, 24.0};
@@ -147,6 +148,8 @@ etb::BfsParams run_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* o,
     ETB_CUDA(cudaMemsetAsync(p.trace, 0, 256, h->stream));
   }
   p.bstamp = bstamp;
+  p.wstamp = wstamp;
+  p.wdepth = wdepth;
   if (pre_launch) ETB_CUDA(cudaEventRecord(pre_launch, h->stream));
   if (h->P) {
     etb::PartParams pp{};
@@ -750,6 +753,29 @@ int etb_debug_block_stamps(etb_layout* h, uint64_t start, uint64_t* out, uint64_
     for (uint64_t i = 0; i < std::min<uint64_t>(cap, 64 * g); ++i) out[i] = hs[i] ? hs[i] - t0 : 0;
     if (grid) *grid = static_cast<uint32_t>(g);
     if (levels) *levels = nl;
+  });
+}
+
+int etb_debug_warp_stamps(etb_layout* h, uint64_t start, int32_t depth, uint64_t* out,
+                          uint64_t cap, uint32_t* nwarps) {
+  return guarded([&] {
+    need(h, "etb_debug_warp_stamps");
+    if (h->P) throw std::invalid_argument("etb_debug_warp_stamps: single-partition kernel only");
+    ETB_CUDA(cudaSetDevice(h->device));
+    const uint64_t nw = static_cast<uint64_t>(h->S.grid) * (h->S.block / 32);
+    etb::DevBuf<unsigned long long> st(8 * nw);
+    ETB_CUDA(cudaMemsetAsync(st.get(), 0, 8 * nw * 8, h->stream));
+    run_bfs(h, start, nullptr, true, nullptr, nullptr, st.get(), depth);
+    uint64_t t0 = 0;
+    ETB_CUDA(cudaMemcpyAsync(&t0, h->S.level_claims.get() + 256, 8, cudaMemcpyDeviceToHost,
+                             h->stream));
+    std::vector<uint64_t> hs(8 * nw);
+    ETB_CUDA(cudaMemcpyAsync(hs.data(), st.get(), 8 * nw * 8, cudaMemcpyDeviceToHost, h->stream));
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
+    for (uint64_t w = 0; w < nw; ++w)
+      if (hs[8 * w]) hs[8 * w] -= t0;
+    std::copy(hs.begin(), hs.begin() + std::min<uint64_t>(cap, 8 * nw), out);
+    if (nwarps) *nwarps = static_cast<uint32_t>(nw);
   });
 }
 

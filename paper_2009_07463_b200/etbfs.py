@@ -167,6 +167,7 @@ def lib() -> C.CDLL:
     sig("etb_debug_phase_stamps", vp, vp)
     sig("etb_debug_launch_floor", vp, i32, C.POINTER(C.c_double))
     sig("etb_debug_block_stamps", vp, u64, vp, u64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32))
+    sig("etb_debug_warp_stamps", vp, u64, C.c_int32, vp, u64, C.POINTER(C.c_uint32))
     sig("etb_layout_partition", vp, C.c_uint32)
     sig("etb_layout_partition_bounds", vp, C.c_uint32, vp)
     sig("etb_mp_blob_size")

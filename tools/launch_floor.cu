@@ -64,6 +64,32 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     printf("back-to-back coop=%d: %.2f us per launch\n", coop, ms * 1e3f / 20);
   }
+  // after a 2xL2 memset (the bench's flush), as in the per-root sequence
+  void* flush = nullptr;
+  const size_t fb = 256ull << 20;
+  cudaMalloc(&flush, fb);
+  for (int coop = 0; coop < 2; ++coop)
+    for (int sm : {0, 48 * 1024, 100 * 1024}) {
+      std::vector<float> t;
+      for (int i = 0; i < 40; ++i) {
+        cudaMemsetAsync(flush, i & 0xff, fb, s);
+        cudaEventRecord(a, s);
+        int* sink = nullptr;
+        void* args[] = {&sink};
+        if (coop)
+          cudaLaunchCooperativeKernel((void*)empty_k, dim3(sms), dim3(768), args, sm, s);
+        else
+          empty_k<<<sms, 768, sm, s>>>(sink);
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (i >= 8) t.push_back(ms * 1e3f);
+      }
+      std::sort(t.begin(), t.end());
+      printf("after memset coop=%d block=768 smem=%6d median=%.2f us min=%.2f\n", coop, sm,
+             t[t.size() / 2], t[0]);
+    }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
