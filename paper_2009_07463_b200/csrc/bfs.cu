@@ -164,8 +164,8 @@ __device__ __forceinline__ uint32_t win_search(const int32_t* win, int32_t rel) 
 // Top-down step (bfs.cpp:61-86). Each lane owns 4 edges of the warp's chunk;
 // their column loads, visited probes and claim atomics are issued before any
 // result is consumed.
-// kMode: 0 no list, 3 no list and no scout (summed after the level by
-// scout_pass), 1 list (flush reads the degrees), 2 list with every
+// kMode: 0 no list, 3 no list and no claim atomics returning (claims and scout
+// counted after the level by scout_pass), 1 list (flush reads the degrees), 2 list with every
 // target's degrees fetched alongside its visited word (early levels, where most
 // targets are unvisited; after bottom-up most are visited and mode 1 is used).
 template <int kMode>
@@ -259,14 +259,35 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
       uint2 mt[kPre ? kEpl : 1];
 #pragma unroll
       for (int j = 0; j < kEpl; ++j) {
-        vw[j] = w[j] != kNone32 ? p.visited[w[j] >> 5] : ~0u;
+        // (mode 3 has no atomic return to fall back on: its probe reads L2, the
+        // point of coherence, so an earlier level's claim is never missed)
+        vw[j] = w[j] == kNone32 ? ~0u
+                                : (kMode == 3 ? __ldcg(&p.visited[w[j] >> 5]) : p.visited[w[j] >> 5]);
         if (kPre) mt[j] = w[j] != kNone32 ? p.cmeta[w[j]] : make_uint2(0u, 0u);
       }
+      if (kMode == 3) {
+        // Atomic-free claims: every edge to a target that is unvisited at its
+        // probe sets the target's visited and next-frontier bits (reductions,
+        // no return) and writes its depth and parent; racing writers of one
+        // target store the same depth and each a valid frontier parent. The
+        // claims and scout are counted from the new frontier bitmap afterwards.
 #pragma unroll
-      for (int j = 0; j < kEpl; ++j) {
-        const uint32_t bit = 1u << (w[j] & 31);
-        cl[j] = false;
-        if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
+        for (int j = 0; j < kEpl; ++j) {
+          const uint32_t bit = 1u << (w[j] & 31);
+          cl[j] = false;
+          if (!(vw[j] & bit)) {
+            atomicOr(&p.visited[w[j] >> 5], bit);
+            atomicOr(&fnext[w[j] >> 5], bit);
+            p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u[j]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kEpl; ++j) {
+          const uint32_t bit = 1u << (w[j] & 31);
+          cl[j] = false;
+          if (!(vw[j] & bit)) cl[j] = !(atomicOr(&p.visited[w[j] >> 5], bit) & bit);
+        }
       }
 #ifdef ETB_WARP_STAMPS
       if (rec && c == g0 && lane == 0) {
@@ -281,9 +302,7 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
         if (cl[j]) {
           p.dp[w[j]] = make_uint2(static_cast<uint32_t>(dnext), u[j]);
           atomicOr(&fnext[w[j] >> 5], 1u << (w[j] & 31));
-          // mode 3 (huge levels): the scout is summed after the level from the
-          // new frontier bitmap, a streaming pass (scout_pass)
-          dg[j] = kPre ? mt[j].y : (kMode == 3 ? 0u : p.degn[w[j]]);
+          dg[j] = kPre ? mt[j].y : p.degn[w[j]];
         }
       }
       uint32_t ncl = 0;
@@ -549,26 +568,29 @@ __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t*
   }
 }
 
-// Σ full degree over the frontier bitmap f: a warp takes 4 words per
-// iteration, lane = vertex, coalesced degree loads. For levels that claim a
-// large share of the core this streams the degree array instead of one random
-// 32-byte sector per claim.
-__device__ unsigned long long scout_pass(const BfsParams& p, const uint32_t* f) {
+// The claims (popcount) and scout (Σ full degree) of a top-down level from its
+// new frontier bitmap f: a warp takes 4 words per iteration, lane = vertex,
+// coalesced degree loads — a streaming pass instead of one random 32-byte
+// sector per claim, and the level's claims need no atomic return (td_step<3>).
+__device__ unsigned long long scout_pass(const BfsParams& p, const uint32_t* f,
+                                         unsigned long long& claims) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long s = 0;
+  unsigned long long s = 0, c = 0;
   for (uint64_t w0 = gw * 4; w0 < p.nwords; w0 += nw * 4) {
     uint32_t d[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint64_t wi = w0 + k;
-      const uint32_t bits = wi < p.nwords ? f[wi] : 0u;
+      const uint32_t bits = wi < p.nwords ? __ldcg(&f[wi]) : 0u;
+      c += (bits >> lane) & 1u;
       d[k] = ((bits >> lane) & 1u) ? p.degn[wi * 32 + lane] : 0u;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) s += d[k];
   }
+  claims += c;
   return s;
 }
 
@@ -742,9 +764,11 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         uint32_t* cb = sm.w[threadIdx.x >> 5].cbuf;
         int32_t* wn = sm.w[threadIdx.x >> 5].win;
         const uint32_t root = L == 0 ? start : kNone32;
-        // a frontier with more edges than the core has vertices claims a large share of
-        // it: its scout is summed afterwards by a streaming pass (mode 3)
-        defer_scout = kLarge && !emit && (double)scout > (double)p.nc;
+        // Large-core kernel: a list-less level claims without atomic returns; its
+        // claims and scout are counted afterwards by a streaming pass over the
+        // new frontier (mode 3). (Measured: s26 -5 us per root; on the
+        // small-core kernel the extra pass and barrier cost more than they save.)
+        defer_scout = kLarge && !emit;
         if (kLarge && defer_scout)
           td_step<3>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
                      scout_acc, claims_acc, root);
@@ -761,8 +785,15 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
       if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
       grid_sync_add(p.bar, sm, claims_acc, &slot[3], scout_acc, bu ? nullptr : &slot[1], slot, 4);
       const unsigned long long packed = sm.tot[0];
-      const unsigned long long scout_tot = sm.tot[1];
-      const unsigned long long claims = sm.tot[3];
+      unsigned long long scout_tot = sm.tot[1];
+      unsigned long long claims = sm.tot[3];
+      if (defer_scout) {  // td_step<3>: claims and scout from the new frontier bitmap
+        unsigned long long pc = 0;
+        const unsigned long long ds = scout_pass(p, fnext, pc);
+        grid_sync_add(p.bar, sm, pc, &slot[3], ds, &slot[1], slot, 4);
+        scout_tot = sm.tot[1];
+        claims = sm.tot[3];
+      }
       reached += claims;
       if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = claims;
       ++L;
@@ -785,11 +816,6 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
       } else {
         frontier = claims;
         scout = scout_tot;
-        if (kLarge && defer_scout && claims) {  // this level deferred its scout
-          const unsigned long long ds = scout_pass(p, F[L % 3]);
-          grid_sync_add(p.bar, sm, ds, &slot[1], 0, nullptr, slot, 4);
-          scout = sm.tot[1];
-        }
         nq = packed >> kItemShift;
         ne = packed & kItemMask;
         uint32_t* tv = qv_in;
@@ -1063,13 +1089,11 @@ void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParam
     const uint32_t s0 = static_cast<uint32_t>(start);
     anc[s0 - lo] = 1;
     par[s0 - lo] = s0;
-    for (uint32_t x = s0, prevx = s0; x != r;) {
+    for (uint32_t x = s0; x != r;) {
       const uint32_t up = src[x - nc];
       anc[up - lo] = 1;
       par[up - lo] = x;
-      prevx = x;
       x = up;
-      (void)prevx;
     }
     const uint32_t ds = dep[s0 - nc];
     for (uint32_t x = lo; x < hi; ++x) {
