@@ -341,7 +341,8 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
   }
 }
 
-__device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcur, uint64_t rb,
+template <class P>
+__device__ __forceinline__ bool scan_row(const P& p, const uint32_t* fcur, uint64_t rb,
                                          uint64_t re, uint32_t& par) {
   // The first (highest-degree) neighbour was already probed; the rest of the
   // row [rb, re) is probed four at a time (independent loads) with early exit.
@@ -372,6 +373,10 @@ __device__ __forceinline__ bool scan_row(const BfsParams& p, const uint32_t* fcu
 // whole warp per vertex for longer rows.
 constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (the claim buffer + the window)
 constexpr uint32_t kLaneScan = 1024;
+// bu_sweep on the large-core kernel once fewer than nc / kSweepT vertices are
+// unvisited (measured at s26: 2 best, -5 us per root; inlined — out of line its
+// call cost the rest of the kernel 3%)
+constexpr double kSweepT = 2.0;
 
 // Bottom-up list emission (a level predicted to hand over to top-down): the
 // warp appends its claims, up to K per lane, to the next frontier list with one
@@ -405,7 +410,8 @@ __device__ __forceinline__ void bu_append(const uint32_t (&v)[K], const uint32_t
   }
 }
 
-__device__ void resolve_misses(const BfsParams& p, const uint32_t* fcur, uint32_t* fnext,
+template <class P>
+__device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext,
                                uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
                                unsigned long long& claims_acc, uint32_t* qv_out,
                                uint64_t* qp_out, unsigned long long* lslot) {
@@ -521,6 +527,72 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
     if (nmiss > kMissCap - 32 * kBuU) {
       resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
       nmiss = 0;
+    }
+  }
+  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
+}
+
+template <int kSweep, class P>
+__device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint32_t* fcur,
+                        uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
+                        uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot) {
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1;
+  uint32_t nmiss = 0;
+  // A warp sweeps kSweep visited words with one coalesced load (lane = word)
+  // and works through the words with unvisited vertices kBuU at a time, so
+  // late levels (few unvisited left) skip full words without a round trip each.
+  for (uint64_t b0 = gw * kSweep; b0 < p.nwords; b0 += nw * kSweep) {
+    const uint32_t mine = lane < kSweep && b0 + lane < p.nwords ? p.visited[b0 + lane] : ~0u;
+    unsigned todo = __ballot_sync(0xffffffffu, mine != ~0u);
+    while (todo) {
+      uint32_t vis[kBuU], wi[kBuU];
+#pragma unroll
+      for (int k = 0; k < kBuU; ++k) {
+        const int j = todo ? __ffs(todo) - 1 : 0;
+        vis[k] = todo ? __shfl_sync(0xffffffffu, mine, j) : ~0u;
+        wi[k] = static_cast<uint32_t>(b0) + j;
+        todo &= todo - 1;
+      }
+      uint32_t f[kBuU];
+#pragma unroll
+      for (int k = 0; k < kBuU; ++k)
+        f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[(uint64_t)wi[k] * 32 + lane];
+      bool hit[kBuU];
+#pragma unroll
+      for (int k = 0; k < kBuU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
+#pragma unroll
+      for (int k = 0; k < kBuU; ++k) {
+        const uint32_t v = wi[k] * 32 + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
+        if (hit[k]) {
+          p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), f[k]);
+        }
+        if (lane == 0 && m) {
+          p.visited[wi[k]] = vis[k] | m;
+          fnext[wi[k]] = m;
+          claims_acc += __popc(m);
+        }
+        const bool miss = f[k] != kNone32 && !hit[k];
+        const unsigned mm = __ballot_sync(0xffffffffu, miss);
+        if (miss) mbuf[nmiss + __popc(mm & lt)] = v;
+        nmiss += __popc(mm);
+      }
+      if (lslot) {
+        uint32_t av[kBuU], ad[kBuU];
+#pragma unroll
+        for (int k = 0; k < kBuU; ++k) {
+          av[k] = wi[k] * 32 + lane;
+          ad[k] = hit[k] ? p.cmeta[av[k]].x : 0u;
+        }
+        bu_append<kBuU>(av, ad, qv_out, qp_out, lslot);
+      }
+      if (nmiss > kMissCap - 32 * kBuU) {
+        resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
+        nmiss = 0;
+      }
     }
   }
   if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
@@ -750,8 +822,15 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         // list-counter atomics, was slower overall at scales 22 and 26.)
         bu_list = !p.bottom_up_only && !p.top_down_only &&
                   (double)(p.nc - reached) <= (double)p.nc / p.beta;
-        bu_step(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in, qp_in,
-                bu_list ? &slot[0] : nullptr);
+        // Large-core kernel, levels with few unvisited vertices left: the
+        // coalesced sweep that skips fully visited words (bu_sweep; on the
+        // small-core kernel it measured slower at every level kind)
+        if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
+          bu_sweep<32>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in,
+                       qp_in, bu_list ? &slot[0] : nullptr);
+        else
+          bu_step(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in, qp_in,
+                  bu_list ? &slot[0] : nullptr);
       } else {
         etc -= (double)scout;
         // The next frontier list is emitted only when this frontier's edge count
