@@ -367,12 +367,17 @@ __device__ __forceinline__ bool scan_row(const P& p, const uint32_t* fcur, uint6
 // per iteration, lane = one vertex of each; all first-neighbour probes of the
 // kBuU words are in flight together and each word is written back once.
 // Vertices whose first (highest-degree) neighbour is not in the frontier are
-// deferred to a per-warp smem list and scanned afterwards, one lane per vertex
-// (rows of <= kLaneScan core neighbours: measured best from 512 up, 64 cost 4%
-// at s22 and 2% at s26 — early exit usually comes within a few probes) or the
-// whole warp per vertex for longer rows.
+// deferred to a per-warp smem list and scanned afterwards: one lane per vertex
+// over the next kLaneFirst neighbours (early exit usually comes within a few
+// probes), then the whole warp per vertex for the rest of a row that has not
+// hit yet (so one long miss no longer holds a lane for hundreds of round
+// trips; measured against lane-only scans up to 1024 neighbours: -0.5 us per
+// root at s22, -2 us at s26).
 constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (the claim buffer + the window)
-constexpr uint32_t kLaneScan = 1024;
+#ifndef ETB_LANE_FIRST
+#define ETB_LANE_FIRST 64
+#endif
+constexpr uint32_t kLaneFirst = ETB_LANE_FIRST;
 // bu_sweep on the large-core kernel once fewer than nc / kSweepT vertices are
 // unvisited (measured at s26: 2 best, -5 us per root; inlined — out of line its
 // call cost the rest of the kernel 3%)
@@ -427,8 +432,9 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
       // the row bounds give the degree too: one round trip before the scan
       const uint64_t rb = p.crow[v], re = p.crow[v + 1];
       cd = static_cast<uint32_t>(re - rb);
-      if (cd > kLaneScan) lng = true;
-      else hit = scan_row(p, fcur, rb, re, par);
+      const uint64_t lend = min(re, rb + 1 + kLaneFirst);
+      hit = scan_row(p, fcur, rb, lend, par);
+      lng = !hit && lend < re;
     }
     if (hit) {
       p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
@@ -449,7 +455,7 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
   }
   for (uint32_t i = 0; i < nlong; ++i) {
     const uint32_t v = mbuf[i];
-    const uint64_t rb = p.crow[v] + 1, re = p.crow[v + 1];
+    const uint64_t rb = p.crow[v] + 1 + kLaneFirst, re = p.crow[v + 1];
     uint32_t par = kNone32;
     for (uint64_t e0 = rb; e0 < re; e0 += 32) {
       const uint64_t e = e0 + lane;

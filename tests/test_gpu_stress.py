@@ -85,3 +85,33 @@ def test_extreme_shapes(name, n, pairs):
             assert np.array_equal(got, want), (name, mh, root)
             E.bfs_device(cg, s)
             assert E.result_validate(cg, s)["passed"], (name, mh, root)
+
+
+def warp_scan_graph():
+    """H's core row holds 100 higher-degree neighbours (a clique D) before its
+    only frontier neighbour F, so a bottom-up level scans past the lane-scan
+    prefix into the warp scan: R - F - G triangle, H - F, H - D_i, D a clique."""
+    R, F, G, H = 0, 1, 2, 3
+    D = np.arange(4, 104, dtype=np.uint64)
+    a, b = np.triu_indices(len(D), 1)
+    e = [np.array([[R, F], [F, G], [G, R], [H, F]], np.uint64),
+         np.stack([np.full(len(D), H, np.uint64), D], 1), np.stack([D[a], D[b]], 1)]
+    return 104, np.vstack(e)
+
+
+def test_bottom_up_warp_scan():
+    n, pairs = warp_scan_graph()
+    g = eb.build_csr(n, pairs)
+    oc = O.OracleCsr(n, pairs)
+    cg = eb.relayout_csr(g, mh=-1)
+    for root in (0, 1, 3, 50):
+        s = int(cg.old2new[root])
+        for kw in ({"policy": eb.HybridPolicy(alpha=1e18)},
+                   {"kernel": eb.CoreKernel.BLOCK_SEARCH}):
+            r = eb.et_bfs(cg, s, stats=True, **kw)
+            got = np.full(n, NO, np.uint64)
+            ok = r.depth >= 0
+            got[np.asarray(cg.new2old, np.int64)[ok]] = r.depth[ok].astype(np.uint64)
+            assert np.array_equal(got, oc.levels(root)), (root, kw)
+            assert "b" in r.stats.direction_trace
+
