@@ -48,7 +48,7 @@ constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down chunk
 constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex ids)
 constexpr int kBuU = 8;              // visited words per warp per bottom-up iteration
-constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab on long levels
+constexpr uint64_t kGrab = 4;      // top-down chunks per warp per grab on long levels
 
 struct WarpSmem {
   uint32_t cbuf[kCbuf];     // staged claims (top-down); with win: deferred misses (bottom-up)
@@ -168,7 +168,7 @@ __device__ __forceinline__ uint32_t win_search(const int32_t* win, int32_t rel) 
 // counted after the level by scout_pass), 1 list (flush reads the degrees), 2 list with every
 // target's degrees fetched alongside its visited word (early levels, where most
 // targets are unvisited; after bottom-up most are visited and mode 1 is used).
-template <int kMode>
+template <int kMode, bool kLarge>
 __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const uint32_t* qv,
                         const uint64_t* qp, uint64_t nq, uint64_t ne, uint32_t* qv_out,
                         uint64_t* qp_out, uint32_t* fnext, unsigned long long* slot,
@@ -334,7 +334,15 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
     unsigned long long next = 0;
     // single chunks when the level is only a few chunks per warp (balance),
     // batches when it is long (fewer atomics on the shared counter)
-    const uint64_t want = nu <= 8 * nw ? 1 : kGrab;
+    // Large-core kernel: guided grabs, 4..16 chunks shrinking with the chunks
+    // left (estimated from this warp's last grab). On the s26 levels with
+    // ~10^6 chunks the per-level counter is one L2 address: grabs of 4 kept it
+    // saturated (one atomic per ~1.7 ns), grabs of 2 cost +20%, static ranges
+    // +15% (imbalance); guided 4..16 measured -10% per root (538 -> 485 us).
+    const uint64_t rem = nu - min(nu, g1);
+    const uint64_t want = nu <= 8 * nw ? 1
+                          : kLarge ? max(kGrab, min(uint64_t{16}, rem / (4 * nw)))
+                                   : kGrab;
     if (lane == 0) next = nw + atomicAdd(&slot[2], (unsigned long long)want);
     g0 = __shfl_sync(0xffffffffu, next, 0);
     gn = want;
@@ -855,16 +863,16 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         // small-core kernel the extra pass and barrier cost more than they save.)
         defer_scout = kLarge && !emit;
         if (kLarge && defer_scout)
-          td_step<3>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
+          td_step<3, kLarge>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
                      scout_acc, claims_acc, root);
         else if (!emit)
-          td_step<0>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
+          td_step<0, kLarge>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
                      scout_acc, claims_acc, root);
         else if (saw_bu)
-          td_step<1>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
+          td_step<1, kLarge>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
                      scout_acc, claims_acc, root);
         else
-          td_step<2>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
+          td_step<2, kLarge>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
                      scout_acc, claims_acc, root);
       }
       if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();

@@ -259,7 +259,11 @@ __device__ void part_td(const BfsParams& p, const PartDev& me, uint64_t nq, uint
     }
     if (nu <= nw) break;
     unsigned long long next = 0;
-    const uint64_t want = nu <= 8 * nw ? 1 : kPGrab;
+    // guided grabs (as the large-core single-GPU kernel): 4..16 chunks,
+    // shrinking with the chunks left, so the per-partition counter is not
+    // saturated on levels with ~10^6 chunks
+    const uint64_t rem = nu - min(nu, g1);
+    const uint64_t want = nu <= 8 * nw ? 1 : max((uint64_t)kPGrab, min(uint64_t{16}, rem / (4 * nw)));
     if (lane == 0) next = nw + atomicAdd(grab, (unsigned long long)want);
     g0 = __shfl_sync(0xffffffffu, next, 0);
     gn = want;
