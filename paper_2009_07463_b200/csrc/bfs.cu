@@ -382,10 +382,7 @@ __device__ __forceinline__ bool scan_row(const P& p, const uint32_t* fcur, uint6
 // trips; measured against lane-only scans up to 1024 neighbours: -0.5 us per
 // root at s22, -2 us at s26).
 constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (the claim buffer + the window)
-#ifndef ETB_LANE_FIRST
-#define ETB_LANE_FIRST 64
-#endif
-constexpr uint32_t kLaneFirst = ETB_LANE_FIRST;
+constexpr uint32_t kLaneFirst = 64;
 // bu_sweep on the large-core kernel once fewer than nc / kSweepT vertices are
 // unvisited (measured at s26: 2 best, -5 us per root; inlined — out of line its
 // call cost the rest of the kernel 3%)
