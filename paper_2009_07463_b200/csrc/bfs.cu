@@ -349,28 +349,6 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
   }
 }
 
-template <class P>
-__device__ __forceinline__ bool scan_row(const P& p, const uint32_t* fcur, uint64_t rb,
-                                         uint64_t re, uint32_t& par) {
-  // The first (highest-degree) neighbour was already probed; the rest of the
-  // row [rb, re) is probed four at a time (independent loads) with early exit.
-  for (uint64_t e = rb + 1; e < re; e += 4) {
-    uint32_t x[4];
-    bool b[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) x[j] = e + j < re ? p.ccol[e + j] : kNone32;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = x[j] != kNone32 && test_bit(fcur, x[j]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (b[j]) {
-        par = x[j];
-        return true;
-      }
-  }
-  return false;
-}
-
 // Bottom-up step (bfs.cpp:88-111). A warp takes kBuU consecutive visited words
 // per iteration, lane = one vertex of each; all first-neighbour probes of the
 // kBuU words are in flight together and each word is written back once.
@@ -420,6 +398,42 @@ __device__ __forceinline__ void bu_append(const uint32_t (&v)[K], const uint32_t
   }
 }
 
+// Two rows scanned together by one lane, two probes each per round trip (the
+// same four loads in flight as one row scanned four at a time), each row with
+// its own early exit: a lane resolves two deferred vertices per pass (half
+// the passes: s22 -1.3 us, s26 -14 us per root; a generic K-row version and
+// four rows spilled).
+template <class P>
+__device__ __forceinline__ void scan_rows2(const P& p, const uint32_t* fcur, uint64_t ea,
+                                           uint64_t enda, uint64_t eb, uint64_t endb,
+                                           uint32_t& pa, uint32_t& pb, bool& ha, bool& hb) {
+  ha = hb = false;
+  while (ea < enda || eb < endb) {
+    const uint32_t x0 = ea < enda ? p.ccol[ea] : kNone32;
+    const uint32_t x1 = ea + 1 < enda ? p.ccol[ea + 1] : kNone32;
+    const uint32_t y0 = eb < endb ? p.ccol[eb] : kNone32;
+    const uint32_t y1 = eb + 1 < endb ? p.ccol[eb + 1] : kNone32;
+    const bool bx0 = x0 != kNone32 && test_bit(fcur, x0);
+    const bool bx1 = x1 != kNone32 && test_bit(fcur, x1);
+    const bool by0 = y0 != kNone32 && test_bit(fcur, y0);
+    const bool by1 = y1 != kNone32 && test_bit(fcur, y1);
+    if (bx0 || bx1) {
+      pa = bx0 ? x0 : x1;
+      ha = true;
+      enda = ea;
+    } else {
+      ea += 2;
+    }
+    if (by0 || by1) {
+      pb = by0 ? y0 : y1;
+      hb = true;
+      endb = eb;
+    } else {
+      eb += 2;
+    }
+  }
+}
+
 template <class P>
 __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext,
                                uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
@@ -428,34 +442,47 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
   const unsigned lane = threadIdx.x & 31;
   __syncwarp();
   uint32_t nlong = 0;
-  for (uint32_t i0 = 0; i0 < nmiss; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    const uint32_t v = i < nmiss ? mbuf[i] : kNone32;
-    bool lng = false, hit = false;
-    uint32_t par = 0, cd = 0;
-    if (v != kNone32) {
-      // the row bounds give the degree too: one round trip before the scan
-      const uint64_t rb = p.crow[v], re = p.crow[v + 1];
-      cd = static_cast<uint32_t>(re - rb);
-      const uint64_t lend = min(re, rb + 1 + kLaneFirst);
-      hit = scan_row(p, fcur, rb, lend, par);
-      lng = !hit && lend < re;
+  for (uint32_t i0 = 0; i0 < nmiss; i0 += 64) {
+    const uint32_t va = i0 + lane < nmiss ? mbuf[i0 + lane] : kNone32;
+    const uint32_t vb = i0 + 32 + lane < nmiss ? mbuf[i0 + 32 + lane] : kNone32;
+    // the row bounds give the degrees too: one round trip before the scans
+    uint64_t rba = 0, rea = 0, rbb = 0, reb = 0;
+    if (va != kNone32) rba = p.crow[va], rea = p.crow[va + 1];
+    if (vb != kNone32) rbb = p.crow[vb], reb = p.crow[vb + 1];
+    const uint64_t la = min(rea, rba + 1 + kLaneFirst), lb = min(reb, rbb + 1 + kLaneFirst);
+    uint32_t pa = 0, pb = 0;
+    bool ha, hb;
+    scan_rows2(p, fcur, rba + 1, va != kNone32 ? la : 0, rbb + 1, vb != kNone32 ? lb : 0, pa, pb,
+               ha, hb);
+    const bool lnga = va != kNone32 && !ha && la < rea;
+    const bool lngb = vb != kNone32 && !hb && lb < reb;
+    if (ha) {
+      p.dp[va] = make_uint2(static_cast<uint32_t>(dnext), pa);
+      atomicOr(&p.visited[va >> 5], 1u << (va & 31));
+      atomicOr(&fnext[va >> 5], 1u << (va & 31));
+      ++claims_acc;
     }
-    if (hit) {
-      p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
-      atomicOr(&p.visited[v >> 5], 1u << (v & 31));
-      atomicOr(&fnext[v >> 5], 1u << (v & 31));
+    if (hb) {
+      p.dp[vb] = make_uint2(static_cast<uint32_t>(dnext), pb);
+      atomicOr(&p.visited[vb >> 5], 1u << (vb & 31));
+      atomicOr(&fnext[vb >> 5], 1u << (vb & 31));
       ++claims_acc;
     }
     if (lslot) {
-      const uint32_t av[1] = {v}, ad[1] = {hit ? cd : 0u};
-      bu_append<1>(av, ad, qv_out, qp_out, lslot);
+      const uint32_t av[2] = {va, vb};
+      const uint32_t ad[2] = {ha ? static_cast<uint32_t>(rea - rba) : 0u,
+                              hb ? static_cast<uint32_t>(reb - rbb) : 0u};
+      bu_append<2>(av, ad, qv_out, qp_out, lslot);
     }
-    // compact long rows to the front of the buffer (slots < i0 are consumed)
-    const unsigned lm = __ballot_sync(0xffffffffu, lng);
+    // compact long rows (no hit in the lane-scanned prefix) to the front of the
+    // buffer (slots < i0 + 64 are already read)
     __syncwarp();
-    if (lng) mbuf[nlong + __popc(lm & ((1u << lane) - 1))] = v;
-    nlong += __popc(lm);
+    const unsigned lma = __ballot_sync(0xffffffffu, lnga);
+    if (lnga) mbuf[nlong + __popc(lma & ((1u << lane) - 1))] = va;
+    nlong += __popc(lma);
+    const unsigned lmb = __ballot_sync(0xffffffffu, lngb);
+    if (lngb) mbuf[nlong + __popc(lmb & ((1u << lane) - 1))] = vb;
+    nlong += __popc(lmb);
     __syncwarp();
   }
   for (uint32_t i = 0; i < nlong; ++i) {
