@@ -270,24 +270,19 @@ __device__ void part_td(const BfsParams& p, const PartDev& me, uint64_t nq, uint
   }
 }
 
-__device__ __forceinline__ bool part_scan_row(const BfsParams& p, const uint32_t* fcur, uint32_t v,
-                                              uint32_t& par) {
-  const uint64_t re = p.crow[v + 1];
-  for (uint64_t e = p.crow[v] + 1; e < re; e += 4) {
-    uint32_t x[4];
-    bool b[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) x[j] = e + j < re ? p.ccol[e + j] : kNone32;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = x[j] != kNone32 && test_bit(fcur, x[j]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (b[j]) {
-        par = x[j];
-        return true;
-      }
-  }
-  return false;
+// Deferred bottom-up misses (as the single-GPU kernel's resolve_misses): each
+// lane scans two rows together over their next kPLaneFirst neighbours (two
+// probes per row in flight, per-row early exit); rows without a hit there are
+// finished by the whole warp, 32 probes per round trip.
+constexpr uint32_t kPLaneFirst = 64;
+
+__device__ __forceinline__ void part_claim(const BfsParams& p, const PartDev& me,
+                                           const Peers& fnext, uint32_t v, uint32_t par,
+                                           int32_t dnext, unsigned long long& claims_acc) {
+  p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
+  atomicOr(&me.visited[v >> 5], 1u << (v & 31));
+  fnext.or_bit(v);
+  ++claims_acc;
 }
 
 __device__ void part_misses(const BfsParams& p, const PartDev& me, const uint32_t* fcur,
@@ -295,15 +290,59 @@ __device__ void part_misses(const BfsParams& p, const PartDev& me, const uint32_
                             unsigned long long& claims_acc) {
   const unsigned lane = threadIdx.x & 31;
   __syncwarp();
-  for (uint32_t i = lane; i < nmiss; i += 32) {
-    const uint32_t v = mbuf[i];
-    uint32_t par = 0;
-    if (part_scan_row(p, fcur, v, par)) {
-      p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
-      atomicOr(&me.visited[v >> 5], 1u << (v & 31));
-      fnext.or_bit(v);
-      ++claims_acc;
+  uint32_t nlong = 0;
+  for (uint32_t i0 = 0; i0 < nmiss; i0 += 64) {
+    const uint32_t va = i0 + lane < nmiss ? mbuf[i0 + lane] : kNone32;
+    const uint32_t vb = i0 + 32 + lane < nmiss ? mbuf[i0 + 32 + lane] : kNone32;
+    uint64_t rba = 0, rea = 0, rbb = 0, reb = 0;
+    if (va != kNone32) rba = p.crow[va], rea = p.crow[va + 1];
+    if (vb != kNone32) rbb = p.crow[vb], reb = p.crow[vb + 1];
+    const uint64_t la = min(rea, rba + 1 + kPLaneFirst), lb = min(reb, rbb + 1 + kPLaneFirst);
+    uint64_t ea = rba + 1, eb = rbb + 1, enda = va != kNone32 ? la : 0,
+             endb = vb != kNone32 ? lb : 0;
+    uint32_t pa = 0, pb = 0;
+    bool ha = false, hb = false;
+    while (ea < enda || eb < endb) {
+      const uint32_t x0 = ea < enda ? p.ccol[ea] : kNone32;
+      const uint32_t x1 = ea + 1 < enda ? p.ccol[ea + 1] : kNone32;
+      const uint32_t y0 = eb < endb ? p.ccol[eb] : kNone32;
+      const uint32_t y1 = eb + 1 < endb ? p.ccol[eb + 1] : kNone32;
+      const bool bx0 = x0 != kNone32 && test_bit(fcur, x0);
+      const bool bx1 = x1 != kNone32 && test_bit(fcur, x1);
+      const bool by0 = y0 != kNone32 && test_bit(fcur, y0);
+      const bool by1 = y1 != kNone32 && test_bit(fcur, y1);
+      if (bx0 || bx1) pa = bx0 ? x0 : x1, ha = true, enda = ea;
+      else ea += 2;
+      if (by0 || by1) pb = by0 ? y0 : y1, hb = true, endb = eb;
+      else eb += 2;
     }
+    if (ha) part_claim(p, me, fnext, va, pa, dnext, claims_acc);
+    if (hb) part_claim(p, me, fnext, vb, pb, dnext, claims_acc);
+    const bool lnga = va != kNone32 && !ha && la < rea;
+    const bool lngb = vb != kNone32 && !hb && lb < reb;
+    __syncwarp();
+    const unsigned lma = __ballot_sync(0xffffffffu, lnga);
+    if (lnga) mbuf[nlong + __popc(lma & ((1u << lane) - 1))] = va;
+    nlong += __popc(lma);
+    const unsigned lmb = __ballot_sync(0xffffffffu, lngb);
+    if (lngb) mbuf[nlong + __popc(lmb & ((1u << lane) - 1))] = vb;
+    nlong += __popc(lmb);
+    __syncwarp();
+  }
+  for (uint32_t i = 0; i < nlong; ++i) {
+    const uint32_t v = mbuf[i];
+    const uint64_t rb = p.crow[v] + 1 + kPLaneFirst, re = p.crow[v + 1];
+    uint32_t par = kNone32;
+    for (uint64_t e0 = rb; e0 < re; e0 += 32) {
+      const uint64_t e = e0 + lane;
+      const uint32_t x = e < re ? p.ccol[e] : kNone32;
+      const unsigned m = __ballot_sync(0xffffffffu, x != kNone32 && test_bit(fcur, x));
+      if (m) {
+        par = __shfl_sync(0xffffffffu, x, __ffs(m) - 1);
+        break;
+      }
+    }
+    if (lane == 0 && par != kNone32) part_claim(p, me, fnext, v, par, dnext, claims_acc);
   }
   __syncwarp();
 }
