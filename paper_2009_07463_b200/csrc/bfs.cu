@@ -8,16 +8,20 @@
 //                   (src/bfs.cpp:232-293), decided redundantly by every thread
 //                   from grid-reduced counters, with no host round trip;
 //                     top-down  (bfs.cpp:61-86): merge path — the frontier's
-//                               rows concatenated and cut into 128-edge chunks,
+//                               rows concatenated and cut into 128-edge chunks
+//                               dealt CTA-minor then grabbed from a counter,
 //                               4 edges per lane in flight, check-then-atomicOr
 //                               claims staged in smem and appended to the next
-//                               list in batches (td_step);
+//                               list in batches; on the large-core kernel
+//                               list-less levels claim with reductions and count
+//                               afterwards (td_step);
 //                     bottom-up (bfs.cpp:88-111): 8 visited words per warp, lane
 //                               = vertex, first probe on the contiguous first-
 //                               neighbour array (the highest-degree neighbour,
 //                               since relaid ids are degree sorted), deferred
-//                               scans for misses, one word write-back per word
-//                               (bu_step);
+//                               scans for misses (two rows per lane, then the
+//                               warp for long rows), one word write-back per
+//                               word (bu_step; bu_sweep on late large levels);
 //                   and stops once every core vertex is visited (the level the
 //                   reference would run next claims nothing);
 //   tree replay     TEET/TEOLV (et_bfs.cpp:14-32) as one streaming pass giving
@@ -48,7 +52,7 @@ constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down chunk
 constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex ids)
 constexpr int kBuU = 8;              // visited words per warp per bottom-up iteration
-constexpr uint64_t kGrab = 4;      // top-down chunks per warp per grab on long levels
+constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab on long levels
 
 struct WarpSmem {
   uint32_t cbuf[kCbuf];     // staged claims (top-down); with win: deferred misses (bottom-up)
