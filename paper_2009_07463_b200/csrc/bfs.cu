@@ -752,6 +752,9 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     uint64_t* qp_in = p.qp0;
     uint64_t* qp_out = p.qp1;
     unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0, reached = 1;
+    // The traversal can reach the start's core component only (p.reachable, a
+    // per-root launch parameter): once all of it is visited, the next level
+    // would claim nothing (checked at the level ends).
     double etc = p.edges_to_check;
     bool bu = bu0, saw_bu = bu0;
     if (bu) awake = frontier;
@@ -962,10 +965,11 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           ne = cp & kItemMask;
         }
       }
-      // Every core vertex is visited: the level the reference would run next
-      // (bfs.cpp:240-292; either direction) claims nothing and ends the loop.
-      // Record it with its direction and no claims, without running it.
-      if (reached == p.nc) {
+      // Every core vertex of the start's component is visited: the level the
+      // reference would run next (bfs.cpp:240-292; either direction) claims
+      // nothing and ends the loop. Record it with its direction and no claims,
+      // without running it.
+      if (reached == p.reachable) {
         if (tid == 0 && p.trace && L < 255) p.trace[L] = bu ? 'b' : 't';
         if (p.level_claims && tid == 0 && L < 256) p.level_claims[L] = 0;
         ++L;
@@ -1129,6 +1133,7 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.crow = L.crow.get();
   p.ccol = L.ccol.get();
   p.cfirst = L.cfirst.get();
+  p.reachable = L.nc;
   p.degn = L.degn.get();
   p.cmeta = L.cmeta.get();
   p.nc = static_cast<uint32_t>(L.nc);
@@ -1246,6 +1251,9 @@ void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParam
     ++np;
     S.last_isolated = static_cast<uint32_t>(start);
   }
+  // the start's core component bounds the traversal (see the level loop's end)
+  p.reachable = p.start != kNone32 && p.start < L.h_comp_size.size() ? L.h_comp_size[p.start]
+                                                                       : L.nc;
   p.npatch = 0;
   p.nipatch = 0;
   if (np <= static_cast<uint32_t>(kInlinePatch)) {

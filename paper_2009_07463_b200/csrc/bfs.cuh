@@ -17,6 +17,7 @@ struct BfsParams {
   const uint32_t* cfirst;
   const uint32_t* degn;  // full degree (scout, bfs.cpp:80)
   const uint2* cmeta;    // per core vertex {core degree, full degree}
+  uint64_t reachable;  // core vertices in the start's core component (set per root)
   uint32_t nc;
   uint32_t nwords;       // ceil(nc / 32)
   // edge trees

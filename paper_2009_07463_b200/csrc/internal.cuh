@@ -55,6 +55,10 @@ struct DevLayout {
   DevBuf<uint32_t> ccol;   // ecore
   DevBuf<uint32_t> cfirst; // nc: first (highest-degree) core neighbour or kNone32
   DevBuf<uint2> cmeta;     // nc: {core degree, full degree} — one load per claim
+  // connected components of the core graph: per core vertex, the size of its
+  // component (host copy; a traversal ends once the start's component is
+  // exhausted, as once the whole core is)
+  std::vector<uint32_t> h_comp_size;
   // edge-tree arrays, index t - nc for t in [nc, nc + nt)
   DevBuf<uint32_t> tsrc;    // tree parent (CE for attached roots, self for component roots)
   DevBuf<uint32_t> tanchor; // CE, or kNone32 for whole-component trees

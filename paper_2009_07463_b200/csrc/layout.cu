@@ -434,6 +434,88 @@ std::vector<T> to_host(const T* d, uint64_t n, cudaStream_t s) {
 
 }  // namespace
 
+// ---- core connected components (untimed preprocessing) -------------------------
+// Union-find with hooking of the larger root under the smaller by CAS and path
+// halving; every core edge (u < w) is hooked once, then every vertex is
+// pointed at its root and the roots count their component.
+// Parents only ever point at smaller ids (hooking and halving both move a
+// pointer down), so every walk terminates; loads bypass L1 (the pointers change
+// under concurrent CAS in L2).
+__device__ __forceinline__ uint32_t uf_find(uint32_t* par, uint32_t v) {
+  for (;;) {
+    const uint32_t p = __ldcg(&par[v]);
+    if (p == v) return v;
+    const uint32_t g = __ldcg(&par[p]);
+    if (g == p) return p;
+    atomicCAS(&par[v], p, g);  // path halving
+    v = g;
+  }
+}
+
+__global__ void uf_init_kernel(uint32_t* par, uint32_t* size, uint64_t nc) {
+  GRID_LOOP(v, nc) {
+    par[v] = static_cast<uint32_t>(v);
+    size[v] = 0;
+  }
+}
+
+__global__ void uf_hook_kernel(const uint64_t* crow, const uint32_t* ccol, uint32_t* par,
+                               uint64_t nc) {
+  // warp per core vertex, lanes over its row
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t u = gw; u < nc; u += nw) {
+    for (uint64_t e = crow[u] + lane; e < crow[u + 1]; e += 32) {
+      const uint32_t w = ccol[e];
+      if (w <= u) continue;
+      uint32_t a = static_cast<uint32_t>(u), b = w;
+      for (;;) {
+        a = uf_find(par, a);
+        b = uf_find(par, b);
+        if (a == b) break;
+        if (a > b) {
+          const uint32_t t = a;
+          a = b;
+          b = t;
+        }
+        // hook the larger root b under a
+        if (atomicCAS(&par[b], b, a) == b) break;
+      }
+    }
+  }
+}
+
+__global__ void uf_flatten_kernel(uint32_t* par, uint32_t* size, uint64_t nc) {
+  GRID_LOOP(v, nc) {
+    const uint32_t r = uf_find(par, static_cast<uint32_t>(v));
+    par[v] = r;
+    atomicAdd(&size[r], 1u);
+  }
+}
+
+__global__ void uf_size_of_kernel(const uint32_t* par, const uint32_t* size, uint64_t nc,
+                                  uint32_t* out) {
+  GRID_LOOP(v, nc) out[v] = size[par[v]];
+}
+
+void core_components(DevLayout& L, cudaStream_t s) {
+  const uint64_t nc = L.nc;
+  L.h_comp_size.assign(nc, 0);
+  if (!nc) return;
+  DevBuf<uint32_t> par(nc), size(nc);
+  uf_init_kernel<<<grid_for(nc, 256), 256, 0, s>>>(par.get(), size.get(), nc);
+  ETB_LAUNCH_CHECK();
+  uf_hook_kernel<<<grid_for(nc * 32, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), par.get(), nc);
+  ETB_LAUNCH_CHECK();
+  uf_flatten_kernel<<<grid_for(nc, 256), 256, 0, s>>>(par.get(), size.get(), nc);
+  ETB_LAUNCH_CHECK();
+  uf_size_of_kernel<<<grid_for(nc, 256), 256, 0, s>>>(par.get(), size.get(), nc, par.get());
+  ETB_LAUNCH_CHECK();
+  ETB_CUDA(cudaMemcpyAsync(L.h_comp_size.data(), par.get(), nc * 4, cudaMemcpyDeviceToHost, s));
+  ETB_CUDA(cudaStreamSynchronize(s));
+}
+
 void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout& L,
                   cudaStream_t s) {
   const uint64_t n = g.n;
@@ -683,6 +765,7 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
                                                        nc, L.cfirst.get(), L.cmeta.get());
     ETB_LAUNCH_CHECK();
   }
+  core_components(L, s);
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 
