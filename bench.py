@@ -295,6 +295,8 @@ def run_ours(args):
         eb.write_tree(args.tree_out, int(roots[0]), par)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, roots[: args.cpu_roots])
+    if rank == 0 and world == 1 and args.mh == -1 and not args.no_paper_mode:
+        out["paper_mode"] = measure_paper_mode(g, roots, args.steps, args.warmup)
     scales = [int(x) for x in str(args.secondary_scale).split(",") if x.strip() and int(x)]
     scales = [x for x in scales if x != args.scale]
     if world == 1 and scales:
@@ -330,6 +332,31 @@ def write_report_v1(args, roots, te, seconds, valid, prep_s, n, m):
     }
     with open(args.report_json, "w") as f:
         json.dump(rep, f, indent=2)
+
+
+def measure_paper_mode(g, roots, steps, warmup):
+    """The paper's own configuration at the primary scale (mh=0 with TEOLV,
+    PAPER.md:623): same protocol (L2 flushed between roots, events around the
+    launch), every root validated on the device."""
+    import paper_2009_07463_b200 as eb
+    from paper_2009_07463_b200 import etbfs as E
+    cg = eb.relayout_csr(g, mh=0)
+    starts = cg.old2new[roots.astype(np.int64)]
+    reps = np.tile(starts, steps)
+    ms, _ = E.time_roots(cg, reps, warmup=warmup * len(starts), flush_l2=True,
+                         replay=E.TreeReplay.TEOLV, kernel_times=False)
+    sec = np.asarray(ms, np.float64).reshape(steps, len(starts)).mean(axis=0) / 1e3
+    te = np.empty(len(starts), np.float64)
+    ok = 0
+    for i, s in enumerate(starts):
+        E.bfs_device(cg, int(s), replay=E.TreeReplay.TEOLV)
+        ok += E.result_validate(cg, int(s))["passed"]
+        te[i] = E.result_traversed_edges(cg)
+    hm, _ = harmonic_gteps(te, sec)
+    return {"mh": 0, "replay": "teolv", "value": round(hm, 3), "unit": "GTEPS",
+            "ms_per_bfs_mean": round(float(sec.mean()) * 1e3, 4),
+            "validated_roots": int(ok), "all_valid": ok == len(starts),
+            "core_vertices": int(cg.core_vertex_count)}
 
 
 def measure_secondary(scale, ef, mh, steps, warmup):
@@ -518,6 +545,8 @@ def main():
                     help="also write the reference's JSON report (schema v1, bench.cpp:301-343)")
     ap.add_argument("--tree-out", default=None,
                     help="write the first root's BFS tree (original ids) as an ETT1 file")
+    ap.add_argument("--no-paper-mode", action="store_true",
+                    help="skip the mh=0/TEOLV line at the primary scale")
     ap.add_argument("--secondary-scale", default="26,28",
                     help="comma list of further scales to time (0 = none); under 'secondary'")
     args = ap.parse_args()
