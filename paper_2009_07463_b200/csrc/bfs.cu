@@ -51,7 +51,9 @@ constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
 
 constexpr int kEpl = kTdChunk / 32;  // edges per lane per top-down chunk
 constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex ids)
-constexpr int kBuU = 8;              // visited words per warp per bottom-up iteration
+// visited words per warp per bottom-up iteration: 8 on the large-core kernel,
+// 7 on the small-core one (s22: 5/6/7 all -0.5..-1 us per root against 8, 7 best)
+constexpr int kBuU = 8, kBuUSmall = 7;
 constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab on long levels
 
 struct WarpSmem {
@@ -516,6 +518,7 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
   __syncwarp();
 }
 
+template <int kU>
 __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
                         uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot) {
@@ -524,24 +527,24 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
   const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
-  for (uint64_t w0 = gw * kBuU; w0 < p.nwords; w0 += nw * kBuU) {
-    uint32_t vis[kBuU];
+  for (uint64_t w0 = gw * kU; w0 < p.nwords; w0 += nw * kU) {
+    uint32_t vis[kU];
     bool any = false;
 #pragma unroll
-    for (int k = 0; k < kBuU; ++k) {
+    for (int k = 0; k < kU; ++k) {
       vis[k] = w0 + k < p.nwords ? p.visited[w0 + k] : ~0u;
       any |= vis[k] != ~0u;
     }
     if (!any) continue;
-    uint32_t f[kBuU];
+    uint32_t f[kU];
 #pragma unroll
-    for (int k = 0; k < kBuU; ++k)
+    for (int k = 0; k < kU; ++k)
       f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[(w0 + k) * 32 + lane];
-    bool hit[kBuU];
+    bool hit[kU];
 #pragma unroll
-    for (int k = 0; k < kBuU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
+    for (int k = 0; k < kU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
 #pragma unroll
-    for (int k = 0; k < kBuU; ++k) {
+    for (int k = 0; k < kU; ++k) {
       const uint32_t v = static_cast<uint32_t>((w0 + k) * 32 + lane);
       const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
       if (hit[k]) {
@@ -558,15 +561,15 @@ __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur
       nmiss += __popc(mm);
     }
     if (lslot) {
-      uint32_t av[kBuU], ad[kBuU];
+      uint32_t av[kU], ad[kU];
 #pragma unroll
-      for (int k = 0; k < kBuU; ++k) {
+      for (int k = 0; k < kU; ++k) {
         av[k] = static_cast<uint32_t>((w0 + k) * 32 + lane);
         ad[k] = hit[k] ? p.cmeta[av[k]].x : 0u;
       }
-      bu_append<kBuU>(av, ad, qv_out, qp_out, lslot);
+      bu_append<kU>(av, ad, qv_out, qp_out, lslot);
     }
-    if (nmiss > kMissCap - 32 * kBuU) {
+    if (nmiss > kMissCap - 32 * kU) {
       resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
       nmiss = 0;
     }
@@ -874,8 +877,9 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           bu_sweep<32>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in,
                        qp_in, bu_list ? &slot[0] : nullptr);
         else
-          bu_step(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in, qp_in,
-                  bu_list ? &slot[0] : nullptr);
+          bu_step<kLarge ? kBuU : kBuUSmall>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext,
+                                             claims_acc, qv_in, qp_in,
+                                             bu_list ? &slot[0] : nullptr);
       } else {
         etc -= (double)scout;
         // The next frontier list is emitted only when this frontier's edge count
