@@ -522,6 +522,7 @@ template <int kU>
 __device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
                         uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot) {
+  static_assert(32 * kU <= kMissCap, "one iteration's misses must fit the miss buffer");
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
