@@ -42,9 +42,10 @@ namespace {
 
 using namespace dev;
 
-// One CTA per SM, 768 or 1024 threads (et_bfs_kernel<B>): 768 leaves 80
-// registers per thread and is faster on latency-bound levels (small cores),
-// 1024 keeps more bottom-up probes in flight (large cores); see block_for().
+// One CTA per SM, 640 or 1024 threads (et_bfs_kernel<B>): 640 leaves 96
+// registers per thread (no spills) and is faster on latency-bound levels
+// (small cores), 1024 keeps more probes in flight (large cores); see block_for().
+constexpr int kSmallBlock = 640;
 constexpr int kMaxWarps = 32;
 constexpr int kItemShift = 36;
 constexpr unsigned long long kItemMask = (1ull << kItemShift) - 1;
@@ -1057,26 +1058,28 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
 
 template <int B>
 __global__ void __launch_bounds__(B, 1) et_bfs_kernel(BfsParams p) {
-  et_bfs_body<(B > 768)>(p);
+  et_bfs_body<(B == 1024)>(p);
 }
 
 }  // namespace
 
 const void* kernel_for(int block) {
-  return block == 768 ? reinterpret_cast<const void*>(et_bfs_kernel<768>)
-                      : reinterpret_cast<const void*>(et_bfs_kernel<1024>);
+  return block == kSmallBlock ? reinterpret_cast<const void*>(et_bfs_kernel<kSmallBlock>)
+                              : reinterpret_cast<const void*>(et_bfs_kernel<1024>);
 }
 
-// Measured on B200 (tools/root_profile.py, 64 roots): 768 threads win at
-// scale 22 (102 vs 109 us per root), 1024 at scale 26 (632 vs 655 us); even
-// at scale 24 (core ~10M vertices).
-// ETB_BFS_BLOCK=768|1024 overrides (experiments).
+// Measured on B200 (tools/root_profile.py, 64 roots, end of round 1): the
+// small-core kernel at scale 22 runs 68.2 us per root at 640 threads (with 7
+// words per bottom-up iteration) vs 69.6 at 768 and 92 with the 1024-thread
+// large-core kernel; at scale 26 the large-core kernel at 1024 threads runs
+// 471 us vs 476 at 896 and 578 for the small-core kernel.
+// ETB_BFS_BLOCK=640|1024 overrides (experiments).
 int block_for(uint64_t nc) {
   if (const char* e = getenv("ETB_BFS_BLOCK")) {
     const int b = atoi(e);
-    if (b == 768 || b == 1024) return b;
+    if (b == kSmallBlock || b == 1024) return b;
   }
-  return nc < (uint64_t{1} << 23) ? 768 : 1024;
+  return nc < (uint64_t{1} << 23) ? kSmallBlock : 1024;
 }
 
 void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
