@@ -518,8 +518,9 @@ __global__ void __launch_bounds__(kPBlock, 2) et_bfs_part_kernel(PartParams pp) 
           awake = frontier;
         }
       }
-      // every core vertex visited: the next level claims nothing (see bfs.cu)
-      if (reached == p.nc) {
+      // every core vertex of the start's component visited: the next level
+      // claims nothing (see bfs.cu)
+      if (reached == p.reachable) {
         if (stats && L < 255) p.trace[L] = bu ? 'b' : 't';
         if (stats && L < 256) p.level_claims[L] = 0;
         ++L;
