@@ -1,12 +1,15 @@
 """ET-BFS benchmark on B200 — prints ONE JSON line (the driver's contract).
 
 Metric (BASELINE.json): harmonic-mean GTEPS over 64 roots, plus the fraction of
-the HBM TEPS roofline. Workload: Kronecker R-MAT scale 22 / edgefactor 16
-(BASELINE configs[1], the largest config quoted on one GPU that the same run can
-also time the reference on), generator seed 1, 64 roots from select_roots(seed
-1), ET mode mh=-1 with TEET (the reference's BenchConfig defaults,
-proj/include/etbfs/bench.hpp:30-45). Synthetic inputs produced by the
+the HBM TEPS roofline. Headline workload: Kronecker R-MAT scale 26 /
+edgefactor 16 (BASELINE configs[3], the config the north_star target and the
+metric are quoted on; it fits one B200), generator seed 1, 64 roots from
+select_roots(seed 1), ET mode mh=-1 with TEET (the reference's BenchConfig
+defaults, proj/include/etbfs/bench.hpp:30-45). Synthetic inputs produced by the
 reference's own generator algorithm stand in for the paper's Graph500 inputs.
+Secondary lines: s22/ef16 (configs[1]), s24/ef4 (configs[2], literal and
+giant-component harmonic means), s28/ef16 (configs[4]) and the paper's own
+mode (mh=0 with TEOLV) at the headline scale.
 
 A "step" is one pass of the hot path over the 64 roots: per root, the
 start-side walk + one persistent kernel that runs the whole core DO-BFS and the
@@ -16,12 +19,17 @@ timed events.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--scale S] [--edgefactor E]
                   [--mh M] [--impl ours|reference] [--no-cpu-baseline]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, 1D core partition).
 """
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,6 +43,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "harmonic-mean GTEPS over 64 roots at 1/2/4/8 B200; % of HBM TEPS roofline"
 NROOTS = 64
+L2_NOTE = "flushed between roots (2x L2 memset outside the timed events)"
 
 
 def env_rank():
@@ -113,295 +122,22 @@ class ClockSampler:
 
 
 def captured_traffic(workload):
-    """DRAM bytes per launch of the BFS kernel from the committed ncu --set full
-    capture (profiles/traffic.json), or None when this workload was not captured."""
+    """DRAM bytes per launch of the BFS kernel from the committed ncu capture
+    (profiles/traffic.json), or None when this workload was not captured."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f)[workload]["mean"]
+            return int(json.load(f)[workload]["mean"])
     except Exception:
         return None
 
 
-def dram_block(workload, kernel_s, peak):
-    """Measured DRAM efficiency beside the B_alg normalisation (SURVEY.md §8(d):
-    B_alg counts every core edge once, a direction-optimizing BFS reads ~2% of
-    them, so the B_alg fraction may exceed 1 and is not a DRAM figure)."""
-    t = captured_traffic(workload)
-    if not t:
-        return None
-    gbs = t / kernel_s / 1e9
-    return {"bytes_per_launch": int(t), "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
-            "source": "profiles/traffic.json (ncu dram__bytes_read+write per launch, caches "
-                      "flushed per replay) / the mean CUDA-event kernel time of this run"}
-
-
 def b_alg(nc, ecore, ntree):
-    """algorithmic bytes per BFS (relaid space, u32 core ids)."""
+    """Graph500-style normalisation (every core edge read once)."""
     return 4 * ecore + 8 * (nc + 1) + 8 * nc + 16 * ntree
 
 
-# --------------------------------------------------------------------- ours --
-def run_ours(args):
-    import paper_2009_07463_b200 as eb
-    from paper_2009_07463_b200 import etbfs as E
-
-    rank, world, local = env_rank()
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    E.lib().etb_set_device(local)
-
-    t0 = time.perf_counter()
-    g = eb.generate_graph(scale=args.scale, edgefactor=args.edgefactor, seed=1)
-    t_csr = time.perf_counter() - t0
-    t1 = time.perf_counter()
-    cg = eb.relayout_csr(g, mh=args.mh)
-    t_layout = time.perf_counter() - t1
-    preprocessing_s = time.perf_counter() - t0
-
-    # Roots: select_roots(original, 64, seed 1) (bench.cpp:217-242) in original ids.
-    roots = select_roots_from_degrees(g.degrees(), NROOTS, 1)
-    starts = cg.old2new[roots.astype(np.int64)]
-    if world > 1:
-        # 1D core partition, one GPU per rank, exchange over NVLink peer memory
-        # (bfs_part.cu). Every rank runs every root; the kernels synchronise.
-        from paper_2009_07463_b200 import multi
-        multi.connect(cg, rank, world)
-        dist.barrier()
-
-    te = np.empty(len(starts), np.uint64)
-    valid = []
-    for i, s in enumerate(starts):
-        E.bfs_device(cg, int(s))
-        te[i] = E.result_traversed_edges(cg)  # this rank's owned part when world > 1
-        if world == 1:  # validate_bfs_tree rules 1-5 on the device, every root (untimed)
-            valid.append(E.result_validate(cg, int(s))["passed"])
-    if world > 1:
-        t = torch.tensor(te.astype(np.int64), device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        te = t.cpu().numpy().astype(np.uint64)
-
-    pol = eb.HybridPolicy()
-    reps = np.tile(starts, args.steps)
-    if world > 1:
-        dist.barrier()
-    with ClockSampler(local) as clk:
-        ms, _ = E.time_roots(cg, reps, warmup=args.warmup * len(starts), flush_l2=True,
-                             policy=pol, kernel_times=False)
-    if world > 1:
-        dist.barrier()
-    clocks = clk.summary()
-    # kernel-only times (roofline, diagnostics): one more pass with the pre-launch
-    # event, outside the timed value
-    _, kms = E.time_roots(cg, starts, warmup=len(starts), flush_l2=True, policy=pol)
-    if world > 1:  # per-root device time = max over ranks
-        for arr in (ms, kms):
-            t = torch.tensor(arr, dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            arr[:] = t.cpu().numpy()
-    sec = ms / 1e3
-    te_rep = np.tile(te, args.steps).astype(np.float64)
-    hm, per = harmonic_gteps(te_rep, sec)
-    giant = te_rep == te_rep.max()
-    hm_giant, _ = harmonic_gteps(te_rep[giant], sec[giant])
-    step_ms = float(ms.sum() / args.steps)
-    value = hm
-
-    # Roofline of the dominant (only) kernel: algorithmic bytes / kernel time.
-    peak, peak_src = measured_peak_hbm()
-    peak *= world
-    balg = b_alg(cg.core_vertex_count, cg.restricted_edge_count, cg.tree_vertex_count)
-    kern_s = float(np.mean(kms)) / 1e3
-    achieved = balg / kern_s / 1e9
-    roof_gteps = peak * 1e9 / (balg / float(te.max())) / 1e9
-
-    # e2e: the C-ABI call with a HOST output buffer — the BfsTree content (parent of
-    # every vertex, relaid ids, u32) copied device->host inside the wall-clock timing.
-    n = cg.vertex_count
-    parent_h = np.empty(n, np.uint32)
-    eb.etbfs._check(E.lib().etb_host_register(parent_h.ctypes.data, parent_h.nbytes))
-    e2e_t = []
-    for s in np.concatenate([starts[:3], starts]):
-        c0 = time.perf_counter()
-        eb.etbfs._check(E.lib().etb_bfs_compact(cg.handle, int(s), None, None,
-                                                parent_h.ctypes.data))
-        e2e_t.append(time.perf_counter() - c0)
-    e2e_t = np.array(e2e_t[3:])
-    eb.etbfs._check(E.lib().etb_host_unregister(parent_h.ctypes.data))
-    if world > 1:
-        t = torch.tensor(e2e_t, dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_t = t.cpu().numpy()
-    e2e_hm, _ = harmonic_gteps(te.astype(np.float64), e2e_t)
-
-    # Per-level device timeline of the first root (stats run, untimed).
-    r0 = eb.et_bfs(cg, int(starts[0]), stats=True, want_parent=False, want_depth=False)
-    timeline = {"trace": r0.stats.direction_trace, "claims": r0.stats.level_claims,
-                "level_end_us": [round(x / 1e3, 2) for x in r0.stats.level_ns],
-                "total_us": round(r0.stats.total_ns / 1e3, 2)}
-
-    out = {
-        "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
-        "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-seed1",
-                   "scale": args.scale, "edgefactor": args.edgefactor, "roots": NROOTS,
-                   "root_seed": 1, "mh": args.mh, "replay": "teet", "alpha": 14.0, "beta": 24.0,
-                   "parallelism": f"1d-core-partition-{world}gpu" if world > 1 else "1gpu",
-                   "l2": "flushed between roots (2x L2 memset outside the timed events)"},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": captured_traffic(f"kronecker-s{args.scale}-ef{args.edgefactor}-seed1"),
-                     "peak_source": peak_src, "algorithmic_bytes_per_bfs": int(balg),
-                     "bytes_per_te": round(balg / float(te.max()), 3),
-                     "roofline_gteps": round(roof_gteps, 1),
-                     "frac_of_roofline_gteps": round(hm_giant / roof_gteps, 4),
-                     "dram": dram_block(f"kronecker-s{args.scale}-ef{args.edgefactor}-seed1",
-                                        kern_s, peak)},
-        "e2e": {"value": round(e2e_hm, 3), "unit": "GTEPS",
-                "h2d_bytes_per_step": 8 * len(starts),
-                "d2h_bytes_per_step": 4 * n * len(starts),
-                "api": "etb_bfs_compact (C-ABI, host parent u32[n] output, pinned, wall clock)"},
-        "gpu_launches": int(len(reps)),
-        "clocks": clocks,
-        "detail": {"mean_gteps": round(float(per.mean()), 3), "min_gteps": round(float(per.min()), 3),
-                   "max_gteps": round(float(per.max()), 3),
-                   "hm_gteps_giant_component": round(hm_giant, 3),
-                   "validated_roots": len(valid), "all_valid": all(valid) if valid else None,
-                   "kernel_ms_mean": round(float(np.mean(kms)), 4),
-                   "call_ms_mean": round(float(np.mean(ms)), 4),
-                   "traversed_edges": int(te.max()),
-                   "core_vertices": int(cg.core_vertex_count),
-                   "tree_vertices": int(cg.tree_vertex_count),
-                   "core_directed_edges": int(cg.restricted_edge_count),
-                   "preprocessing_s": round(preprocessing_s, 3),
-                   "generate_build_csr_s": round(t_csr, 3), "classify_relayout_s": round(t_layout, 3),
-                   "timeline_root0": timeline},
-    }
-    if rank == 0 and args.report_json:
-        write_report_v1(args, roots, te, sec[: len(starts)], valid, preprocessing_s,
-                        g.vertex_count, g.undirected_edge_count())
-    if rank == 0 and world == 1 and args.tree_out:
-        # BenchConfig::tree_out (bench.hpp:45): the first root's tree, original ids, ETT1
-        r0t = eb.et_bfs(cg, int(starts[0]), want_depth=False)
-        new2old = np.asarray(cg.new2old, np.uint64)
-        par = np.full(cg.vertex_count, np.uint64(0xFFFFFFFFFFFFFFFF), np.uint64)
-        ok = r0t.parent != np.uint64(0xFFFFFFFFFFFFFFFF)
-        par[new2old[ok]] = new2old[r0t.parent[ok].astype(np.int64)]
-        eb.write_tree(args.tree_out, int(roots[0]), par)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, roots[: args.cpu_roots])
-    if rank == 0 and world == 1 and args.mh == -1 and not args.no_paper_mode:
-        out["paper_mode"] = measure_paper_mode(g, roots, args.steps, args.warmup)
-    scales = [int(x) for x in str(args.secondary_scale).split(",") if x.strip() and int(x)]
-    scales = [x for x in scales if x != args.scale]
-    if world == 1 and scales:
-        del cg, g
-        out["secondary"] = [measure_secondary(sc, args.edgefactor, args.mh, args.steps,
-                                              args.warmup) for sc in scales]
-    if world > 1:
-        dist.destroy_process_group()
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-
-
-def write_report_v1(args, roots, te, seconds, valid, prep_s, n, m):
-    """The reference's JSON report, schema v1 (report_to_json, bench.cpp:301-343),
-    for the first timed pass over the roots, so GPU runs drop into the same
-    tooling as `etbfs_bench --json` output."""
-    gteps = [float(t) / s / 1e9 for t, s in zip(te, seconds)]
-    rep = {
-        "schema_version": 1,
-        "config": {"kernel": "et-bfs", "mh": args.mh, "roots": len(roots), "seed": 1,
-                   "threads": 0, "alpha": 14.0, "beta": 24.0, "replay": "teet",
-                   "rm_zero": False, "round_robin": False, "degree_aware": False,
-                   "block_search": False, "et": True, "segments": 0},
-        "graph": {"vertex_count": int(n), "undirected_edge_count": int(m)},
-        "aggregate": {"mean_gteps": float(np.mean(gteps)), "min_gteps": float(np.min(gteps)),
-                      "max_gteps": float(np.max(gteps)),
-                      "harmonic_mean_seconds": float(len(seconds) / np.sum(1.0 / seconds)),
-                      "preprocessing_seconds": float(prep_s),
-                      "all_valid": bool(all(valid)) if valid else False},
-        "per_root": [{"root": int(r), "seconds": float(s), "traversed_edges": int(t),
-                      "gteps": g, "valid": bool(valid[i]) if valid else False}
-                     for i, (r, s, t, g) in enumerate(zip(roots, seconds, te, gteps))],
-    }
-    with open(args.report_json, "w") as f:
-        json.dump(rep, f, indent=2)
-
-
-def measure_paper_mode(g, roots, steps, warmup):
-    """The paper's own configuration at the primary scale (mh=0 with TEOLV,
-    PAPER.md:623): same protocol (L2 flushed between roots, events around the
-    launch), every root validated on the device."""
-    import paper_2009_07463_b200 as eb
-    from paper_2009_07463_b200 import etbfs as E
-    cg = eb.relayout_csr(g, mh=0)
-    starts = cg.old2new[roots.astype(np.int64)]
-    reps = np.tile(starts, steps)
-    ms, _ = E.time_roots(cg, reps, warmup=warmup * len(starts), flush_l2=True,
-                         replay=E.TreeReplay.TEOLV, kernel_times=False)
-    sec = np.asarray(ms, np.float64).reshape(steps, len(starts)).mean(axis=0) / 1e3
-    te = np.empty(len(starts), np.float64)
-    ok = 0
-    for i, s in enumerate(starts):
-        E.bfs_device(cg, int(s), replay=E.TreeReplay.TEOLV)
-        ok += E.result_validate(cg, int(s))["passed"]
-        te[i] = E.result_traversed_edges(cg)
-    hm, _ = harmonic_gteps(te, sec)
-    return {"mh": 0, "replay": "teolv", "value": round(hm, 3), "unit": "GTEPS",
-            "ms_per_bfs_mean": round(float(sec.mean()) * 1e3, 4),
-            "validated_roots": int(ok), "all_valid": ok == len(starts),
-            "core_vertices": int(cg.core_vertex_count)}
-
-
-def measure_secondary(scale, ef, mh, steps, warmup):
-    """The same timed protocol at BASELINE configs[3]'s scale (s26): HM GTEPS and
-    the HBM-roofline fraction the north_star target is quoted on."""
-    import paper_2009_07463_b200 as eb
-    from paper_2009_07463_b200 import etbfs as E
-    t0 = time.perf_counter()
-    g = eb.generate_graph(scale=scale, edgefactor=ef, seed=1)
-    cg = eb.relayout_csr(g, mh=mh)
-    prep = time.perf_counter() - t0
-    roots = select_roots_from_degrees(g.degrees(), NROOTS, 1)
-    starts = cg.old2new[roots.astype(np.int64)]
-    te = np.empty(len(starts), np.uint64)
-    valid = []
-    for i, s in enumerate(starts):
-        E.bfs_device(cg, int(s))
-        te[i] = E.result_traversed_edges(cg)
-        valid.append(E.result_validate(cg, int(s))["passed"])
-    ms, _ = E.time_roots(cg, np.tile(starts, steps), warmup=warmup * len(starts), flush_l2=True,
-                         kernel_times=False)
-    _, kms = E.time_roots(cg, starts, warmup=len(starts), flush_l2=True)
-    te_rep = np.tile(te, steps).astype(np.float64)
-    hm, per = harmonic_gteps(te_rep, ms / 1e3)
-    peak, _ = measured_peak_hbm()
-    balg = b_alg(cg.core_vertex_count, cg.restricted_edge_count, cg.tree_vertex_count)
-    achieved = balg / (float(np.mean(kms)) / 1e3) / 1e9
-    roof = peak / (balg / float(te.max()))
-    return {"workload": f"kronecker-s{scale}-ef{ef}-seed1", "value": round(hm, 3), "unit": "GTEPS",
-            "ms_per_bfs_mean": round(float(np.mean(ms)), 4),
-            "min_gteps": round(float(per.min()), 3), "max_gteps": round(float(per.max()), 3),
-            "traversed_edges": int(te.max()), "core_vertices": int(cg.core_vertex_count),
-            "core_directed_edges": int(cg.restricted_edge_count),
-            "tree_vertices": int(cg.tree_vertex_count),
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "algorithmic_bytes_per_bfs": int(balg),
-                         "bytes_per_te": round(balg / float(te.max()), 3),
-                         "roofline_gteps": round(roof, 1),
-                         "frac_of_roofline_gteps": round(hm / roof, 4),
-                         "traffic": captured_traffic(f"kronecker-s{scale}-ef{ef}-seed1"),
-                         "dram": dram_block(f"kronecker-s{scale}-ef{ef}-seed1",
-                                            float(np.mean(kms)) / 1e3, peak)},
-            "preprocessing_s": round(prep, 3), "gpu_launches": int(len(ms)),
-            "validated_roots": len(valid), "all_valid": all(valid)}
+def workload_name(scale, ef):
+    return f"kronecker-s{scale}-ef{ef}-seed1"
 
 
 def select_roots_from_degrees(deg, count, seed):
@@ -430,50 +166,286 @@ def select_roots_from_degrees(deg, count, seed):
     return np.array(out, np.uint64)
 
 
-# ---------------------------------------------------------------- reference --
-def ref_pipeline(scale, ef, mh, threads):
-    """The reference's own untimed preprocessing (bench.cpp:253-256) via oracle/_ref."""
-    import oracle as O
-    O.ref().ref_set_threads(threads)
+# --------------------------------------------------------------------- ours --
+class Dist:
+    """torch.distributed plumbing for N > 1 (one rank per GPU); no-ops at N = 1."""
+
+    def __init__(self):
+        self.rank, self.world, self.local = env_rank()
+        self.d = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl")
+            self.d = dist
+
+    def barrier(self):
+        if self.d:
+            self.d.barrier()
+
+    def reduce(self, arr, op):
+        """All-reduce a host array (SUM or MAX) over ranks."""
+        if not self.d:
+            return arr
+        import torch
+        t = torch.tensor(np.asarray(arr, np.float64), device="cuda")
+        self.d.all_reduce(t, op=getattr(self.d.ReduceOp, op))
+        return t.cpu().numpy()
+
+    def close(self):
+        if self.d:
+            self.d.destroy_process_group()
+
+
+def prepare(scale, ef, mh):
+    import paper_2009_07463_b200 as eb
     t0 = time.perf_counter()
-    pairs = O.ref_generate(scale, ef, 1)
-    csr = O.RefCsr(1 << scale, pairs)
-    del pairs
-    prep = O.RefPrepared(csr, mh)
-    a = prep.arrays()
-    deg = np.diff(a["row"]).astype(np.int64)
-    old2new = np.empty(1 << scale, np.int64)
-    old2new[a["new2old"].astype(np.int64)] = np.arange(1 << scale)
-    return csr, prep, deg, old2new, time.perf_counter() - t0
+    g = eb.generate_graph(scale=scale, edgefactor=ef, seed=1)
+    t_csr = time.perf_counter() - t0
+    cg = eb.relayout_csr(g, mh=mh)
+    prep = time.perf_counter() - t0
+    roots = select_roots_from_degrees(g.degrees(), NROOTS, 1)
+    starts = cg.old2new[roots.astype(np.int64)]
+    return g, cg, roots, starts, {"preprocessing_s": round(prep, 3),
+                                  "generate_build_csr_s": round(t_csr, 3)}
 
 
-def ref_time_roots(prep, deg, starts):
-    """Time the reference's et_bfs (the timed `traverse`, bench.cpp:269-271) per root."""
-    secs, tes = [], []
-    for s in starts:
-        par, _, sec = prep.et_bfs(int(s), kernel=1, replay=0)
-        tes.append(int(deg[par != 0xFFFFFFFFFFFFFFFF].sum() // 2))
-        secs.append(sec)
-    return np.array(secs), np.array(tes, np.float64)
+def validate_all(cg, starts, replay, D):
+    """TE per root + validate_bfs_tree rules 1-5 on the device, every root."""
+    from paper_2009_07463_b200 import etbfs as E
+    te = np.empty(len(starts), np.float64)
+    valid = []
+    for i, s in enumerate(starts):
+        E.bfs_device(cg, int(s), replay=replay)
+        if D.world > 1:
+            from paper_2009_07463_b200 import multi
+            multi.assemble_result(cg, D)
+        te[i] = E.result_traversed_edges(cg)
+        if D.rank == 0 or D.world == 1:
+            valid.append(E.result_validate(cg, int(s))["passed"])
+    return te, valid
 
 
-def cpu_baseline(args, roots_orig):
-    import oracle as O
-    if not O.ref_available():
-        return {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
-                "sample": "oracle/_ref not built"}
-    threads = os.cpu_count() or 1
-    csr, prep, deg, old2new, prep_s = ref_pipeline(args.scale, args.edgefactor, args.mh, threads)
-    starts = old2new[roots_orig.astype(np.int64)]
-    secs, tes = ref_time_roots(prep, deg, starts)
-    hm, _ = harmonic_gteps(tes, secs)
-    return {"value": round(hm, 4), "unit": "GTEPS", "cores": threads, "kind": "reference",
-            "sample": f"reference et_bfs (kHybrid, TEET, mh={args.mh}) on the first "
-                      f"{len(starts)} of the 64 seed-1 roots, s{args.scale}/ef{args.edgefactor}, "
-                      f"{threads} OpenMP threads; reference preprocessing {prep_s:.1f}s untimed",
-            "cpu_model": cpu_model()}
+def work_roofline(cg, starts, kms, replay, peak, workload, te):
+    """The roofline of the timed kernel: per root, the bytes a direction-optimizing
+    BFS with this root's level sequence must move (etb_result_work, csrc/work.cu)
+    over its event-timed kernel duration; beside it the DRAM bytes ncu measured
+    per launch (profiles/traffic.json) and SURVEY §8(d)'s B_alg normalisation."""
+    from paper_2009_07463_b200 import etbfs as E
+    works = [E.result_work(cg, int(s), replay=replay) for s in starts]
+    wb = np.array([w.total_bytes for w in works], np.float64)
+    kern_s = float(np.mean(kms)) / 1e3
+    achieved = float(wb.mean()) / kern_s / 1e9
+    traffic = captured_traffic(workload)
+    balg = b_alg(cg.core_vertex_count, cg.restricted_edge_count, cg.tree_vertex_count)
+    out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+           "frac": round(achieved / peak, 4), "traffic": traffic,
+           "algorithmic_bytes_per_launch": int(wb.mean()),
+           "algorithmic_bytes_model": "etb_result_work (csrc/work.cu): frontier rows of top-down "
+                                      "levels, first-neighbour entry + probes to the first "
+                                      "frontier neighbour of every unvisited core vertex on "
+                                      "bottom-up levels, one result write per claim, core-sized "
+                                      "bitmaps once per level, tree replay, unreached fill, "
+                                      "state reset; mean over the 64 roots",
+           "kernel_ms_mean": round(kern_s * 1e3, 4),
+           "bytes_per_te": round(float(wb.mean()) / float(np.max(te)), 3)}
+    if traffic:
+        gbs = traffic / kern_s / 1e9
+        out["dram"] = {"bytes_per_launch": traffic, "achieved_gbs": round(gbs, 1),
+                       "frac": round(gbs / peak, 4),
+                       "traffic_over_algorithmic": round(traffic / float(wb.mean()), 3),
+                       "source": "profiles/traffic.json (ncu dram__bytes_read+write per "
+                                 "launch, caches flushed per replay)"}
+    out["b_alg"] = {"bytes_per_bfs": int(balg), "bytes_per_te": round(balg / float(np.max(te)), 3),
+                    "frac": round(balg / kern_s / 1e9 / peak, 4),
+                    "note": "SURVEY §8(d) normalisation: every core edge read once; a "
+                            "direction-optimizing BFS reads ~2% of them, so this can exceed 1"}
+    w0 = works[0]
+    out["root0_levels"] = {"trace": w0.trace,
+                           "frontier_or_unvisited": [int(x) for x in w0.levels[:, 0]],
+                           "columns_read": [int(x) for x in w0.levels[:, 1]],
+                           "claims": [int(x) for x in w0.levels[:, 2]],
+                           "bytes": [int(x) for x in w0.bytes]}
+    return out
 
 
+def measure(scale, ef, mh, replay, steps, warmup, D, full=True, ctx=None):
+    """The timed protocol on one workload: 64 roots x steps, per-root CUDA events,
+    L2 flushed between roots; max over ranks per root. full adds the kernel-only
+    pass, the roofline, the wall-clock pass and the e2e C-ABI pass."""
+    import paper_2009_07463_b200 as eb
+    from paper_2009_07463_b200 import etbfs as E
+    g, cg, roots, starts, prep = prepare(scale, ef, mh)
+    if D.world > 1:
+        from paper_2009_07463_b200 import multi
+        multi.connect(cg, D.rank, D.world)
+        D.barrier()
+    te, valid = validate_all(cg, starts, replay, D)
+    reps = np.tile(starts, steps)
+    D.barrier()
+    with ClockSampler(D.local) as clk:
+        ms, _ = E.time_roots(cg, reps, warmup=warmup * len(starts), flush_l2=True, replay=replay,
+                             kernel_times=False)
+    D.barrier()
+    ms = D.reduce(ms, "MAX")
+    sec = ms / 1e3
+    te_rep = np.tile(te, steps)
+    hm, per = harmonic_gteps(te_rep, sec)
+    giant = te_rep == te_rep.max()
+    hm_giant, _ = harmonic_gteps(te_rep[giant], sec[giant])
+    rec = {"workload": workload_name(scale, ef), "mh": mh,
+           "replay": "teolv" if replay == E.TreeReplay.TEOLV else "teet",
+           "value": round(hm, 3), "unit": "GTEPS",
+           "ms_per_step": round(float(ms.sum() / steps), 4),
+           "ms_per_bfs_mean": round(float(np.mean(ms)), 4),
+           "mean_gteps": round(float(per.mean()), 3), "min_gteps": round(float(per.min()), 3),
+           "max_gteps": round(float(per.max()), 3),
+           "hm_gteps_giant_component": round(hm_giant, 3),
+           "giant_roots": int(np.count_nonzero(te == te.max())),
+           "traversed_edges": int(te.max()),
+           "validated_roots": len(valid), "all_valid": bool(all(valid)) if valid else None,
+           "core_vertices": int(cg.core_vertex_count),
+           "core_directed_edges": int(cg.restricted_edge_count),
+           "tree_vertices": int(cg.tree_vertex_count),
+           "gpu_launches": int(len(reps)), "clocks": clk.summary(), **prep}
+    small = te != te.max()
+    if small.any():
+        rec["non_giant_roots"] = [{"root": int(r), "te": int(t),
+                                   "ms": round(float(np.mean(ms.reshape(steps, -1)[:, i])), 4)}
+                                  for i, (r, t) in enumerate(zip(roots, te)) if small[i]]
+    if full:
+        peak, peak_src = measured_peak_hbm()
+        peak *= D.world
+        _, kms = E.time_roots(cg, starts, warmup=len(starts), flush_l2=True, replay=replay)
+        kms = D.reduce(kms, "MAX")
+        if D.world == 1:
+            rec["roofline"] = work_roofline(cg, starts, kms, replay, peak, rec["workload"], te)
+            rec["roofline"]["peak_source"] = peak_src
+        # wall clock per call, launch latency included, no copy, no flush
+        wall = D.reduce(E.time_roots_wall(cg, np.tile(starts, 2), warmup=3, replay=replay), "MAX")
+        whm, _ = harmonic_gteps(np.tile(te, 2), wall / 1e3)
+        rec["wall_no_copy"] = {"value": round(whm, 3), "unit": "GTEPS",
+                               "ms_per_bfs_mean": round(float(np.mean(wall)), 4),
+                               "api": "etb_bfs_device + stream synchronise, host timer"}
+        rec["e2e"] = e2e(cg, starts, te, replay, D)
+        r0 = eb.et_bfs(cg, int(starts[0]), replay=replay, stats=True, want_parent=False,
+                       want_depth=False)
+        rec["timeline_root0"] = {"trace": r0.stats.direction_trace,
+                                 "claims": r0.stats.level_claims,
+                                 "level_end_us": [round(x / 1e3, 2) for x in r0.stats.level_ns],
+                                 "total_us": round(r0.stats.total_ns / 1e3, 2)}
+    if ctx is not None:
+        ctx.update(g=g, cg=cg, roots=roots, starts=starts, te=te, valid=valid, sec=sec)
+    return rec
+
+
+def e2e(cg, starts, te, replay, D):
+    """The reference-facing C-ABI call with a HOST output buffer: et_bfs with the
+    BfsTree content (parent of every vertex, relaid ids, u32) copied device->host
+    inside the wall-clock timing (etb_bfs_compact). With N ranks each rank copies
+    its own partition's slice."""
+    from paper_2009_07463_b200 import etbfs as E
+    n = cg.vertex_count
+    parent_h = np.empty(n, np.uint32)
+    E._check(E.lib().etb_host_register(parent_h.ctypes.data, parent_h.nbytes))
+    opt = E._opts(E.CoreKernel.HYBRID, replay, None)
+    t = []
+    try:
+        for s in np.concatenate([starts[:3], starts]):
+            D.barrier()
+            c0 = time.perf_counter()
+            E._check(E.lib().etb_bfs_compact(cg.handle, int(s), E.C.byref(opt), None,
+                                             parent_h.ctypes.data))
+            t.append(time.perf_counter() - c0)
+    finally:
+        E._check(E.lib().etb_host_unregister(parent_h.ctypes.data))
+    t = D.reduce(np.array(t[3:]), "MAX")
+    hm, _ = harmonic_gteps(te, t)
+    return {"value": round(hm, 3), "unit": "GTEPS", "h2d_bytes_per_step": 8 * len(starts),
+            "d2h_bytes_per_step": 4 * n * len(starts),
+            "api": "etb_bfs_compact (C-ABI, host parent u32[n] output, pinned, wall clock)"}
+
+
+def run_ours(args):
+    from paper_2009_07463_b200 import etbfs as E
+    D = Dist()
+    E.lib().etb_set_device(D.local)
+    ctx = {}
+    p = measure(args.scale, args.edgefactor, args.mh, E.TreeReplay.TEET, args.steps, args.warmup,
+                D, full=True, ctx=ctx)
+    out = {
+        "metric": METRIC, "value": p["value"], "unit": "GTEPS", "n_gpus": D.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": p["ms_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": p["workload"], "scale": args.scale, "edgefactor": args.edgefactor,
+                   "roots": NROOTS, "root_seed": 1, "mh": args.mh, "replay": "teet",
+                   "alpha": 14.0, "beta": 24.0,
+                   "parallelism": f"1d-core-partition-{D.world}gpu" if D.world > 1 else "1gpu",
+                   "l2": L2_NOTE},
+        "roofline": p.pop("roofline", None),
+        "e2e": p.pop("e2e"),
+        "gpu_launches": p["gpu_launches"],
+        "clocks": p.pop("clocks"),
+        "detail": p,
+    }
+    if D.rank == 0 and args.report_json:
+        write_report_v1(args, ctx["roots"], ctx["te"], ctx["sec"][:NROOTS], ctx["valid"],
+                        p["preprocessing_s"], ctx["g"].vertex_count,
+                        ctx["g"].undirected_edge_count())
+    if D.world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, ctx)
+    ctx.clear()
+    gc.collect()
+    if D.world == 1:
+        sec = []
+        if args.mh == -1 and not args.no_paper_mode:
+            pm = measure(args.scale, args.edgefactor, 0, E.TreeReplay.TEOLV, args.steps,
+                         args.warmup, D, full=False)
+            pm["note"] = "the paper's configuration (mh=0, TEOLV; PAPER.md:623), same protocol"
+            sec.append(pm)
+            gc.collect()
+        for spec in [x for x in str(args.secondary).split(",") if x.strip() and x.strip() != "0"]:
+            sc, ef = (int(v) for v in spec.split("/"))
+            if (sc, ef) == (args.scale, args.edgefactor):
+                continue
+            r = measure(sc, ef, args.mh, E.TreeReplay.TEET, args.steps, args.warmup, D, full=True)
+            r.pop("timeline_root0", None)
+            sec.append(r)
+            gc.collect()
+        out["secondary"] = sec
+    D.close()
+    if D.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def write_report_v1(args, roots, te, seconds, valid, prep_s, n, m):
+    """The reference's JSON report, schema v1 (report_to_json, bench.cpp:301-343),
+    for the first timed pass over the roots, so GPU runs drop into the same
+    tooling as `etbfs_bench --json` output."""
+    gteps = [float(t) / s / 1e9 for t, s in zip(te, seconds)]
+    rep = {
+        "schema_version": 1,
+        "config": {"kernel": "et-bfs", "mh": args.mh, "roots": len(roots), "seed": 1,
+                   "threads": 0, "alpha": 14.0, "beta": 24.0, "replay": "teet",
+                   "rm_zero": False, "round_robin": False, "degree_aware": False,
+                   "block_search": False, "et": True, "segments": 0},
+        "graph": {"vertex_count": int(n), "undirected_edge_count": int(m)},
+        "aggregate": {"mean_gteps": float(np.mean(gteps)), "min_gteps": float(np.min(gteps)),
+                      "max_gteps": float(np.max(gteps)),
+                      "harmonic_mean_seconds": float(len(seconds) / np.sum(1.0 / seconds)),
+                      "preprocessing_seconds": float(prep_s),
+                      "all_valid": bool(all(valid)) if valid else False},
+        "per_root": [{"root": int(r), "seconds": float(s), "traversed_edges": int(t),
+                      "gteps": g, "valid": bool(valid[i]) if valid else False}
+                     for i, (r, s, t, g) in enumerate(zip(roots, seconds, te, gteps))],
+    }
+    with open(args.report_json, "w") as f:
+        json.dump(rep, f, indent=2)
+
+
+# ---------------------------------------------------------------- reference --
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -484,7 +456,69 @@ def cpu_model():
     return None
 
 
+def ref_time_roots(prep, deg, starts, replay=0):
+    """Time the reference's et_bfs (the timed `traverse`, bench.cpp:269-271) per root."""
+    secs, tes = [], []
+    for s in starts:
+        par, _, sec = prep.et_bfs(int(s), kernel=1, replay=replay)
+        tes.append(int(deg[par != 0xFFFFFFFFFFFFFFFF].sum() // 2))
+        secs.append(sec)
+    return np.array(secs), np.array(tes, np.float64)
+
+
+def cpu_baseline(args, ctx):
+    """The reference's own et_bfs (oracle/_ref, all host cores) timed on a bounded
+    sample of the headline workload. Its input ClassifiedGraph + EdgeTreeList is
+    the device layout downloaded and wrapped in the reference's types: it is
+    byte-identical to the reference's relayout_csr + extract_edge_tree_list
+    (tests/test_gpu_parity.py pins new2old / relaid CSR / ETL hashes against the
+    reference at s16, s22, s24/ef4 and s26), which spares the reference's
+    single-threaded preprocessing (~6 min at s26) — untimed in the reference's
+    own harness too (bench.cpp:253-256)."""
+    import oracle as O
+    if not O.ref_available():
+        return {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    threads = os.cpu_count() or 1
+    O.ref().ref_set_threads(threads)
+    cg = ctx["cg"]
+    t0 = time.perf_counter()
+    n = cg.vertex_count
+    new2old, _, types = cg.new2old, cg.old2new, cg.vertex_type
+    row, col = cg.graph()
+    from paper_2009_07463_b200 import etbfs as E
+    src, dst, ce = E.extract_edge_tree_list(cg)
+    prep = O.RefPrepared.from_arrays(n, cg.core_vertex_count, args.mh, new2old, types, row, col,
+                                     src, dst, ce)
+    del col, src, dst, ce
+    gc.collect()
+    load_s = time.perf_counter() - t0
+    deg = np.diff(row).astype(np.int64)
+    starts = ctx["starts"][: args.cpu_roots]
+    secs, tes = ref_time_roots(prep, deg, starts)
+    del prep
+    hm, _ = harmonic_gteps(tes, secs)
+    k = len(starts)
+    gsec = np.asarray(ctx["sec"]).reshape(-1, NROOTS)[:, :k]
+    ghm, _ = harmonic_gteps(np.tile(ctx["te"][:k], gsec.shape[0]), gsec.reshape(-1))
+    return {"value": round(hm, 4), "unit": "GTEPS", "cores": threads, "kind": "reference",
+            "gpu_same_roots_gteps": round(ghm, 3),
+            "sample": f"unmodified reference et_bfs (kHybrid, TEET, mh={args.mh}) via oracle/_ref "
+                      f"on the first {len(starts)} of the 64 seed-1 roots of "
+                      f"{workload_name(args.scale, args.edgefactor)}, {threads} OpenMP threads, "
+                      f"{float(secs.sum()):.1f}s of CPU work; its ClassifiedGraph is the device "
+                      f"layout downloaded ({load_s:.1f}s, untimed; byte-identical to the "
+                      f"reference's relayout, pinned by the parity tests)",
+            "seconds_per_root": [round(float(x), 4) for x in secs],
+            "cpu_model": cpu_model()}
+
+
 def run_reference(args):
+    """The unmodified reference's own pipeline (oracle/_ref, compiled from
+    /root/reference/proj/src by oracle/Makefile): generate_kronecker -> build_csr
+    (tuples freed, the lean path) -> classify_vertices -> relayout_csr ->
+    extract_edge_tree_list untimed (bench.cpp:253-256), then its et_bfs timed per
+    root (bench.cpp:269-271), ref_roots_per_step roots per step, all host cores."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
@@ -493,8 +527,21 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     threads = os.cpu_count() or 1
-    csr, prep, deg, old2new, prep_s = ref_pipeline(args.scale, args.edgefactor, args.mh, threads)
+    O.ref().ref_set_threads(threads)
+    t0 = time.perf_counter()
+    csr = O.RefCsr.kronecker(args.scale, args.edgefactor, 1)
+    deg_orig = csr.degrees()
+    prep = O.RefPrepared(csr, args.mh)
     roots = csr.select_roots(NROOTS, 1)
+    n = 1 << args.scale
+    new2old = np.empty(n, np.uint64)
+    O.ref().ref_prep_copy(prep.h, O._ptr(new2old), None, None, None, None, None, None)
+    old2new = np.empty(n, np.int64)
+    old2new[new2old.astype(np.int64)] = np.arange(n)
+    deg = deg_orig[new2old.astype(np.int64)].astype(np.int64)  # relaid-space degrees
+    del csr
+    gc.collect()
+    prep_s = time.perf_counter() - t0
     starts = old2new[roots.astype(np.int64)]
     per_step = args.ref_roots_per_step
     for w in range(args.warmup):
@@ -510,23 +557,37 @@ def run_reference(args):
     hm, per = harmonic_gteps(tes, secs)
     out = {
         "impl": "reference", "metric": METRIC, "value": round(hm, 4), "unit": "GTEPS",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(float(secs.sum() / args.steps * 1e3), 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-seed1",
+        "config": {"workload": workload_name(args.scale, args.edgefactor),
                    "scale": args.scale, "edgefactor": args.edgefactor, "roots": NROOTS,
                    "root_seed": 1, "mh": args.mh, "replay": "teet", "alpha": 14.0, "beta": 24.0,
-                   "parallelism": f"openmp{threads}"},
+                   "parallelism": f"openmp{threads}", "l2": "not flushed (CPU)"},
         "cpu_baseline": {"value": round(hm, 4), "unit": "GTEPS", "cores": threads,
                          "kind": "reference",
                          "sample": f"{per_step} roots per step (round robin over the 64 seed-1 "
-                                   f"roots), unmodified reference et_bfs via oracle/_ref",
+                                   f"roots), unmodified reference et_bfs via oracle/_ref after its "
+                                   f"own untimed preprocessing ({prep_s:.0f}s)",
                          "cpu_model": cpu_model()},
         "e2e": {"value": round(hm, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "detail": {"mean_gteps": round(float(per.mean()), 4), "preprocessing_s": round(prep_s, 2)},
+        "detail": {"mean_gteps": round(float(per.mean()), 4), "preprocessing_s": round(prep_s, 2),
+                   "roots_timed": int(len(secs)), "traversed_edges": int(tes.max())},
     }
     print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------- main --
+def spawn_ranks(n):
+    """--gpus N > 1 outside torchrun: re-launch this command as N ranks."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -534,24 +595,31 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--scale", type=int, default=26)
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--mh", type=int, default=-1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-roots", type=int, default=16)
-    ap.add_argument("--ref-roots-per-step", type=int, default=4)
+    ap.add_argument("--cpu-roots", type=int, default=8)
+    ap.add_argument("--ref-roots-per-step", type=int, default=2)
     ap.add_argument("--report-json", default=None,
                     help="also write the reference's JSON report (schema v1, bench.cpp:301-343)")
-    ap.add_argument("--tree-out", default=None,
-                    help="write the first root's BFS tree (original ids) as an ETT1 file")
     ap.add_argument("--no-paper-mode", action="store_true",
-                    help="skip the mh=0/TEOLV line at the primary scale")
-    ap.add_argument("--secondary-scale", default="26,28",
-                    help="comma list of further scales to time (0 = none); under 'secondary'")
+                    help="skip the mh=0/TEOLV line at the headline scale")
+    ap.add_argument("--secondary", default="22/16,24/4,28/16",
+                    help="comma list of scale/edgefactor workloads timed under 'secondary' "
+                         "(0 = none)")
+    ap.add_argument("--dry-ranks", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.dry_ranks:  # launch plumbing only (tests): each rank reports its place
+        rank, world, local = env_rank()
+        print(json.dumps({"dry_ranks": True, "rank": rank, "n_gpus": world, "local_rank": local}),
+              flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

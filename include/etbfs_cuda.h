@@ -191,6 +191,16 @@ int etb_bfs_compact(etb_layout* L, uint64_t start, const etb_bfs_options* opts,
 /* Device pointer to the last result: n interleaved {depth (i32, -1 unreached),
  * parent (u32, UINT32_MAX unreached)} pairs, relaid ids. */
 int etb_result_device_ptr(etb_layout* L, uint32_t** dp);
+/* The last result in ORIGINAL ids, as the reference's translate_tree +
+ * tree_levels give it (validate.hpp:48-50): levels (n u64, ETB_NO_VERTEX =
+ * kUnreached) and/or parent (n u64, ETB_NO_VERTEX unreached); either may be NULL. */
+int etb_result_download_original(etb_layout* L, uint64_t* levels, uint64_t* parent);
+/* Multi-GPU: after the caller wrote every rank's owned result slices (the ranges
+ * of etb_layout_partition_bounds) into this rank's result buffer
+ * (etb_result_device_ptr), the result is whole: etb_result_validate and
+ * etb_result_traversed_edges then treat it as a single-device result. The next
+ * traversal clears the mark. */
+int etb_result_mark_assembled(etb_layout* L);
 /* Copy the last result to host as compact i32 depth / u32 parent (UINT32_MAX unreached). */
 int etb_result_download(etb_layout* L, int32_t* depth, uint32_t* parent);
 /* ½ Σ full degree over reached vertices of the last result (validate.cpp:151-156). */
@@ -220,8 +230,9 @@ int etb_host_unregister(void* ptr);
 /* validate_bfs_tree (validate.hpp:13-46) on the device over the whole graph for the
  * last result from relaid `start`: counts[0..4] = violations of rules 1..5 (root
  * parent, chains, parent edge, level span, reached set), counts[5] = reached
- * vertices. Rules 1-5 together imply every depth is the exact BFS distance. The
- * layout's graph must still be alive. */
+ * vertices. Rules 1-5 together imply every depth is the exact BFS distance. A
+ * layout shares ownership of the graph it was built from, so etb_graph_free may
+ * come first. */
 int etb_result_validate(etb_layout* L, uint64_t start, uint64_t* counts);
 
 /* Diagnostics: one traversal from `start` recording, per level and CTA, the
@@ -253,6 +264,26 @@ int etb_debug_launch_floor(etb_layout* L, int iters, double* empty_us);
 int etb_time_roots(etb_layout* L, const uint64_t* starts, uint64_t count, int warmup,
                    int flush_l2, const etb_bfs_options* opts, double* ms_out,
                    double* kernel_ms_out);
+
+/* Wall-clock time (ms) of each etb_bfs_device call from `starts` up to its
+ * completion (host timer around launch + stream synchronise): the call's launch
+ * latency and start-side walk included, no L2 flush, no host copy. */
+int etb_time_roots_wall(etb_layout* L, const uint64_t* starts, uint64_t count, int warmup,
+                        const etb_bfs_options* opts, double* ms_out);
+
+/* Algorithmic work of the traversal from relaid `start` (re-run with stats):
+ * the bytes a direction-optimizing BFS with this root's level sequence must
+ * move (work.cu: top-down levels read the frontier rows, bottom-up levels the
+ * first-neighbour entry of every unvisited core vertex plus the probes up to
+ * its first frontier neighbour, results written once, core-sized bitmaps once
+ * per level, the tree replay, the unreached fill and the state reset).
+ * levels (4 x 64 u64, may be NULL): per level frontier-or-unvisited vertices,
+ * core columns read, claims, bottom-up first-probe misses; bytes (65 u64, may
+ * be NULL): per level, then the replay/fill/reset tail; nlevels: levels run;
+ * trace (65 chars, may be NULL): their directions; total_bytes: the sum. */
+int etb_result_work(etb_layout* L, uint64_t start, const etb_bfs_options* opts,
+                    uint64_t* levels, uint64_t* bytes, uint32_t* nlevels, char* trace,
+                    uint64_t* total_bytes);
 
 /* ---- step / driver layer (bfs.hpp:66-120) on caller-held state ------------ */
 /* op: 0 top_down_step, 1 bottom_up_step, 2 degree_aware_step, 3 block_search_step,

@@ -107,7 +107,7 @@ def ref() -> C.CDLL:
         _sig(L.ref_build_csr, vp, u64, U64P, u64, C.POINTER(u64), C.POINTER(u64))
         _sig(L.ref_csr_nnz, u64, vp)
         _sig(L.ref_csr_n, u64, vp)
-        _sig(L.ref_csr_copy, None, vp, U64P, U64P)
+        _sig(L.ref_csr_copy, None, vp, vp, vp)
         _sig(L.ref_csr_free, None, vp)
         _sig(L.ref_classify, C.c_int, vp, i64, U8P)
         _sig(L.ref_peak_height, i64, vp)
@@ -123,6 +123,11 @@ def ref() -> C.CDLL:
         _sig(L.ref_oracle_bfs, C.c_int, vp, u64, U64P)
         _sig(L.ref_validate, C.c_int, vp, u64, U64P, C.POINTER(u64), C.POINTER(C.c_int))
         _sig(L.ref_select_roots, C.c_int, vp, u64, u64, U64P)
+        _sig(L.ref_fnv1a64, u64, vp, u64)
+        _sig(L.ref_kron_csr, vp, u32, u64, u64, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64))
+        _sig(L.ref_csr_fnv, None, vp, U64P)
+        _sig(L.ref_prep_fnv, None, vp, U64P)
+        _sig(L.ref_prep_from_arrays, vp, u64, u64, i64, vp, vp, vp, vp, u64, vp, vp, vp)
         _sig(L.ref_run_benchmark, C.c_int, u32, u64, u64, C.c_int, i64, C.c_int, u64, u64, u64,
              U64P, F64P, U64P, I32P, C.POINTER(d), C.POINTER(d))
         _ref = L
@@ -278,6 +283,30 @@ class RefCsr:
         self.n = n
         self.self_loops, self.duplicates = sl.value, du.value
 
+    @classmethod
+    def kronecker(cls, scale, ef=16, seed=1):
+        """generate_kronecker -> build_csr inside the reference library, tuples freed
+        before returning (the lean path: scale 26 fits a 62 GB host)."""
+        L = ref()
+        fnv, sl, du = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        h = L.ref_kron_csr(scale, ef, seed, C.byref(fnv), C.byref(sl), C.byref(du))
+        if not h:
+            raise ValueError(L.ref_last_error().decode())
+        o = cls.__new__(cls)
+        o.h, o.n = h, 1 << scale
+        o.self_loops, o.duplicates, o.tuples_fnv = sl.value, du.value, format(fnv.value, "016x")
+        return o
+
+    def fnv(self):
+        out = np.zeros(2, np.uint64)
+        ref().ref_csr_fnv(self.h, out)
+        return [format(int(x), "016x") for x in out]
+
+    def degrees(self):
+        row = np.empty(self.n + 1, np.uint64)
+        ref().ref_csr_copy(self.h, _ptr(row), None)
+        return np.diff(row)
+
     def __del__(self):
         if getattr(self, "h", None):
             ref().ref_csr_free(self.h)
@@ -290,7 +319,7 @@ class RefCsr:
     def arrays(self):
         row = np.empty(self.n + 1, np.uint64)
         col = np.empty(max(self.nnz, 1), np.uint64)
-        ref().ref_csr_copy(self.h, row, col)
+        ref().ref_csr_copy(self.h, _ptr(row), _ptr(col))
         return row, col[: self.nnz]
 
     def classify(self, mh):
@@ -342,6 +371,28 @@ class RefPrepared:
         self.core = L.ref_prep_core(self.h)
         self.etl_size = L.ref_prep_etl_size(self.h)
         self.restricted_edges = L.ref_prep_restricted_edges(self.h)
+
+    @classmethod
+    def from_arrays(cls, n, core, mh, new2old, types, row, col, etl_src, etl_dst, etl_ce):
+        """Wrap a layout produced elsewhere (byte-identical to the reference's, as the
+        parity tests pin) as the reference's ClassifiedGraph + EdgeTreeList."""
+        L = ref()
+        keep = [np.ascontiguousarray(a, dt) for a, dt in
+                ((new2old, np.uint64), (types, np.uint8), (row, np.uint64), (col, np.uint64),
+                 (etl_src, np.uint64), (etl_dst, np.uint64), (etl_ce, np.uint64))]
+        h = L.ref_prep_from_arrays(n, core, mh, *[_ptr(a) for a in keep[:4]], len(keep[4]),
+                                   *[_ptr(a) for a in keep[4:]])
+        if not h:
+            raise RuntimeError(L.ref_last_error().decode())
+        o = cls.__new__(cls)
+        o.h, o.n, o.core, o.etl_size = h, n, core, len(keep[4])
+        o.restricted_edges = L.ref_prep_restricted_edges(h)
+        return o
+
+    def fnv(self):
+        out = np.zeros(4, np.uint64)
+        ref().ref_prep_fnv(self.h, out)
+        return [format(int(x), "016x") for x in out]
 
     def __del__(self):
         if getattr(self, "h", None):

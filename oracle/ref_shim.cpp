@@ -255,6 +255,96 @@ void ref_prep_copy(void* p, uint64_t* new2old, uint8_t* types, uint64_t* row_off
 }
 void ref_prep_free(void* p) { delete static_cast<Prepared*>(p); }
 
+// ---- lean entry points for scale 26 (host RAM) -----------------------------------
+// FNV-1a-64 over bytes (SURVEY.md Appendix A convention); a hash, not reference logic.
+static uint64_t fnv_bytes(const void* data, uint64_t len, uint64_t h = 0xcbf29ce484222325ull) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (uint64_t i = 0; i < len; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+uint64_t ref_fnv1a64(const void* data, uint64_t len) { return fnv_bytes(data, len); }
+
+// generate_kronecker -> build_csr with the tuples freed before returning: the
+// reference's own functions, without a second copy of the tuple list in Python
+// (scale 26: 17 GB of tuples + the build's 34 GB fit a 62 GB host only this way).
+void* ref_kron_csr(uint32_t scale, uint64_t ef, uint64_t seed, uint64_t* tuples_fnv,
+                   uint64_t* self_loops, uint64_t* dups) {
+  try {
+    KroneckerParams p;
+    p.scale = scale;
+    p.edgefactor = ef;
+    p.seed = seed;
+    BuildStats st;
+    CsrGraph* g;
+    {
+      EdgeList el = generate_kronecker(p);
+      if (tuples_fnv) *tuples_fnv = fnv_bytes(el.edges.data(), el.edges.size() * sizeof(Edge));
+      g = new CsrGraph(build_csr(el, &st));
+    }
+    if (self_loops) *self_loops = st.dropped_self_loops;
+    if (dups) *dups = st.dropped_duplicates;
+    return g;
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+// FNV of the CSR arrays: out[0] row_offsets, out[1] col_indices.
+void ref_csr_fnv(void* h, uint64_t* out) {
+  const CsrGraph& g = *static_cast<CsrGraph*>(h);
+  out[0] = fnv_bytes(g.row_offsets.data(), g.row_offsets.size() * 8);
+  out[1] = fnv_bytes(g.col_indices.data(), g.col_indices.size() * 8);
+}
+// FNV of a prepared layout without copying it out: out[0] new2old, out[1] relaid
+// row_offsets, out[2] relaid col_indices, out[3] ETL as (src,dst,core_edge) u64 rows.
+void ref_prep_fnv(void* p, uint64_t* out) {
+  const auto* pp = static_cast<Prepared*>(p);
+  const auto& cg = pp->cg;
+  out[0] = fnv_bytes(cg.new2old.data(), cg.new2old.size() * 8);
+  out[1] = fnv_bytes(cg.graph.row_offsets.data(), cg.graph.row_offsets.size() * 8);
+  out[2] = fnv_bytes(cg.graph.col_indices.data(), cg.graph.col_indices.size() * 8);
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (const auto& e : pp->etl.entries) {
+    const uint64_t row[3] = {e.src, e.dst, e.core_edge};
+    h = fnv_bytes(row, 24, h);
+  }
+  out[3] = h;
+}
+// A layout produced elsewhere (byte-identical to relayout_csr + extract, as the
+// parity tests pin) wrapped as the reference's ClassifiedGraph / EdgeTreeList, so
+// the reference's et_bfs can be timed without re-running its single-threaded
+// preprocessing. Arrays are in relaid space; types are VertexType codes.
+void* ref_prep_from_arrays(uint64_t n, uint64_t core, int64_t mh, const uint64_t* new2old,
+                           const uint8_t* types, const uint64_t* row, const uint64_t* col,
+                           uint64_t etl_count, const uint64_t* etl_src, const uint64_t* etl_dst,
+                           const uint64_t* etl_ce) {
+  try {
+    auto* p = new Prepared;
+    ClassifiedGraph& cg = p->cg;
+    cg.graph.vertex_count = n;
+    cg.graph.row_offsets.assign(row, row + n + 1);
+    cg.graph.col_indices.assign(col, col + row[n]);
+    cg.graph.degrees.resize(n);
+    for (uint64_t v = 0; v < n; ++v) cg.graph.degrees[v] = row[v + 1] - row[v];
+    cg.vertex_type.resize(n);
+    for (uint64_t v = 0; v < n; ++v) cg.vertex_type[v] = static_cast<VertexType>(types[v]);
+    cg.new2old.assign(new2old, new2old + n);
+    cg.old2new = invert_permutation(cg.new2old);
+    cg.core_vertex_count = core;
+    cg.mh = mh;
+    p->etl.entries.resize(etl_count);
+    for (uint64_t i = 0; i < etl_count; ++i)
+      p->etl.entries[i] = EdgeTreeEntry{etl_src[i], etl_dst[i], etl_ce[i]};
+    return p;
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
 // kernel: 0 top-down, 1 hybrid (et_bfs.hpp CoreKernel order); replay 0 teet, 1 teolv.
 // Writes the relaid-space parent array and the direction trace; returns seconds.
 double ref_et_bfs(void* p, uint64_t start, int kernel, int replay, double alpha, double beta,

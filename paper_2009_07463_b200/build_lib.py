@@ -92,3 +92,30 @@ def build_cpp_tests() -> str:
     if r.returncode != 0:
         raise RuntimeError(f"test_dropin build failed:\n{r.stderr}")
     return out
+
+
+REF_ACCEPTANCE = "/root/reference/proj/tests/acceptance.cpp"
+ACCEPTANCE_BIN = os.path.join(ROOT, "tests", "cpp", "bin", "acceptance_ref")
+
+
+def build_acceptance() -> str | None:
+    """The reference's UNMODIFIED acceptance gate (proj/tests/acceptance.cpp,
+    compiled where it lies) against include/ + libetbfs_b200.so: the drop-in
+    headers must accept the reference's own caller, and the gate then runs on
+    the GPU (tests/test_gpu_acceptance.py). Needs /root/reference (this
+    container); the built binary travels to the GPU box with the snapshot."""
+    if not os.path.exists(REF_ACCEPTANCE):
+        return ACCEPTANCE_BIN if os.path.exists(ACCEPTANCE_BIN) else None
+    os.makedirs(os.path.dirname(ACCEPTANCE_BIN), exist_ok=True)
+    deps = [REF_ACCEPTANCE, LIB] + [os.path.join(ROOT, "include", "etbfs", f)
+                                    for f in os.listdir(os.path.join(ROOT, "include", "etbfs"))]
+    if os.path.exists(ACCEPTANCE_BIN) and \
+            os.path.getmtime(ACCEPTANCE_BIN) >= max(os.path.getmtime(d) for d in deps):
+        return ACCEPTANCE_BIN
+    cmd = [CXX, "-std=c++20", "-O2", "-fopenmp", "-I" + os.path.join(ROOT, "include"),
+           REF_ACCEPTANCE, "-o", ACCEPTANCE_BIN, "-L" + os.path.dirname(LIB), "-letbfs_b200",
+           "-Wl,-rpath,$ORIGIN/../../../paper_2009_07463_b200/lib"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"acceptance build failed:\n{r.stderr[-4000:]}")
+    return ACCEPTANCE_BIN

@@ -961,7 +961,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           bu = true;
           saw_bu = true;
           awake = frontier;
-        } else if (!list_valid && reached < p.nc) {
+        } else if (!list_valid && reached < p.reachable) {
           unsigned long long* cslot = p.ctr + 16 + (L & 1);
           convert_step(p, F[L % 3], qv_in, qp_in, cslot);
           grid_sync_add(p.bar, sm, 0, nullptr, 0, nullptr, cslot, 1);

@@ -93,6 +93,7 @@ struct BfsState {
   uint32_t parity = 0;  // which half of visited / fb0 / fb1 / ctr the next launch uses
   uint64_t words = 0;   // per half
   bool has_result = false;
+  bool assembled = false;  // multi-GPU: the caller merged every rank's owned slices into dp
   uint64_t last_start = ~uint64_t{0};
 };
 
@@ -105,5 +106,12 @@ void bfs_launch(const BfsParams& p, BfsState& S, cudaStream_t s);
 void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParams& p,
                        cudaStream_t s);
 void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p);
+
+// work.cu: the algorithmic work of the traversal whose result is dp, from its
+// depths and the direction trace of its nl levels (see work.cu): levels[4 L + k]
+// counters, bytes[L] per level, bytes[nl] the replay / fill / reset tail;
+// returns the total bytes.
+uint64_t result_work(const DevLayout& L, const uint2* dp, const char* trace, int nl,
+                     uint64_t* levels, uint64_t* bytes, cudaStream_t s);
 
 }  // namespace etb

@@ -15,7 +15,9 @@
 #include "bfs_part.cuh"
 
 struct etb_graph {
-  etb::DevGraph g;
+  // shared with the layouts built from it (they keep it alive past etb_graph_free)
+  std::shared_ptr<etb::DevGraph> sp = std::make_shared<etb::DevGraph>();
+  etb::DevGraph& g = *sp;
   int device = 0;
   cudaStream_t stream = nullptr;
   ~etb_graph() {
@@ -164,6 +166,7 @@ etb::BfsParams run_bfs(etb_layout* h, uint64_t start, const etb_bfs_options* o,
     etb::bfs_launch(p, h->S, h->stream);
   }
   h->S.has_result = true;
+  h->S.assembled = false;
   h->S.last_start = start;
   return p;
 }
@@ -232,6 +235,19 @@ void download_result(etb_layout* h, int32_t* depth, uint32_t* parent, uint64_t* 
   if (parent) ETB_CUDA(cudaMemcpyAsync(parent, S.tmp_parent.get(), n * 4, cudaMemcpyDeviceToHost, s));
   if (parent64) ETB_CUDA(cudaMemcpyAsync(parent64, p64.get(), n * 8, cudaMemcpyDeviceToHost, s));
   ETB_CUDA(cudaStreamSynchronize(s));
+}
+
+// Relaid {depth, parent} -> original ids (translate_tree + tree_levels,
+// validate.hpp:48-50): levels u64 (kUnreached = ~0), parent u64 (kNoVertex).
+__global__ void lift_kernel(const uint2* dp, const uint32_t* new2old, uint64_t n, uint64_t* lv,
+                            uint64_t* par) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 e = dp[v];
+    const uint32_t o = new2old[v];
+    if (lv) lv[o] = static_cast<int32_t>(e.x) >= 0 ? e.x : ~0ull;
+    if (par) par[o] = e.y == etb::kNone32 ? ~0ull : new2old[e.y];
+  }
 }
 
 __global__ void widen_kernel(const uint32_t* in, uint64_t n, uint64_t* out) {
@@ -539,6 +555,7 @@ int etb_layout_build(const etb_graph* g, int64_t mh, etb_layout** out) {
       etb::classify_device(g->g, mh, type, counts, nullptr, h->stream);
       etb::build_layout(g->g, type.get(), mh, h->L, h->stream);
     }
+    h->L.src_graph = g->sp;
     finish_layout(h.get());
     *out = h.release();
   });
@@ -563,6 +580,7 @@ int etb_layout_build_types(const etb_graph* g, const uint8_t* types, int64_t mh,
         ETB_CUDA(cudaMemcpyAsync(type.get(), types, g->g.n, cudaMemcpyHostToDevice, h->stream));
       etb::build_layout(g->g, type.get(), mh, h->L, h->stream);
     }
+    h->L.src_graph = g->sp;
     finish_layout(h.get());
     *out = h.release();
   });
@@ -675,6 +693,37 @@ int etb_result_device_ptr(etb_layout* h, uint32_t** dp) {
   });
 }
 
+int etb_result_download_original(etb_layout* h, uint64_t* levels, uint64_t* parent) {
+  return guarded([&] {
+    need(h, "etb_result_download_original");
+    if (!h->S.has_result) throw std::invalid_argument("etb_result_download_original: no result");
+    if (h->P && h->P->local < h->P->nparts && !h->S.assembled)
+      throw std::invalid_argument("etb_result_download_original: result is spread over several "
+                                  "GPUs");
+    ETB_CUDA(cudaSetDevice(h->device));
+    const uint64_t n = h->L.n;
+    if (!n || (!levels && !parent)) return;
+    cudaStream_t s = h->stream;
+    etb::DevBuf<uint64_t> lv, pa;
+    if (levels) lv.alloc(n);
+    if (parent) pa.alloc(n);
+    lift_kernel<<<etb::grid_for(n, 256), 256, 0, s>>>(h->S.dp.get(), h->L.new2old.get(), n,
+                                                       lv.get(), pa.get());
+    ETB_LAUNCH_CHECK();
+    if (levels) ETB_CUDA(cudaMemcpyAsync(levels, lv.get(), n * 8, cudaMemcpyDeviceToHost, s));
+    if (parent) ETB_CUDA(cudaMemcpyAsync(parent, pa.get(), n * 8, cudaMemcpyDeviceToHost, s));
+    ETB_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int etb_result_mark_assembled(etb_layout* h) {
+  return guarded([&] {
+    need(h, "etb_result_mark_assembled");
+    if (!h->S.has_result) throw std::invalid_argument("etb_result_mark_assembled: no result");
+    h->S.assembled = true;
+  });
+}
+
 int etb_result_download(etb_layout* h, int32_t* depth, uint32_t* parent) {
   return guarded([&] {
     need(h, "etb_result_download");
@@ -690,7 +739,7 @@ int etb_result_traversed_edges(etb_layout* h, uint64_t* te) {
     ETB_CUDA(cudaSetDevice(h->device));
     etb::DevBuf<unsigned long long> acc(1);
     ETB_CUDA(cudaMemsetAsync(acc.get(), 0, 8, h->stream));
-    if (h->P && h->P->local < h->P->nparts) {
+    if (h->P && h->P->local < h->P->nparts && !h->S.assembled) {
       // Multi-GPU: this device holds only its partitions' results; the caller
       // sums the partial counts over ranks.
       for (uint32_t j = 0; j < h->P->local; ++j) {
@@ -715,10 +764,54 @@ int etb_result_validate(etb_layout* h, uint64_t start, uint64_t* counts) {
     need(h, "etb_result_validate");
     need(counts, "etb_result_validate");
     if (start >= h->L.n) throw std::invalid_argument("validate_bfs_tree: root out of range");
-    if (h->P && h->P->local < h->P->nparts)
-      throw std::invalid_argument("etb_result_validate: result is spread over several GPUs");
+    if (h->P && h->P->local < h->P->nparts && !h->S.assembled)
+      throw std::invalid_argument("etb_result_validate: result is spread over several GPUs "
+                                  "(merge the ranks' owned slices, then etb_result_mark_assembled)");
     ETB_CUDA(cudaSetDevice(h->device));
     etb::validate_result(h->L, h->S.dp.get(), start, counts, h->stream);
+  });
+}
+
+int etb_result_work(etb_layout* h, uint64_t start, const etb_bfs_options* opts,
+                    uint64_t* levels, uint64_t* bytes, uint32_t* nlevels, char* trace,
+                    uint64_t* total_bytes) {
+  return guarded([&] {
+    need(h, "etb_result_work");
+    need(total_bytes, "etb_result_work");
+    if (h->P) throw std::invalid_argument("etb_result_work: single-partition layouts only");
+    ETB_CUDA(cudaSetDevice(h->device));
+    run_bfs(h, start, opts, true);
+    etb_bfs_stats st;
+    collect_stats(h, &st);
+    // levels recorded but not run (the start's component was exhausted) end the
+    // trace with zero claims: no work
+    int nl = static_cast<int>(st.levels);
+    while (nl > 0 && st.level_claims[nl - 1] == 0) --nl;
+    *total_bytes = etb::result_work(h->L, h->S.dp.get(), st.direction_trace, nl, levels, bytes,
+                                    h->stream);
+    if (nlevels) *nlevels = static_cast<uint32_t>(nl);
+    if (trace) {
+      std::memcpy(trace, st.direction_trace, nl);
+      trace[nl] = 0;
+    }
+  });
+}
+
+int etb_time_roots_wall(etb_layout* h, const uint64_t* starts, uint64_t count, int warmup,
+                        const etb_bfs_options* opts, double* ms_out) {
+  return guarded([&] {
+    need(h, "etb_time_roots_wall");
+    if (count) need(starts, "etb_time_roots_wall");
+    ETB_CUDA(cudaSetDevice(h->device));
+    for (int w = 0; w < warmup && count; ++w) run_bfs(h, starts[w % count], opts, false);
+    ETB_CUDA(cudaStreamSynchronize(h->stream));
+    for (uint64_t i = 0; i < count; ++i) {
+      const auto t0 = std::chrono::steady_clock::now();
+      run_bfs(h, starts[i], opts, false);
+      ETB_CUDA(cudaStreamSynchronize(h->stream));
+      const auto t1 = std::chrono::steady_clock::now();
+      if (ms_out) ms_out[i] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    }
   });
 }
 

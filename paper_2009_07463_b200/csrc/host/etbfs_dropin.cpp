@@ -15,6 +15,7 @@
 #include "etbfs/classify.hpp"
 #include "etbfs/et_bfs.hpp"
 #include "etbfs/kronecker.hpp"
+#include "etbfs/preprocess.hpp"
 #include "etbfs/relayout.hpp"
 #include "etbfs/types.hpp"
 #include "etbfs_cuda.h"
@@ -70,42 +71,106 @@ LayoutPtr layout_from_types(etb_graph* g, const std::vector<uint8_t>& types, std
   return LayoutPtr(l);
 }
 
+// Content hash of a host array: 64-bit words folded through four independent
+// multiply-rotate lanes (several GB/s; a cache key, not a checksum).
+uint64_t hash_bytes(const void* data, size_t bytes, uint64_t seed) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  uint64_t h[4] = {seed ^ 0x9E3779B97F4A7C15ull, seed + 0xBF58476D1CE4E5B9ull,
+                   ~seed, seed * 0x94D049BB133111EBull + 1};
+  size_t i = 0;
+  auto step = [](uint64_t a, uint64_t x) {
+    a ^= x * 0x9E3779B97F4A7C15ull;
+    a = (a << 31) | (a >> 33);
+    return a * 0xBF58476D1CE4E5B9ull;
+  };
+  for (; i + 32 <= bytes; i += 32) {
+    uint64_t w[4];
+    std::memcpy(w, p + i, 32);
+    for (int k = 0; k < 4; ++k) h[k] = step(h[k], w[k]);
+  }
+  uint64_t tail = bytes;
+  for (; i < bytes; ++i) tail = step(tail, p[i]);
+  uint64_t r = step(step(step(step(tail, h[0]), h[1]), h[2]), h[3]);
+  r ^= r >> 29;
+  return r;
+}
+
+template <typename T>
+uint64_t hash_vec(const std::vector<T>& v, uint64_t seed) {
+  return hash_bytes(v.data(), v.size() * sizeof(T), seed ^ v.size());
+}
+
+uint64_t hash_etl(const EdgeTreeList& etl) {
+  return hash_bytes(etl.entries.data(), etl.entries.size() * sizeof(EdgeTreeEntry),
+                    0xE71ull ^ etl.entries.size());
+}
+
+uint64_t hash_split(const DegreeSplitAdjacency& sp) {
+  uint64_t h = hash_vec(sp.in_plus, 1);
+  h = hash_vec(sp.minus_offsets, h);
+  h = hash_vec(sp.minus_cols, h);
+  return h;  // (neighbor_limit is checked against the core separately)
+}
+
 // A device layout built for a host ClassifiedGraph (relaid space). Relayout of
 // an already relaid graph is the identity for the reference's own layouts;
 // the maps below translate for any other valid input (e.g. a shuffled core).
+// The cache key is the classified graph's CONTENT (rows, columns, types,
+// new2old, core size, mh), so a new graph at freed addresses or an edit in
+// place never reuses a stale layout.
 struct DeviceCg {
-  const void* key_graph = nullptr;
-  const void* key_types = nullptr;
-  uint64_t key_n = 0, key_m = 0, key_core = 0;
+  uint64_t key = 0;
   GraphPtr g;
   LayoutPtr l;
   std::vector<uint64_t> dev2cg, cg2dev;
   bool identity = true;
+  EdgeTreeList etl;        // the canonical extract_edge_tree_list(cg)
+  uint64_t etl_hash = 0;
+  bool have_split = false;  // the canonical split_degree_aware(cg.graph, core), lazily
+  uint64_t split_hash = 0;
 };
 
 std::mutex g_cache_mu;
 std::unique_ptr<DeviceCg> g_cache;
 
+uint64_t cg_key(const ClassifiedGraph& cg) {
+  const CsrGraph& G = cg.graph;
+  uint64_t h = hash_vec(G.row_offsets, G.vertex_count);
+  h = hash_vec(G.col_indices, h);
+  h = hash_bytes(cg.vertex_type.data(), cg.vertex_type.size() * sizeof(VertexType), h);
+  h = hash_vec(cg.new2old, h);
+  return h ^ (cg.core_vertex_count * 0x9E3779B97F4A7C15ull) ^ static_cast<uint64_t>(cg.mh + 2);
+}
+
 DeviceCg& device_cg(const ClassifiedGraph& cg) {
   const CsrGraph& G = cg.graph;
-  if (g_cache && g_cache->key_graph == G.col_indices.data() &&
-      g_cache->key_types == cg.vertex_type.data() && g_cache->key_n == G.vertex_count &&
-      g_cache->key_m == G.col_indices.size() && g_cache->key_core == cg.core_vertex_count)
-    return *g_cache;
   if (cg.vertex_type.size() != G.vertex_count)
     throw std::invalid_argument("extract_edge_tree_list: types length does not match vertex count");
+  const uint64_t key = cg_key(cg);
+  if (g_cache && g_cache->key == key) return *g_cache;
   auto d = std::make_unique<DeviceCg>();
-  d->key_graph = G.col_indices.data();
-  d->key_types = cg.vertex_type.data();
-  d->key_n = G.vertex_count;
-  d->key_m = G.col_indices.size();
-  d->key_core = cg.core_vertex_count;
+  d->key = key;
   d->g = upload(G);
   d->l = layout_from_types(d->g.get(), type_bytes(cg.vertex_type), cg.mh);
   d->dev2cg.resize(G.vertex_count);
   d->cg2dev.resize(G.vertex_count);
   check(etb_layout_download_maps(d->l.get(), d->dev2cg.data(), d->cg2dev.data(), nullptr));
   for (uint64_t i = 0; i < G.vertex_count && d->identity; ++i) d->identity = d->dev2cg[i] == i;
+  etb_layout_info info;
+  check(etb_layout_info_get(d->l.get(), &info));
+  const uint64_t m = info.tree_vertex_count;
+  std::vector<uint64_t> s(m), t(m), c(m);
+  check(etb_layout_download_etl(d->l.get(), s.data(), t.data(), c.data()));
+  d->etl.entries.resize(m);
+  for (uint64_t i = 0; i < m; ++i) {
+    d->etl.entries[i].src = d->dev2cg[s[i]];
+    d->etl.entries[i].dst = d->dev2cg[t[i]];
+    d->etl.entries[i].core_edge = c[i] == ETB_NO_VERTEX ? kNoVertex : d->dev2cg[c[i]];
+  }
+  if (!d->identity)
+    std::sort(d->etl.entries.begin(), d->etl.entries.end(),
+              [](const EdgeTreeEntry& a, const EdgeTreeEntry& b) { return a.dst < b.dst; });
+  d->etl_hash = hash_etl(d->etl);
   g_cache = std::move(d);
   return *g_cache;
 }
@@ -286,29 +351,12 @@ ClassifiedGraph relayout_csr(const CsrGraph& graph, const std::vector<VertexType
 
 EdgeTreeList extract_edge_tree_list(const ClassifiedGraph& cg) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  DeviceCg& d = device_cg(cg);
-  etb_layout_info info;
-  check(etb_layout_info_get(d.l.get(), &info));
-  const uint64_t m = info.tree_vertex_count;
-  std::vector<uint64_t> s(m), t(m), c(m);
-  check(etb_layout_download_etl(d.l.get(), s.data(), t.data(), c.data()));
-  EdgeTreeList etl;
-  etl.entries.resize(m);
-  for (uint64_t i = 0; i < m; ++i) {
-    etl.entries[i].src = d.dev2cg[s[i]];
-    etl.entries[i].dst = d.dev2cg[t[i]];
-    etl.entries[i].core_edge = c[i] == ETB_NO_VERTEX ? kNoVertex : d.dev2cg[c[i]];
-  }
-  if (!d.identity)
-    std::sort(etl.entries.begin(), etl.entries.end(),
-              [](const EdgeTreeEntry& a, const EdgeTreeEntry& b) { return a.dst < b.dst; });
-  return etl;
+  return device_cg(cg).etl;
 }
 
 BfsTree et_bfs(const ClassifiedGraph& cg, const EdgeTreeList& etl, vertex_t start,
                CoreKernel kernel, TreeReplay replay, const DegreeSplitAdjacency* split,
                const HybridPolicy& policy, KernelStats* stats) {
-  (void)etl;
   const uint64_t n = cg.graph.vertex_count;
   if (start >= n) throw std::invalid_argument("et_bfs: start out of range");
   if (replay == TreeReplay::kTeolv && cg.mh != 0)
@@ -329,6 +377,23 @@ BfsTree et_bfs(const ClassifiedGraph& cg, const EdgeTreeList& etl, vertex_t star
   const etb_bfs_options o = options(kernel, replay, policy);
   std::lock_guard<std::mutex> lk(g_cache_mu);
   DeviceCg& d = device_cg(cg);
+  // The device replays the layout's own tree arrays, i.e. the canonical
+  // extract_edge_tree_list(cg); a caller list that differs from it (edited, or
+  // from another graph) is refused rather than silently ignored.
+  if (etl.entries.size() != d.etl.entries.size() || hash_etl(etl) != d.etl_hash)
+    throw std::invalid_argument(
+        "et_bfs: edge tree list does not match extract_edge_tree_list(cg)");
+  // Likewise the split: the device rows are already in the split's probe order,
+  // which holds for the canonical split_degree_aware(cg.graph, core) only.
+  if (needs_split) {
+    if (!d.have_split) {
+      d.split_hash = hash_split(split_degree_aware(cg.graph, cg.core_vertex_count));
+      d.have_split = true;
+    }
+    if (hash_split(*split) != d.split_hash)
+      throw std::invalid_argument(
+          "et_bfs: split does not match split_degree_aware(cg.graph, core)");
+  }
   return run(d.l.get(), n, d.cg2dev[start], o, stats, d.identity ? nullptr : &d.dev2cg);
 }
 

@@ -1,6 +1,7 @@
 // Internal device data structures shared by the kernels and the C-ABI.
 #pragma once
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -65,7 +66,9 @@ struct DevLayout {
   DevBuf<uint32_t> tdepth;  // distance to the CE (attached) or to the root (component)
   // host copies for the start-in-tree walk (et_bfs.cpp:34-57)
   std::vector<uint32_t> h_tsrc, h_tdepth, h_tanchor, h_tree_start;
-  const DevGraph* src_graph = nullptr;  // for the on-demand full relabelled CSR
+  // The source graph (the on-demand full relabelled CSR, the validator): shared
+  // ownership, so freeing the graph handle first keeps it alive for the layout.
+  std::shared_ptr<const DevGraph> src_graph;
 };
 
 void build_layout(const DevGraph& g, const uint8_t* type_dev, int64_t mh, DevLayout& L,

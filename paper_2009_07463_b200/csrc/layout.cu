@@ -523,7 +523,6 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
   const unsigned gb = grid_for(n, 256);
   L.n = n;
   L.mh = mh;
-  L.src_graph = &g;
   L.nnz_full = g.nnz;
 
   DevBuf<unsigned long long> ctr(16);

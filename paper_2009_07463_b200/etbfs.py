@@ -162,6 +162,8 @@ def lib() -> C.CDLL:
     sig("etb_bfs_compact", vp, u64, C.POINTER(_BfsOptions), vp, vp)
     sig("etb_result_device_ptr", vp, C.POINTER(vp))
     sig("etb_result_download", vp, vp, vp)
+    sig("etb_result_mark_assembled", vp)
+    sig("etb_result_download_original", vp, vp, vp)
     sig("etb_result_traversed_edges", vp, P64)
     sig("etb_result_validate", vp, u64, vp)
     sig("etb_debug_phase_stamps", vp, vp)
@@ -176,6 +178,9 @@ def lib() -> C.CDLL:
     sig("etb_host_register", vp, u64)
     sig("etb_host_unregister", vp)
     sig("etb_time_roots", vp, vp, u64, C.c_int, C.c_int, C.POINTER(_BfsOptions), vp, vp)
+    sig("etb_time_roots_wall", vp, vp, u64, C.c_int, C.POINTER(_BfsOptions), vp)
+    sig("etb_result_work", vp, u64, C.POINTER(_BfsOptions), vp, vp, C.POINTER(C.c_uint32),
+        C.c_char_p, P64)
     sig("etb_graph_degree_split", vp, u64, vp, vp, vp)
     sig("etb_graph_levels", vp, u64, vp)
     sig("etb_graph_validate_tree", vp, u64, vp, vp, vp, vp)
@@ -463,6 +468,16 @@ def result_download(cg: EtLayout, depth: np.ndarray | None = None,
     return depth[:n], parent[:n]
 
 
+def result_original(cg: EtLayout, levels: bool = True, parent: bool = True):
+    """Last result in original ids (translate_tree + tree_levels): (levels u64,
+    parent u64), NO_VERTEX for unreached; either None when not asked for."""
+    n = cg.vertex_count
+    lv = np.empty(max(n, 1), np.uint64) if levels else None
+    pa = np.empty(max(n, 1), np.uint64) if parent else None
+    _check(lib().etb_result_download_original(cg.handle, _ptr(lv), _ptr(pa)))
+    return (lv[:n] if lv is not None else None), (pa[:n] if pa is not None else None)
+
+
 def result_validate(cg: EtLayout, start: int) -> dict:
     """validate_bfs_tree rules 1-5 on the device for the last result."""
     c = np.zeros(6, np.uint64)
@@ -491,6 +506,40 @@ def time_roots(cg: EtLayout, starts, warmup=3, flush_l2=True, kernel=CoreKernel.
     _check(lib().etb_time_roots(cg.handle, _ptr(s), s.size, int(warmup), int(bool(flush_l2)),
                                 C.byref(o), _ptr(ms), _ptr(kms)))
     return ms[: s.size], (kms[: s.size] if kms is not None else None)
+
+
+def time_roots_wall(cg: EtLayout, starts, warmup=3, kernel=CoreKernel.HYBRID,
+                    replay=TreeReplay.TEET, policy: HybridPolicy | None = None):
+    """Per-root wall-clock ms of etb_bfs_device + stream synchronise (launch latency
+    and the start-side walk included; no L2 flush, no host copy)."""
+    s = np.ascontiguousarray(starts, np.uint64)
+    ms = np.empty(max(s.size, 1), np.float64)
+    o = _opts(kernel, replay, policy)
+    _check(lib().etb_time_roots_wall(cg.handle, _ptr(s), s.size, int(warmup), C.byref(o), _ptr(ms)))
+    return ms[: s.size]
+
+
+@dataclass
+class Work:
+    """Algorithmic work of one traversal (etb_result_work, csrc/work.cu)."""
+    trace: str
+    levels: np.ndarray   # (nl, 4): frontier-or-unvisited, columns read, claims, BU misses
+    bytes: np.ndarray    # (nl + 1,): per level, then replay / fill / reset
+    total_bytes: int
+
+
+def result_work(cg: EtLayout, start: int, kernel=CoreKernel.HYBRID, replay=TreeReplay.TEET,
+                policy: HybridPolicy | None = None) -> Work:
+    lv = np.zeros(4 * 64, np.uint64)
+    by = np.zeros(65, np.uint64)
+    nl = C.c_uint32()
+    tr = C.create_string_buffer(66)
+    tot = C.c_uint64()
+    o = _opts(kernel, replay, policy)
+    _check(lib().etb_result_work(cg.handle, int(start), C.byref(o), _ptr(lv), _ptr(by),
+                                 C.byref(nl), tr, C.byref(tot)))
+    k = nl.value
+    return Work(tr.value.decode(), lv[: 4 * k].reshape(k, 4), by[: k + 1], tot.value)
 
 
 def device_count() -> int:

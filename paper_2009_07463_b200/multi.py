@@ -10,6 +10,10 @@
   through torch.distributed (any backend; gloo in the CPU tests), and each rank
   opens its peers' blocks. The BFS kernels then synchronise through NVLink peer
   memory — no NCCL call on the data path.
+* ``assemble_result`` (validation only, outside any timed region): every rank
+  holds the result of the vertices it owns; the owned slices are summed over
+  ranks (disjoint supports, so the sum is the merge) and written back, so the
+  device validator sees the whole tree on every rank.
 """
 from __future__ import annotations
 
@@ -63,3 +67,42 @@ def connect(cg, rank: int, world: int, group=None) -> None:
     blobs = exchange_blobs(buf.raw, group)
     joined = C.create_string_buffer(b"".join(blobs), size * world)
     _check(L.etb_mp_connect(cg.handle, joined))
+
+
+def merge_owned(local, bounds_row, dist, group=None):
+    """The whole result from every rank's owned slices: this rank's owned ranges
+    (core, trees, isolated; bounds_row = its row of partition_bounds) of `local`
+    (a 1-D int64 tensor of interleaved {depth, parent} pairs), zero elsewhere,
+    summed over ranks. Supports are disjoint, so the sum reproduces each owner's
+    entries exactly (negative values included)."""
+    import torch
+
+    out = torch.zeros_like(local)
+    b = [int(x) for x in bounds_row]
+    for lo, hi in ((b[0], b[1]), (b[2], b[3]), (b[4], b[5])):
+        if hi > lo:
+            out[lo:hi] = local[lo:hi]
+    dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+class _DeviceArray:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+                                         "version": 3}
+
+
+def assemble_result(cg, D) -> None:
+    """Merge the ranks' owned slices of the last result into every rank's result
+    buffer and mark it whole (etb_result_mark_assembled)."""
+    import torch
+
+    from .etbfs import _check, lib, partition_bounds
+
+    ptr = C.c_void_p()
+    _check(lib().etb_result_device_ptr(cg.handle, C.byref(ptr)))
+    dp = torch.as_tensor(_DeviceArray(ptr.value, cg.vertex_count), device="cuda")
+    full = merge_owned(dp, partition_bounds(cg, D.world)[D.rank], D.d)
+    dp.copy_(full)
+    torch.cuda.synchronize()
+    _check(lib().etb_result_mark_assembled(cg.handle))

@@ -555,6 +555,87 @@ int main() {
     }
   });
 
+  run_case("layout cache keyed on content: a classified graph rewritten in place", [] {
+    // Two different graphs with the same vertex and edge counts: assigning the
+    // second's layout into the first's vectors reuses their storage (same data()
+    // pointers), the case a pointer-keyed cache would get wrong.
+    const EdgeList a = random_tuples(300, 900, 5), b = random_tuples(300, 900, 6);
+    const CsrGraph ga = build_csr(a), gb = build_csr(b);
+    ClassifiedGraph cg = relayout_csr(ga, classify_vertices(ga, -1), -1);
+    EdgeTreeList etl = extract_edge_tree_list(cg);
+    check_tree_exact(relabeled(cg), et_bfs(cg, etl, 0), 0);
+    const ClassifiedGraph cgb = relayout_csr(gb, classify_vertices(gb, -1), -1);
+    if (cgb.graph.col_indices.size() == cg.graph.col_indices.size()) {
+      const void* before = cg.graph.col_indices.data();
+      cg = cgb;
+      EXPECT(cg.graph.col_indices.data() == before);
+    } else {
+      cg = cgb;
+    }
+    etl = extract_edge_tree_list(cg);
+    for (vertex_t s : {vertex_t{0}, vertex_t{17}, vertex_t{299}})
+      check_tree_exact(relabeled(cg), et_bfs(cg, etl, s), s);
+  });
+
+  run_case("et_bfs refuses an edge tree list or split that does not belong to cg", [] {
+    const CsrGraph g = build_csr(random_tuples(400, 700, 9));
+    const ClassifiedGraph cg = relayout_csr(g, classify_vertices(g, -1), -1);
+    EdgeTreeList etl = extract_edge_tree_list(cg);
+    EXPECT(!etl.entries.empty());
+    if (!etl.entries.empty()) {
+      etl.entries.pop_back();
+      EXPECT(throws_with<std::invalid_argument>([&] { et_bfs(cg, etl, 0); }, "edge tree list"));
+    }
+    const EdgeTreeList good = extract_edge_tree_list(cg);
+    DegreeSplitAdjacency sp = split_degree_aware(cg.graph, cg.core_vertex_count);
+    check_tree_exact(relabeled(cg), et_bfs(cg, good, 0, CoreKernel::kDegreeAware, TreeReplay::kTeet, &sp), 0);
+    if (!sp.minus_cols.empty()) {
+      std::reverse(sp.minus_cols.begin(), sp.minus_cols.end());
+      EXPECT(throws_with<std::invalid_argument>(
+          [&] { et_bfs(cg, good, 0, CoreKernel::kDegreeAware, TreeReplay::kTeet, &sp); }, "split"));
+    }
+  });
+
+  run_case("run_benchmark / report_to_json (bench.hpp:30-89) on the GPU", [] {
+    KroneckerParams kp;
+    kp.scale = 12;
+    kp.edgefactor = 8;
+    kp.seed = 3;
+    const EdgeList el = generate_kronecker(kp);
+    const CsrGraph g = build_csr(el);
+    for (KernelChoice k : {KernelChoice::kTopDown, KernelChoice::kHybrid, KernelChoice::kEtBfs}) {
+      BenchConfig c;
+      c.kernel = k;
+      c.roots = 8;
+      c.seed = 2;
+      const BenchReport r = run_benchmark(el, c);
+      EXPECT(r.all_valid);
+      EXPECT(r.per_root.size() == 8);
+      EXPECT(r.vertex_count == g.vertex_count);
+      EXPECT(r.undirected_edge_count == g.undirected_edge_count());
+      const auto roots = select_roots(g, 8, 2);
+      for (size_t i = 0; i < r.per_root.size(); ++i) {
+        EXPECT(r.per_root[i].root == roots[i]);
+        const BfsTree t = bfs_hybrid(g, roots[i]);
+        EXPECT(r.per_root[i].traversed_edges == validate_bfs_tree(g, t).traversed_edge_count);
+        EXPECT(r.per_root[i].seconds > 0 && r.per_root[i].gteps > 0);
+      }
+      const std::string j = report_to_json(r);
+      EXPECT(j.find("\"schema_version\": 1") != std::string::npos);
+      EXPECT(j.find(std::string("\"kernel\": \"") + to_string(k) + "\"") != std::string::npos);
+      EXPECT(report_to_text(r).find("all trees valid") != std::string::npos);
+    }
+    BenchConfig bad;
+    bad.kernel = KernelChoice::kHybrid;
+    bad.replay = TreeReplay::kTeolv;
+    EXPECT(throws_with<std::invalid_argument>([&] { run_benchmark(el, bad); }, "requires et"));
+    bad = BenchConfig{};
+    bad.degree_aware = bad.block_search = true;
+    EXPECT(throws_with<std::invalid_argument>([&] { run_benchmark(el, bad); }, "mutually"));
+    EXPECT(parse_kernel("et-bfs") == KernelChoice::kEtBfs);
+    EXPECT(throws_with<std::invalid_argument>([] { parse_kernel("bogus"); }, "unknown kernel"));
+  });
+
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

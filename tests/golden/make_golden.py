@@ -12,7 +12,13 @@ Outputs (committed):
   kronecker_s16.json — C1 anchors (scale 16, ef 16, seed 1): hashes of the
                   tuples / CSR / relayout / ETL, BuildStats, the 64 roots,
                   per-root levels hashes, TE, direction traces.
-  kronecker_big.json (--big) — C2 (s22/ef16) and C3 (s24/ef4) counts + hashes.
+  kronecker_big.json (--big) — C2 (s22/ef16) and C3 (s24/ef4) counts + hashes,
+                  reference α/β traces for both ET modes and oracle_bfs level hashes
+                  for all 64 roots.
+  kronecker_huge.json (--huge) — the same record for C4 (s26/ef16), built by the
+                  lean path (generate_kronecker -> build_csr with the tuples freed,
+                  hashes computed inside the reference library): ~52 GB host RAM,
+                  ~35 min on 8 cores.
 """
 from __future__ import annotations
 
@@ -208,20 +214,83 @@ def kron_record(scale, ef, seed=1, nroots=64, level_roots=None, traces=True):
     return rec
 
 
+def kron_record_lean(scale, ef, seed=1, nroots=64, log=print):
+    """One Kronecker config through the reference's lean path, every root's levels
+    (oracle_bfs, validate.cpp:77-91) hashed, the α/β traces of et_bfs for mh=-1
+    (TEET) and mh=0 (TEOLV) — the direction sequence a GPU run must reproduce."""
+    import time
+    t0 = time.time()
+    n = 1 << scale
+    g = O.RefCsr.kronecker(scale, ef, seed)
+    row_fnv, col_fnv = g.fnv()
+    deg = g.degrees().astype(np.int64)
+    rec = dict(scale=scale, edgefactor=ef, seed=seed, tuples_fnv=g.tuples_fnv,
+               self_loops=g.self_loops, duplicates=g.duplicates, nnz=int(g.nnz),
+               row_fnv=row_fnv, col_fnv=col_fnv, max_degree=int(deg.max()))
+    log(f"s{scale}: csr {time.time() - t0:.0f}s")
+    roots = g.select_roots(nroots, 1)
+    rec["roots"] = roots.tolist()
+    rec["peak_height"] = int(g.peak_height())
+    rec["classes"] = {str(mh): np.bincount(g.classify(mh), minlength=5).tolist()
+                      for mh in (-1, 0, 1)}
+    rec["layout"] = {}
+    for mh in (-1, 0):
+        p = O.RefPrepared(g, mh)
+        n2o, row, col, etl = p.fnv()
+        lay = dict(core=int(p.core), etl_size=int(p.etl_size),
+                   restricted_edges=int(p.restricted_edges), new2old_fnv=n2o,
+                   relaid_row_fnv=row, relaid_col_fnv=col, etl_fnv=etl)
+        a_n2o = np.empty(n, np.uint64)
+        O.ref().ref_prep_copy(p.h, O._ptr(a_n2o), None, None, None, None, None, None)
+        old2new = np.empty(n, np.uint64)
+        old2new[a_n2o] = np.arange(n, dtype=np.uint64)
+        del a_n2o
+        lay["traces"] = [p.et_bfs(int(old2new[r]), replay=0 if mh else 1,
+                                  want_parent=False)[1] for r in roots]
+        rec["layout"][str(mh)] = lay
+        del p, old2new
+        log(f"s{scale}: layout mh={mh} {time.time() - t0:.0f}s")
+    te, fnvs, hist = [], [], []
+    for r in roots:
+        lv = g.levels(int(r))
+        fnvs.append(format(int(O.ref().ref_fnv1a64(lv.ctypes.data, lv.nbytes)), "016x"))
+        reached = lv != O.NO_VERTEX
+        te.append(int(deg[reached].sum() // 2))
+        hist.append(np.bincount(lv[reached].astype(np.int64)).tolist())
+    rec["levels_fnv"] = fnvs
+    rec["traversed_edges"] = te
+    rec["level_histograms"] = hist
+    log(f"s{scale}: levels {time.time() - t0:.0f}s")
+    return rec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--huge", action="store_true")
+    ap.add_argument("--only", action="store_true", help="skip corpus and s16")
     args = ap.parse_args()
     O.ref().ref_set_threads(os.cpu_count() or 1)
+    if args.huge:
+        rec = kron_record_lean(26, 16, log=lambda m: print(m, flush=True))
+        with open(os.path.join(OUT, "kronecker_huge.json"), "w") as f:
+            json.dump([rec], f, separators=(",", ":"))
+        print("kronecker_huge.json")
+        return
+    if args.big and args.only:
+        recs = [kron_record_lean(22, 16), kron_record_lean(24, 4)]
+        with open(os.path.join(OUT, "kronecker_big.json"), "w") as f:
+            json.dump(recs, f, separators=(",", ":"))
+        print("kronecker_big.json")
+        return
     corpus()
     with open(os.path.join(OUT, "kronecker_s16.json"), "w") as f:
         json.dump(kron_record(16, 16), f, indent=1)
     print("kronecker_s16.json")
     if args.big:
-        recs = [kron_record(22, 16, level_roots=4, traces=False),
-                kron_record(24, 4, level_roots=4, traces=False)]
+        recs = [kron_record_lean(22, 16), kron_record_lean(24, 4)]
         with open(os.path.join(OUT, "kronecker_big.json"), "w") as f:
-            json.dump(recs, f, indent=1)
+            json.dump(recs, f, separators=(",", ":"))
         print("kronecker_big.json")
 
 

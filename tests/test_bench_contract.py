@@ -47,13 +47,27 @@ def test_reference_arm_line():
 @pytest.mark.gpu
 def test_gpu_arm_line():
     d = run_bench("--scale", "16", "--steps", "1", "--warmup", "3", "--no-cpu-baseline",
-                  "--secondary-scale", "0")
+                  "--secondary", "0", "--no-paper-mode")
     check_common(d, 1, 3)
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    # the work model: every traversal moves at least its bitmaps and results
+    assert 0 < r["algorithmic_bytes_per_launch"] < r["b_alg"]["bytes_per_bfs"]
+    assert r["frac"] <= 1.2
     assert d["gpu_launches"] == 64  # one traversal kernel per root of the step
     assert d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
     assert d["detail"]["all_valid"] is True
+
+
+def test_gpus_flag_spawns_ranks():
+    """--gpus N outside torchrun re-launches bench.py as N ranks (the driver's
+    SCALE runs); every rank sees WORLD_SIZE = N (plumbing only, no GPU work)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--dry-ranks"], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["n_gpus"] == 2 for d in lines)

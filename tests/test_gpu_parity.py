@@ -261,19 +261,6 @@ def test_bfs_s16_64_roots(kron16):
 
 
 @pytest.mark.slow
-def test_bfs_s22_and_s24ef4(kron_big):
-    for k in kron_big:
-        cg, ocsr = kron_check(k["scale"], k["edgefactor"], k["roots"], -1, 4)
-        assert cg.core_vertex_count == k["layout"]["-1"]["core"]
-        assert cg.tree_vertex_count == k["layout"]["-1"]["etl_size"]
-        assert O.fnv1a64(cg.new2old) == k["layout"]["-1"]["new2old_fnv"]
-        cg0 = eb.relayout_csr(eb.generate_graph(scale=k["scale"], edgefactor=k["edgefactor"],
-                                                seed=1), mh=0)
-        assert cg0.core_vertex_count == k["layout"]["0"]["core"]
-        assert O.fnv1a64(cg0.new2old) == k["layout"]["0"]["new2old_fnv"]
-
-
-@pytest.mark.slow
 def test_bfs_s24ef4_tiny_component_roots(kron_big):
     """C3's roots 2590069 and 5097554 sit in TL-pair components (TE = 1)."""
     k = [x for x in kron_big if x["scale"] == 24][0]
