@@ -121,12 +121,14 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def captured_traffic(workload):
+def captured_traffic(workload, per_launch=False):
     """DRAM bytes per launch of the BFS kernel from the committed ncu capture
-    (profiles/traffic.json), or None when this workload was not captured."""
+    (profiles/traffic.json: the first roots of the workload, in order), or None
+    when this workload was not captured."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return int(json.load(f)[workload]["mean"])
+            d = json.load(f)[workload]
+        return [int(x) for x in d["dram_bytes_per_launch"]] if per_launch else int(d["mean"])
     except Exception:
         return None
 
@@ -252,9 +254,13 @@ def work_roofline(cg, starts, kms, replay, peak, workload, te):
            "bytes_per_te": round(float(wb.mean()) / float(np.max(te)), 3)}
     if traffic:
         gbs = traffic / kern_s / 1e9
+        per = captured_traffic(workload, per_launch=True) or []
+        k = min(len(per), len(wb))
+        ratio = float(np.sum(per[:k])) / float(np.sum(wb[:k])) if k else traffic / float(wb.mean())
         out["dram"] = {"bytes_per_launch": traffic, "achieved_gbs": round(gbs, 1),
                        "frac": round(gbs / peak, 4),
-                       "traffic_over_algorithmic": round(traffic / float(wb.mean()), 3),
+                       "traffic_over_algorithmic": round(ratio, 3),
+                       "traffic_over_algorithmic_roots": k,
                        "source": "profiles/traffic.json (ncu dram__bytes_read+write per "
                                  "launch, caches flushed per replay)"}
     out["b_alg"] = {"bytes_per_bfs": int(balg), "bytes_per_te": round(balg / float(np.max(te)), 3),
@@ -340,6 +346,47 @@ def measure(scale, ef, mh, replay, steps, warmup, D, full=True, ctx=None):
     return rec
 
 
+def measure_emulated(ctx, parts_list, steps, warmup):
+    """The multi-GPU algorithm (1D core partition, per-level bitmap allgather
+    fused in the kernel) with G partitions emulated in ONE cooperative launch on
+    this GPU: each partition gets 1/G of the SMs and exchanges through local
+    memory. Same protocol as the headline (64 roots x steps, L2 flushed, CUDA
+    events); every root validated. A G-GPU run would give each partition a whole
+    B200, so this measures the algorithm's overhead (exchange, extra barriers),
+    not multi-GPU throughput."""
+    from paper_2009_07463_b200 import etbfs as E
+    import paper_2009_07463_b200 as eb
+    cg, starts, te = ctx["cg"], ctx["starts"], ctx["te"]
+    single = float(np.mean(ctx["sec"])) * 1e3
+    out = []
+    for G in parts_list:
+        E.partition(cg, G)
+        try:
+            ok = 0
+            for s, t in zip(starts, te):
+                E.bfs_device(cg, int(s))
+                ok += int(bool(E.result_validate(cg, int(s))["passed"]) and
+                          E.result_traversed_edges(cg) == int(t))
+            ms, _ = E.time_roots(cg, np.tile(starts, steps), warmup=warmup * len(starts),
+                                 flush_l2=True, kernel_times=False)
+            hm, _ = harmonic_gteps(np.tile(te, steps), ms / 1e3)
+            r0 = eb.et_bfs(cg, int(starts[0]), stats=True, want_parent=False, want_depth=False)
+            out.append({"partitions": G, "value": round(hm, 3), "unit": "GTEPS",
+                        "ms_per_bfs_mean": round(float(np.mean(ms)), 4),
+                        "vs_single_partition_time": round(float(np.mean(ms)) / single, 3),
+                        "validated_roots": int(ok), "all_valid": bool(ok == len(starts)),
+                        "timeline_root0": {"trace": r0.stats.direction_trace,
+                                           "level_end_us": [round(x / 1e3, 2)
+                                                            for x in r0.stats.level_ns],
+                                           "total_us": round(r0.stats.total_ns / 1e3, 2)}})
+        finally:
+            E.partition(cg, 1)
+    return {"note": "G partitions in one cooperative launch on ONE B200 (1/G of the SMs each, "
+                    "exchange through local memory): the multi-GPU kernel's overhead, not a "
+                    "multi-GPU number", "single_partition_ms_per_bfs": round(single, 4),
+            "runs": out}
+
+
 def e2e(cg, starts, te, replay, D):
     """The reference-facing C-ABI call with a HOST output buffer: et_bfs with the
     BfsTree content (parent of every vertex, relaid ids, u32) copied device->host
@@ -396,6 +443,10 @@ def run_ours(args):
                         ctx["g"].undirected_edge_count())
     if D.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, ctx)
+    if D.world == 1 and args.emulate_partitions:
+        out["partitioned_emulation"] = measure_emulated(
+            ctx, [int(x) for x in args.emulate_partitions.split(",") if x.strip()], args.steps,
+            args.warmup)
     ctx.clear()
     gc.collect()
     if D.world == 1:
@@ -417,7 +468,13 @@ def run_ours(args):
         out["secondary"] = sec
     D.close()
     if D.rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out, default=_json_default), flush=True)
+
+
+def _json_default(o):
+    if isinstance(o, np.generic):
+        return o.item()
+    raise TypeError(f"not JSON serializable: {type(o).__name__}")
 
 
 def write_report_v1(args, roots, te, seconds, valid, prep_s, n, m):
@@ -609,6 +666,8 @@ def main():
     ap.add_argument("--secondary", default="22/16,24/4,28/16",
                     help="comma list of scale/edgefactor workloads timed under 'secondary' "
                          "(0 = none)")
+    ap.add_argument("--emulate-partitions", default="2,4,8",
+                    help="partition counts emulated on one GPU at the headline scale ('' = none)")
     ap.add_argument("--dry-ranks", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3:

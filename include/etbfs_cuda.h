@@ -210,6 +210,11 @@ int etb_result_traversed_edges(etb_layout* L, uint64_t* te);
  * multi-GPU algorithm with the peer exchange in local memory); parts <= 1
  * restores the single-partition kernel. */
 int etb_layout_partition(etb_layout* L, uint32_t parts);
+/* The scope of the partitioned kernel's exchange (fences, counter atomics and
+ * barrier polls): 1 = system scope, as between GPUs (set by etb_mp_export);
+ * 0 = device scope, as between partitions sharing one GPU (the default of
+ * etb_layout_partition). Lets the one-GPU emulation run the multi-GPU code path. */
+int etb_layout_partition_scope(etb_layout* L, int system_scope);
 /* Partition k's owned ranges: bounds[6k..6k+5] = core lo, hi, tree lo, hi,
  * isolated lo, hi (relaid ids). */
 int etb_layout_partition_bounds(const etb_layout* L, uint32_t parts, uint64_t* bounds);

@@ -32,6 +32,8 @@ def sources():
 
 def headers():
     out = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    host = os.path.join(CSRC, "host")
+    out += [os.path.join(host, f) for f in os.listdir(host) if f.endswith(".hpp")]
     out.append(os.path.join(ROOT, "include", "etbfs_cuda.h"))
     return out
 

@@ -36,6 +36,7 @@
 #include <algorithm>
 
 #include "bfs_dev.cuh"
+#include "bfs_part.cuh"
 
 namespace etb {
 namespace {
@@ -56,6 +57,17 @@ constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex i
 // 7 on the small-core one (s22: 5/6/7 all -0.5..-1 us per root against 8, 7 best)
 constexpr int kBuU = 8, kBuUSmall = 7;
 constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab on long levels
+
+// The step functions below are templates on their parameter view P: BfsParams
+// (one partition: the whole core, the whole grid) or PartView (one partition of
+// the 1D core partition, et_bfs_part_body: its owned visited words, its CTA
+// group, row segments restricted to its owned neighbours). These accessors fold
+// to the single-partition expressions for BfsParams.
+__device__ __forceinline__ uint64_t wlo_of(const BfsParams&) { return 0; }
+__device__ __forceinline__ uint32_t whi_of(const BfsParams& p) { return p.nwords; }
+__device__ __forceinline__ unsigned cta_of(const BfsParams&) { return blockIdx.x; }
+__device__ __forceinline__ unsigned ncta_of(const BfsParams&) { return gridDim.x; }
+__device__ __forceinline__ uint32_t seg_off(const BfsParams&, uint32_t) { return 0; }
 
 struct WarpSmem {
   uint32_t cbuf[kCbuf];     // staged claims (top-down); with win: deferred misses (bottom-up)
@@ -118,8 +130,8 @@ __device__ void grid_sync_add(unsigned long long* bar, Smem& sm, unsigned long l
 // Append the staged claims to the next list (vertices without core edges skipped).
 // kStaged: the claims' core degrees are staged in cdeg (else read from cmeta,
 // all loads of the batch in flight at once).
-template <bool kStaged>
-__device__ void flush_claims(const BfsParams& p, const uint32_t* cbuf, const int32_t* cdeg,
+template <bool kStaged, class P>
+__device__ void flush_claims(const P& p, const uint32_t* cbuf, const int32_t* cdeg,
                              uint32_t ncl, uint32_t* qv_out, uint64_t* qp_out,
                              unsigned long long* slot) {
   const unsigned lane = threadIdx.x & 31;
@@ -175,15 +187,15 @@ __device__ __forceinline__ uint32_t win_search(const int32_t* win, int32_t rel) 
 // counted after the level by scout_pass), 1 list (flush reads the degrees), 2 list with every
 // target's degrees fetched alongside its visited word (early levels, where most
 // targets are unvisited; after bottom-up most are visited and mode 1 is used).
-template <int kMode, bool kLarge>
-__device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const uint32_t* qv,
+template <int kMode, bool kLarge, class P>
+__device__ void td_step(const P& p, uint32_t* cbuf, int32_t* win, const uint32_t* qv,
                         const uint64_t* qp, uint64_t nq, uint64_t ne, uint32_t* qv_out,
                         uint64_t* qp_out, uint32_t* fnext, unsigned long long* slot,
                         int32_t dnext, unsigned long long& scout_acc,
                         unsigned long long& claims_acc, uint32_t root) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)wib * gridDim.x + blockIdx.x;  // CTA-minor: spread over SMs
-  const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
+  const uint64_t gw = (uint64_t)wib * ncta_of(p) + cta_of(p);  // CTA-minor: spread over SMs
+  const uint64_t nw = (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   const uint64_t nu = (ne + kTdChunk - 1) / kTdChunk;
   for (uint64_t g0 = gw, gn = 1; g0 < nu;) {
@@ -220,7 +232,13 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
           win[k] = wv;
         }
         __syncwarp();
-        inext = i + win_search(win, kTdChunk);
+        // the row holding the next chunk's first edge; a chunk of 128 one-edge
+        // rows ends exactly where row i + 128 starts, one past the window
+        const uint32_t kk = win_search(win, kTdChunk);
+        inext = i + kk;
+        if (kk == kTdChunk - 1 && win[kk] < static_cast<int32_t>(kTdChunk) && inext + 1 < nq &&
+            qp[inext + 1] <= e1)
+          inext += 1;
       } else {
         inext = iend == e1 ? i + 1 : i;
       }
@@ -229,7 +247,7 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
       bool cl[kEpl];
       if (single) {  // one row: its vertex and row start once for the chunk
         const uint32_t uu = root != kNone32 ? root : qv[i];
-        const uint64_t base = p.crow[uu] + (e0 - qi);
+        const uint64_t base = p.crow[uu] + seg_off(p, uu) + (e0 - qi);
 #pragma unroll
         for (int j = 0; j < kEpl; ++j) {
           const uint32_t rel = lane + 32 * j;
@@ -251,7 +269,7 @@ __device__ void td_step(const BfsParams& p, uint32_t* cbuf, int32_t* win, const 
           uint32_t col = kNone32;
           if (u[j] != kNone32) {
             const uint64_t vs = w[j] == 0 ? qi : e0 + static_cast<uint64_t>(max(win[w[j]], 0));
-            col = p.ccol[p.crow[u[j]] + (e0 + rel - vs)];
+            col = p.ccol[p.crow[u[j]] + seg_off(p, u[j]) + (e0 + rel - vs)];
           }
           w[j] = col;
         }
@@ -519,22 +537,22 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
   __syncwarp();
 }
 
-template <int kU>
-__device__ void bu_step(const BfsParams& p, uint32_t* mbuf, const uint32_t* fcur,
+template <int kU, class P>
+__device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
                         uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot) {
   static_assert(32 * kU <= kMissCap, "one iteration's misses must fit the miss buffer");
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
+  const uint64_t gw = (uint64_t)cta_of(p) * (blockDim.x >> 5) + wib;
+  const uint64_t nw = (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
-  for (uint64_t w0 = gw * kU; w0 < p.nwords; w0 += nw * kU) {
+  for (uint64_t w0 = wlo_of(p) + gw * kU; w0 < whi_of(p); w0 += nw * kU) {
     uint32_t vis[kU];
     bool any = false;
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
-      vis[k] = w0 + k < p.nwords ? p.visited[w0 + k] : ~0u;
+      vis[k] = w0 + k < whi_of(p) ? p.visited[w0 + k] : ~0u;
       any |= vis[k] != ~0u;
     }
     if (!any) continue;
@@ -584,15 +602,15 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
                         uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  const uint64_t nw = (uint64_t)(gridDim.x * blockDim.x) >> 5;
+  const uint64_t gw = (uint64_t)cta_of(p) * (blockDim.x >> 5) + wib;
+  const uint64_t nw = (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
   // A warp sweeps kSweep visited words with one coalesced load (lane = word)
   // and works through the words with unvisited vertices kBuU at a time, so
   // late levels (few unvisited left) skip full words without a round trip each.
-  for (uint64_t b0 = gw * kSweep; b0 < p.nwords; b0 += nw * kSweep) {
-    const uint32_t mine = lane < kSweep && b0 + lane < p.nwords ? p.visited[b0 + lane] : ~0u;
+  for (uint64_t b0 = wlo_of(p) + gw * kSweep; b0 < whi_of(p); b0 += nw * kSweep) {
+    const uint32_t mine = lane < kSweep && b0 + lane < whi_of(p) ? p.visited[b0 + lane] : ~0u;
     unsigned todo = __ballot_sync(0xffffffffu, mine != ~0u);
     while (todo) {
       uint32_t vis[kBuU], wi[kBuU];
@@ -1061,6 +1079,390 @@ __global__ void __launch_bounds__(B, 1) et_bfs_kernel(BfsParams p) {
   et_bfs_body<(B == 1024)>(p);
 }
 
+// ============================================================================
+// (5) The 1D core partition (bfs_part.cuh): partition k owns the core ids
+// [lo_k, hi_k) (Eq. 1 of the paper, proj/src/preprocess.cpp:77, word aligned)
+// and the trees anchored there. The level loop is the single-partition one,
+// run by each partition over its own work with the same step functions:
+//   bottom-up  its owned visited words (bu_step / bu_sweep on a PartView);
+//   top-down   every frontier row restricted to its owned neighbours (rows
+//              are sorted: one segment per row, seg[u]), atomic-free claims
+//              (td_step<3>), the frontier list built per level from the
+//              replicated frontier bitmap;
+// claims touch only partition-local memory (owned visited and next-frontier
+// words). At the end of a level each partition pushes its owned next-frontier
+// words to every peer's replica — the per-level frontier-bitmap allgather,
+// fused into the kernel as coalesced stores over peer memory (NVLink) or local
+// memory (all partitions on one GPU) — counting its claims and α/β scout in the
+// same pass, and one barrier over all partitions adds the partials into every
+// partition's counters, so every partition takes the same α/β decision.
+// ============================================================================
+
+// What the step functions read, for one partition: the shared core graph and
+// result array, the partition's own visited replica, its CTA group, its owned
+// words and the owned segment of every core row.
+struct PartView {
+  const uint64_t* crow;
+  const uint32_t* ccol;
+  const uint32_t* cfirst;
+  const uint32_t* degn;
+  const uint2* cmeta;
+  uint2* dp;
+  uint32_t* visited;
+  const uint2* seg;
+  uint32_t nc, nwords, wlo, whi;
+  unsigned cta, ncta;
+  unsigned long long* wstamp;  // (ETB_WARP_STAMPS diagnostics: unused here)
+  int32_t wdepth;
+};
+__device__ __forceinline__ uint64_t wlo_of(const PartView& v) { return v.wlo; }
+__device__ __forceinline__ uint32_t whi_of(const PartView& v) { return v.whi; }
+__device__ __forceinline__ unsigned cta_of(const PartView& v) { return v.cta; }
+__device__ __forceinline__ unsigned ncta_of(const PartView& v) { return v.ncta; }
+__device__ __forceinline__ uint32_t seg_off(const PartView& v, uint32_t u) { return v.seg[u].x; }
+
+// Exchange-block counters (per partition): two parities of {four level slots
+// of [claims, scout, grab, -], conversion counters at [16], [17]}; [62] cross
+// barriers completed by earlier launches, [63] launches completed. Launch k
+// uses parity k & 1 and clears the other parity at its start: every peer's add
+// into that parity happened in launch k - 1, before its last cross barrier.
+constexpr int kXkSlot = 62, kLaunchSlot = 63;
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Barrier over the `n` CTAs of one partition's group (this GPU's memory only).
+__device__ __forceinline__ void group_sync(unsigned long long* bar, unsigned n) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long old = atom_add_release(bar, 1ull);
+    const unsigned long long target = (old / n + 1) * n;
+    const long long t0 = clock64();
+    while (ld_acquire(bar) < target)
+      if (clock64() - t0 > 40000000000ll) __trap();
+  }
+  __syncthreads();
+}
+
+// The level barrier over every CTA of every partition: block-reduce (a, b),
+// add them into every partition's counters at `off`, release this CTA's writes
+// (owned results, pushed replica words) and arrive at every partition's
+// counter; complete when all nparts x group CTAs arrived (`target` counts
+// arrivals since the counters were created). Thread 0 then reads the n totals
+// at rd once for the CTA (sm.tot).
+__device__ void part_level_sync(const PartParams& pp, uint32_t part, unsigned par, Smem& sm,
+                                unsigned long long a, unsigned long long b, uint32_t off,
+                                unsigned long long target, const unsigned long long* rd, int n) {
+  const bool sys = pp.system_scope;
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    sm.red[0][wib] = a;
+    sm.red[1][wib] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned nwb = blockDim.x >> 5;
+    a = warp_sum(lane < nwb ? sm.red[0][lane] : 0ull);
+    b = warp_sum(lane < nwb ? sm.red[1][lane] : 0ull);
+    if (lane == 0) {
+      for (uint32_t q = 0; q < pp.nparts; ++q) {
+        unsigned long long* c = pp.parts[q].ctr + 32 * par + off;
+        if (sys) {
+          if (a) atomicAdd_system(&c[0], a);
+          if (b) atomicAdd_system(&c[1], b);
+        } else {
+          if (a) atomicAdd(&c[0], a);
+          if (b) atomicAdd(&c[1], b);
+        }
+      }
+      if (sys) __threadfence_system(); else __threadfence();
+      for (uint32_t q = 0; q < pp.nparts; ++q) {
+        if (sys) atomicAdd_system(pp.parts[q].arrive, 1ull);
+        else atomicAdd(pp.parts[q].arrive, 1ull);
+      }
+      const unsigned long long* me_arrive = pp.parts[part].arrive;
+      const long long t0 = clock64();
+      while ((sys ? ld_acquire_sys(me_arrive) : ld_acquire(me_arrive)) < target)
+        if (clock64() - t0 > 40000000000ll) __trap();
+      for (int k = 0; k < n; ++k) sm.tot[k] = ld_volatile(&rd[k]);
+    }
+  }
+  __syncthreads();
+}
+
+// The frontier bitmap (replica, all words) -> this partition's list of
+// frontier vertices with a non-empty owned segment and the prefix of the
+// segment lengths (as convert_step, with seg[v].y for the core degree).
+__device__ void part_convert(const PartView& v, const uint32_t* fcur, uint32_t* qv, uint64_t* qp,
+                             unsigned long long* cslot) {
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)wib * v.ncta + v.cta;
+  const uint64_t nw = (uint64_t)(v.ncta * blockDim.x) >> 5;
+  for (uint64_t w0 = gw * 32; w0 < v.nwords; w0 += nw * 32) {
+    const uint64_t wi = w0 + lane;
+    const uint32_t bits = wi < v.nwords ? fcur[wi] : 0u;
+    uint32_t cnt = 0, edges = 0;
+    for (uint32_t b = bits; b; b &= b - 1) {
+      const uint32_t d = v.seg[static_cast<uint32_t>(wi * 32 + __ffs(b) - 1)].y;
+      cnt += d != 0;
+      edges += d;
+    }
+    const uint32_t vin = warp_incl_scan(cnt);
+    const uint32_t vtot = __shfl_sync(0xffffffffu, vin, 31);
+    if (vtot == 0) continue;
+    const unsigned long long ein = warp_incl_scan64(edges);
+    const unsigned long long etot = __shfl_sync(0xffffffffu, ein, 31);
+    unsigned long long old = 0;
+    if (lane == 31) old = atomicAdd(cslot, ((unsigned long long)vtot << kItemShift) | etot);
+    old = __shfl_sync(0xffffffffu, old, 31);
+    uint64_t vpos = (old >> kItemShift) + vin - cnt, epos = (old & kItemMask) + ein - edges;
+    for (uint32_t b = bits; b; b &= b - 1) {
+      const uint32_t x = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
+      const uint32_t d = v.seg[x].y;
+      if (!d) continue;
+      qv[vpos] = x;
+      qp[vpos] = epos;
+      ++vpos;
+      epos += d;
+    }
+  }
+}
+
+// The allgather of one level: this partition's owned next-frontier words, 32
+// per warp iteration (one coalesced 128-byte store per peer), into every
+// peer's replica of that ring slot; with kCount also the level's claims
+// (popcount) and α/β scout (Σ full degree, coalesced: lane = vertex).
+template <bool kCount>
+__device__ void part_push(const PartParams& pp, uint32_t part, const PartView& v, uint32_t ring,
+                          const uint32_t* fnext, unsigned long long& claims,
+                          unsigned long long& scout) {
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)wib * v.ncta + v.cta;
+  const uint64_t nw = (uint64_t)(v.ncta * blockDim.x) >> 5;
+  for (uint64_t w0 = v.wlo + gw * 32; w0 < v.whi; w0 += nw * 32) {
+    const uint64_t wi = w0 + lane;
+    const bool in = wi < v.whi;
+    const uint32_t f = in ? __ldcg(&fnext[wi]) : 0u;
+    for (uint32_t q = 0; q < pp.nparts; ++q) {
+      if (q == part || !in) continue;
+      const PartDev& pq = pp.parts[q];
+      uint32_t* dst = ring == 0 ? pq.fb0 : (ring == 1 ? pq.fb1 : pq.fb2);
+      dst[wi] = f;
+    }
+    if (kCount) {
+      claims += __popc(f);
+      if (__any_sync(0xffffffffu, f != 0)) {
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t bits = __shfl_sync(0xffffffffu, f, j);
+          if ((bits >> lane) & 1u) scout += v.degn[(w0 + j) * 32 + lane];
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ bool owns(const PartDev& me, uint32_t v) {
+  return (v >= me.lo && v < me.hi) || (v >= me.tlo && v < me.thi) || (v >= me.zlo && v < me.zhi);
+}
+
+template <bool kLarge>
+__device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const BfsParams& p = pp.base;
+  const unsigned gsize = gridDim.x / pp.local_parts;
+  const unsigned cta = blockIdx.x % gsize;
+  const uint32_t part = pp.first_part + blockIdx.x / gsize;
+  const PartDev& me = pp.parts[part];
+  const uint64_t gtid = (uint64_t)cta * blockDim.x + threadIdx.x;
+  const uint64_t gthreads = (uint64_t)gsize * blockDim.x;
+  const bool lead = part == 0 && cta == 0 && threadIdx.x == 0;
+  const bool stats = p.level_claims && lead;
+  PartView v;
+  v.crow = p.crow;
+  v.ccol = p.ccol;
+  v.cfirst = p.cfirst;
+  v.degn = p.degn;
+  v.cmeta = p.cmeta;
+  v.dp = p.dp;
+  v.visited = me.visited;
+  v.seg = me.seg;
+  v.nc = p.nc;
+  v.nwords = p.nwords;
+  v.wlo = me.lo >> 5;
+  v.whi = static_cast<uint32_t>((static_cast<uint64_t>(me.hi) + 31) >> 5);
+  v.cta = cta;
+  v.ncta = gsize;
+  v.wstamp = nullptr;
+  v.wdepth = -1;
+  const unsigned long long launch = me.ctr[kLaunchSlot];
+  const unsigned par = static_cast<unsigned>(launch & 1u);
+  unsigned long long* const ctr = me.ctr + 32 * par;
+  unsigned long long xk = me.ctr[kXkSlot];  // cross barriers completed by earlier launches
+  const unsigned long long per_barrier = static_cast<unsigned long long>(pp.nparts) * gsize;
+  const uint32_t start = p.start;
+  const bool run_core = start != kNone32;
+  if (stats) p.level_claims[256] = gtimer();
+
+  // ---- init: this partition's own memory only (no cross barrier) -------------
+  if (gtid < 18) me.ctr[32 * (par ^ 1u) + gtid] = 0;
+  {
+    const uint32_t tail = p.nc & 31u;
+    const uint32_t sw = run_core ? start >> 5 : kNone32, sb = run_core ? 1u << (start & 31) : 0u;
+    for (uint64_t i = gtid; i < p.nwords; i += gthreads) {
+      me.fb0[i] = i == sw ? sb : 0u;  // the whole replica: a bottom-up level 0 probes it
+      if (i >= v.wlo && i < v.whi) {
+        uint32_t vis = i == sw ? sb : 0u;
+        if (i == p.nwords - 1 && tail) vis |= ~0u << tail;
+        me.visited[i] = vis;
+        me.fb1[i] = 0;
+      }
+    }
+  }
+  if (run_core && gtid == 0 && start >= me.lo && start < me.hi)
+    p.dp[start] = make_uint2(static_cast<uint32_t>(p.base_depth), p.start_parent);
+  group_sync(me.bar, gsize);
+  if (stats) p.level_claims[257] = gtimer();
+
+  uint32_t L = 0;
+  if (run_core) {
+    uint32_t* F[3] = {me.fb0, me.fb1, me.fb2};
+    unsigned long long frontier = 1, scout = p.degn[start], awake = 0, prev = 0, reached = 1;
+    double etc = p.edges_to_check;
+    bool bu = p.bottom_up_only || (!p.top_down_only && (double)scout > etc / p.alpha);
+    if (bu) awake = frontier;
+    for (;;) {
+      uint32_t* fcur = F[L % 3];
+      uint32_t* fnext = F[(L + 1) % 3];
+      uint32_t* fzero = F[(L + 2) % 3];
+      unsigned long long* slot = ctr + (L & 3) * 4;
+      for (uint64_t i = v.wlo + gtid; i < v.whi; i += gthreads) fzero[i] = 0;  // owned words
+      if (gtid == 0) {
+        ctr[((L + 2) & 3) * 4 + 0] = 0;
+        ctr[((L + 2) & 3) * 4 + 1] = 0;
+        ctr[((L + 2) & 3) * 4 + 2] = 0;
+        ctr[((L + 2) & 3) * 4 + 3] = 0;
+        ctr[16 + ((L + 1) & 1)] = 0;
+      }
+      if (stats && L < 255) p.trace[L] = bu ? 'b' : 't';
+      const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
+      unsigned long long claims_acc = 0, scout_acc = 0;
+      uint32_t* mb = sm.w[threadIdx.x >> 5].cbuf;
+      if (bu) {
+        prev = awake;
+        if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
+          bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
+        else
+          bu_step<kLarge ? kBuU : kBuUSmall>(v, mb, fcur, fnext, dnext, claims_acc, nullptr,
+                                             nullptr, nullptr);
+        group_sync(me.bar, gsize);  // the owned next words are final
+        unsigned long long none = 0;
+        part_push<false>(pp, part, v, (L + 1) % 3, fnext, none, none);
+      } else {
+        etc -= (double)scout;
+        uint64_t nq = 0, ne = 0;
+        if (L == 0) {
+          ne = me.seg[start].y;  // the start's owned row segment, no list
+          nq = ne != 0;
+        } else {
+          unsigned long long* cslot = ctr + 16 + (L & 1);
+          part_convert(v, fcur, me.qv, me.qp, cslot);
+          group_sync(me.bar, gsize);
+          if (threadIdx.x == 0) sm.tot[2] = ld_volatile(cslot);
+          __syncthreads();
+          nq = sm.tot[2] >> kItemShift;
+          ne = sm.tot[2] & kItemMask;
+        }
+        td_step<3, kLarge>(v, mb, sm.w[threadIdx.x >> 5].win, me.qv, me.qp, nq, ne, nullptr,
+                           nullptr, fnext, slot, dnext, scout_acc, claims_acc,
+                           L == 0 ? start : kNone32);
+        group_sync(me.bar, gsize);
+        part_push<true>(pp, part, v, (L + 1) % 3, fnext, claims_acc, scout_acc);
+      }
+      ++xk;
+      part_level_sync(pp, part, par, sm, claims_acc, bu ? 0ull : scout_acc, (L & 3) * 4,
+                      xk * per_barrier, slot, 2);
+      const unsigned long long claims = sm.tot[0];
+      const unsigned long long scout_tot = sm.tot[1];
+      reached += claims;
+      if (stats) {
+        if (L < 254) p.level_claims[258 + L] = gtimer();
+        if (L < 256) p.level_claims[L] = claims;
+      }
+      ++L;
+      if (bu && p.bottom_up_only) {
+        if (claims == 0) break;  // run_block_search (bfs.cpp:295-305)
+      } else if (bu) {
+        awake = claims;
+        if (!(awake > 0 && (awake >= prev || (double)awake > (double)p.nc / p.beta))) {
+          bu = false;
+          frontier = awake;
+          scout = 1;
+        }
+      } else {
+        frontier = claims;
+        scout = scout_tot;
+      }
+      if (!bu) {
+        if (frontier == 0) break;
+        if (!p.top_down_only && (double)scout > etc / p.alpha) {
+          bu = true;
+          awake = frontier;
+        }
+      }
+      if (reached == p.reachable) {  // the start's component is exhausted (as et_bfs_body)
+        if (stats && L < 255) p.trace[L] = bu ? 'b' : 't';
+        if (stats && L < 256) p.level_claims[L] = 0;
+        if (stats && L < 254) p.level_claims[258 + L] = gtimer();
+        ++L;
+        break;
+      }
+    }
+  }
+  if (stats && p.nlevels) *p.nlevels = L;
+
+  // ---- owned core fill + owned tree replay + owned patch entries ---------------
+  for (uint64_t wi = v.wlo + gtid; wi < v.whi; wi += gthreads)
+    for (uint32_t un = ~me.visited[wi]; un; un &= un - 1) {
+      const uint64_t x = wi * 32 + __ffs(un) - 1;
+      p.dp[x] = make_uint2(kNone32, kNone32);
+    }
+  for (uint64_t tv = me.tlo + gtid; tv < me.thi; tv += gthreads) {
+    if (tv >= p.skip_lo && tv < p.skip_hi) continue;
+    const uint64_t t = tv - p.nc;
+    const uint32_t a = p.tanchor[t];
+    uint2 out = make_uint2(kNone32, kNone32);
+    if (a != kNone32 && test_bit(me.visited, a))
+      out = make_uint2(__ldcg(&p.dp[a].x) + p.tdepth[t], p.tsrc[t]);
+    p.dp[tv] = out;
+  }
+  for (uint64_t i = gtid; i < p.npatch; i += gthreads) {
+    const uint32_t x = p.patch[3 * i];
+    if (owns(me, x)) p.dp[x] = make_uint2(p.patch[3 * i + 1], p.patch[3 * i + 2]);
+  }
+#pragma unroll
+  for (int k = 0; k < kInlinePatch; ++k)
+    if (gtid == static_cast<uint64_t>(k) && static_cast<uint32_t>(k) < p.nipatch &&
+        owns(me, p.ipatch[3 * k]))
+      p.dp[p.ipatch[3 * k]] = make_uint2(p.ipatch[3 * k + 1], p.ipatch[3 * k + 2]);
+  if (cta == 0 && threadIdx.x == 0) {
+    me.ctr[kXkSlot] = xk;
+    me.ctr[kLaunchSlot] = launch + 1;
+  }
+  if (stats) p.level_claims[511] = gtimer();
+}
+
+template <int B>
+__global__ void __launch_bounds__(B, 1) et_bfs_part_kernel(const __grid_constant__ PartParams pp) {
+  et_bfs_part_body<(B == 1024)>(pp);
+}
+
 }  // namespace
 
 const void* kernel_for(int block) {
@@ -1074,6 +1476,13 @@ const void* kernel_for(int block) {
 // large-core kernel; at scale 26 the large-core kernel at 1024 threads runs
 // 471 us vs 476 at 896 and 578 for the small-core kernel.
 // ETB_BFS_BLOCK=640|1024 overrides (experiments).
+const void* part_kernel_for(int block) {
+  return block == kSmallBlock ? reinterpret_cast<const void*>(et_bfs_part_kernel<kSmallBlock>)
+                              : reinterpret_cast<const void*>(et_bfs_part_kernel<1024>);
+}
+
+size_t bfs_smem_bytes() { return sizeof(Smem); }
+
 int block_for(uint64_t nc) {
   if (const char* e = getenv("ETB_BFS_BLOCK")) {
     const int b = atoi(e);

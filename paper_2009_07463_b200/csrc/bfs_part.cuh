@@ -25,6 +25,9 @@
 namespace etb {
 
 constexpr int kMaxParts = 16;
+// u64 counters at the start of a partition's exchange block (bfs.cu: two
+// parities of level slots, launch bookkeeping); the arrival counter follows.
+constexpr uint64_t kCtrWords = 64;
 
 // Device-visible descriptor of one partition. Pointers must be valid on the
 // device running the kernel (own buffers, or IPC-mapped peer buffers; for a
@@ -38,7 +41,7 @@ struct PartDev {
   uint32_t* fb0;          // frontier replicas (all words) — exchange block
   uint32_t* fb1;
   uint32_t* fb2;
-  unsigned long long* ctr;     // level slots + cross-barrier bookkeeping — exchange block
+  unsigned long long* ctr;     // kCtrWords level / launch counters — exchange block
   unsigned long long* arrive;  // cross-partition barrier counter — exchange block
   unsigned long long* bar;     // group barrier counter (local)
   uint32_t* qv;                // top-down frontier list (this partition's chunking)
@@ -65,7 +68,7 @@ struct PartState {
   DevBuf<unsigned char> xblock;     // exchange blocks, one per local partition
   uint64_t xbytes = 0;              // bytes per exchange block
   DevBuf<unsigned long long> bar;
-  int grid = 0;
+  int grid = 0, block = 0;
   std::vector<void*> peer_maps;     // IPC-opened peer exchange blocks
   ~PartState();
 };
@@ -76,5 +79,11 @@ void part_bounds(const DevLayout& L, uint32_t nparts, std::vector<PartDev>& out)
 void part_build(const DevLayout& L, PartState& P, uint32_t nparts, uint32_t first, uint32_t local,
                 cudaStream_t s);
 void part_launch(const PartParams& p, const PartState& P, cudaStream_t s);
+
+// bfs.cu: the partitioned kernel for a block size, the shared-memory size of
+// both kernels, and the block size for a core size.
+const void* part_kernel_for(int block);
+size_t bfs_smem_bytes();
+int block_for(uint64_t nc);
 
 }  // namespace etb

@@ -907,6 +907,14 @@ int etb_layout_partition(etb_layout* h, uint32_t parts) {
   });
 }
 
+int etb_layout_partition_scope(etb_layout* h, int system_scope) {
+  return guarded([&] {
+    need(h, "etb_layout_partition_scope");
+    if (!h->P) throw std::invalid_argument("etb_layout_partition_scope: layout is not partitioned");
+    h->system_scope = system_scope ? 1 : 0;
+  });
+}
+
 int etb_layout_partition_bounds(const etb_layout* h, uint32_t parts, uint64_t* bounds) {
   return guarded([&] {
     need(h, "etb_layout_partition_bounds");
@@ -974,7 +982,7 @@ int etb_mp_connect(etb_layout* h, const void* blobs) {
       d.fb2 = d.fb1 + words;
       d.ctr = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(base) +
                                                     ((3 * words * 4 + 255) / 256) * 256);
-      d.arrive = d.ctr + 32;
+      d.arrive = d.ctr + etb::kCtrWords;
     }
     ETB_CUDA(cudaMemcpyAsync(P.d_parts.get(), P.h_parts.data(), P.nparts * sizeof(etb::PartDev),
                              cudaMemcpyHostToDevice, h->stream));

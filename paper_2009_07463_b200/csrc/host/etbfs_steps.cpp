@@ -2,7 +2,9 @@
 // proj/include/etbfs/bfs.hpp:66-120) over etb_steps_run (csrc/steps.cu). The
 // caller's FrontierState words and parent vector go to the device and back
 // around each call; a driver keeps them resident for all of its levels. The
-// device graph is cached for the last CsrGraph seen (keyed by its storage).
+// device graph is cached for the last CsrGraph seen, keyed by its content
+// (rows and columns), so a graph rebuilt at the same addresses or edited in
+// place is uploaded again.
 #include <bit>
 #include <memory>
 #include <mutex>
@@ -12,6 +14,7 @@
 
 #include "etbfs/bfs.hpp"
 #include "etbfs_cuda.h"
+#include "etbfs_hash.hpp"
 
 namespace etbfs {
 namespace {
@@ -24,8 +27,7 @@ void check(int rc) {
 }
 
 struct Cached {
-  const void* rows = nullptr;
-  const void* cols = nullptr;
+  uint64_t key = 0;
   uint64_t n = 0, nnz = 0;
   etb_graph* g = nullptr;
   ~Cached() {
@@ -38,8 +40,9 @@ Cached g_cache;
 etb_graph* device_graph(const CsrGraph& graph) {
   if (graph.row_offsets.size() != graph.vertex_count + 1)
     throw std::invalid_argument("etbfs: CsrGraph row_offsets size mismatch");
-  if (g_cache.g && g_cache.rows == graph.row_offsets.data() &&
-      g_cache.cols == graph.col_indices.data() && g_cache.n == graph.vertex_count &&
+  const uint64_t key = detail::hash_vec(graph.col_indices,
+                                       detail::hash_vec(graph.row_offsets, graph.vertex_count));
+  if (g_cache.g && g_cache.key == key && g_cache.n == graph.vertex_count &&
       g_cache.nnz == graph.col_indices.size())
     return g_cache.g;
   etb_graph* h = nullptr;
@@ -47,8 +50,7 @@ etb_graph* device_graph(const CsrGraph& graph) {
                            graph.col_indices.data(), &h));
   if (g_cache.g) etb_graph_free(g_cache.g);
   g_cache = {};
-  g_cache.rows = graph.row_offsets.data();
-  g_cache.cols = graph.col_indices.data();
+  g_cache.key = key;
   g_cache.n = graph.vertex_count;
   g_cache.nnz = graph.col_indices.size();
   g_cache.g = h;

@@ -172,6 +172,7 @@ def lib() -> C.CDLL:
     sig("etb_debug_warp_stamps", vp, u64, C.c_int32, vp, u64, C.POINTER(C.c_uint32))
     sig("etb_layout_partition", vp, C.c_uint32)
     sig("etb_layout_partition_bounds", vp, C.c_uint32, vp)
+    sig("etb_layout_partition_scope", vp, C.c_int)
     sig("etb_mp_blob_size")
     sig("etb_mp_export", vp, C.c_uint32, C.c_uint32, vp)
     sig("etb_mp_connect", vp, vp)
@@ -376,10 +377,14 @@ class EtLayout:
         return row, col[:m]
 
 
-def partition(cg: "EtLayout", parts: int) -> None:
+def partition(cg: "EtLayout", parts: int, system_scope: bool = False) -> None:
     """Run subsequent traversals of cg with the 1D core partition (parts >= 2) on
-    this device, or back on the single-partition kernel (parts <= 1)."""
+    this device, or back on the single-partition kernel (parts <= 1).
+    system_scope runs the exchange with the multi-GPU (system-scope) fences,
+    atomics and polls."""
     _check(lib().etb_layout_partition(cg.handle, int(parts)))
+    if parts > 1 and system_scope:
+        _check(lib().etb_layout_partition_scope(cg.handle, 1))
 
 
 def partition_bounds(cg: "EtLayout", parts: int) -> np.ndarray:

@@ -9,6 +9,7 @@ import pytest
 import oracle as O
 import paper_2009_07463_b200 as eb
 from conftest import edges_of, levels_list
+from paper_2009_07463_b200 import etbfs as E
 from paper_2009_07463_b200.etbfs import (bfs_device, result_download, result_traversed_edges,
                                          time_roots)
 
@@ -350,3 +351,20 @@ def test_bfs_compact_outputs(kron16):
             assert np.array_equal(par, p2), (root, pinned)
             assert np.array_equal(dep, d2), (root, pinned)
             assert E.result_validate(cg, s)["passed"], (root, pinned)
+
+
+@pytest.mark.slow
+def test_whole_graph_top_down_s20():
+    """Top-down only on the whole graph (every vertex in the traversed block, as
+    bfs_top_down / run_benchmark(kTopDown) use it): frontier lists full of
+    one-edge rows, so 128-edge chunks made of 128 rows occur — the next chunk
+    then starts exactly one row past the merge-path window."""
+    csr = eb.generate_graph(scale=20, edgefactor=16, seed=1)
+    n = csr.vertex_count
+    ocsr = O.OracleCsr(n, O.oracle_generate(20, 16, 1))
+    cg = eb.relayout_csr(csr, types=np.zeros(n, np.uint8), mh=-1)
+    for parts in (1, 4):
+        E.partition(cg, parts)
+        for root in ocsr.select_roots(16, 2):
+            check_root(cg, ocsr, int(root), kernel=eb.CoreKernel.TOP_DOWN)
+    E.partition(cg, 1)

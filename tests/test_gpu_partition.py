@@ -32,7 +32,7 @@ def test_partitioned_corpus_all_starts(corpus):
         for mh in (-1, 0):
             cg = eb.relayout_csr(csr, mh=mh)
             for parts in (2, 3, 5):
-                E.partition(cg, parts)
+                E.partition(cg, parts, system_scope=parts == 3)
                 for st in range(g["n"]):
                     root = int(cg.new2old[st])
                     check_root(cg, ocsr, root)
@@ -40,13 +40,17 @@ def test_partitioned_corpus_all_starts(corpus):
             E.partition(cg, 1)
 
 
-@pytest.mark.parametrize("parts", [2, 4, 8])
-def test_partitioned_s16_64_roots(kron16, parts):
+@pytest.mark.parametrize("parts,sys_scope", [(2, False), (4, False), (8, False), (2, True),
+                                            (8, True)])
+def test_partitioned_s16_64_roots(kron16, parts, sys_scope):
+    """sys_scope: the multi-GPU code path (system-scope fences, counter atomics
+    and barrier polls, as between GPUs over NVLink) run by the one-launch
+    emulation, so it executes without kernels waiting on other launches."""
     k = kron16
     csr = eb.generate_graph(scale=16, edgefactor=16, seed=1)
     ocsr = O.OracleCsr(1 << 16, O.oracle_generate(16, 16, 1))
     cg = eb.relayout_csr(csr, mh=-1)
-    E.partition(cg, parts)
+    E.partition(cg, parts, system_scope=sys_scope)
     for i, root in enumerate(k["roots"]):
         r = check_root(cg, ocsr, int(root))
         assert r.stats.direction_trace == k["layout"]["-1"]["traces"][i]
