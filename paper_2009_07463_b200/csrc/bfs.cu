@@ -1309,6 +1309,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   const uint32_t start = p.start;
   const bool run_core = start != kNone32;
   if (stats) p.level_claims[256] = gtimer();
+  if (p.bstamp && threadIdx.x == 0) p.bstamp[62 * gridDim.x + blockIdx.x] = gtimer();
 
   // ---- init: this partition's own memory only (no cross barrier) -------------
   if (gtid < 18) me.ctr[32 * (par ^ 1u) + gtid] = 0;
@@ -1361,6 +1362,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         else
           bu_step<kLarge ? kBuU : kBuUSmall>(v, mb, fcur, fnext, dnext, claims_acc, nullptr,
                                              nullptr, nullptr);
+        if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
         group_sync(me.bar, gsize);  // the owned next words are final
         unsigned long long none = 0;
         part_push<false>(pp, part, v, (L + 1) % 3, fnext, none, none);
@@ -1382,6 +1384,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         td_step<3, kLarge>(v, mb, sm.w[threadIdx.x >> 5].win, me.qv, me.qp, nq, ne, nullptr,
                            nullptr, fnext, slot, dnext, scout_acc, claims_acc,
                            L == 0 ? start : kNone32);
+        if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
         group_sync(me.bar, gsize);
         part_push<true>(pp, part, v, (L + 1) % 3, fnext, claims_acc, scout_acc);
       }
@@ -1427,20 +1430,46 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   }
   if (stats && p.nlevels) *p.nlevels = L;
 
-  // ---- owned core fill + owned tree replay + owned patch entries ---------------
-  for (uint64_t wi = v.wlo + gtid; wi < v.whi; wi += gthreads)
-    for (uint32_t un = ~me.visited[wi]; un; un &= un - 1) {
-      const uint64_t x = wi * 32 + __ffs(un) - 1;
-      p.dp[x] = make_uint2(kNone32, kNone32);
+  // ---- owned tree replay + owned core fill + owned patch entries ---------------
+  // (as et_bfs_body's final phase over the partition's ranges: four tree
+  // entries in flight per thread, and a warp clears the unreached vertices of
+  // 32 owned visited words with coalesced 256-byte stores)
+  const uint64_t tlo = me.tlo, nto = me.thi - me.tlo;
+  for (uint64_t t0 = gtid; t0 < nto; t0 += 4 * gthreads) {
+    uint32_t a[4], td[4], ts[4], vb[4], da[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t tv = tlo + t0 + k * gthreads;
+      const bool in = t0 + k * gthreads < nto && !(tv >= p.skip_lo && tv < p.skip_hi);
+      const uint64_t t = tv - p.nc;
+      a[k] = in ? p.tanchor[t] : kNone32 - 1;
+      td[k] = in ? p.tdepth[t] : 0u;
+      ts[k] = in ? p.tsrc[t] : 0u;
     }
-  for (uint64_t tv = me.tlo + gtid; tv < me.thi; tv += gthreads) {
-    if (tv >= p.skip_lo && tv < p.skip_hi) continue;
-    const uint64_t t = tv - p.nc;
-    const uint32_t a = p.tanchor[t];
-    uint2 out = make_uint2(kNone32, kNone32);
-    if (a != kNone32 && test_bit(me.visited, a))
-      out = make_uint2(__ldcg(&p.dp[a].x) + p.tdepth[t], p.tsrc[t]);
-    p.dp[tv] = out;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool ok = a[k] < kNone32 - 1;
+      vb[k] = ok ? test_bit(me.visited, a[k]) : 0u;
+      da[k] = ok ? __ldcg(&p.dp[a[k]].x) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (a[k] == kNone32 - 1) continue;  // out of range or inside the start's tree
+      p.dp[tlo + t0 + k * gthreads] =
+          vb[k] ? make_uint2(da[k] + td[k], ts[k]) : make_uint2(kNone32, kNone32);
+    }
+  }
+  {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t gw = gtid >> 5, nw = gthreads >> 5;
+    for (uint64_t w0 = v.wlo + gw * 32; w0 < v.whi; w0 += nw * 32) {
+      const uint32_t un = w0 + lane < v.whi ? ~me.visited[w0 + lane] : 0u;
+      for (unsigned m = __ballot_sync(0xffffffffu, un != 0); m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        if ((__shfl_sync(0xffffffffu, un, j) >> lane) & 1u)
+          p.dp[(w0 + j) * 32 + lane] = make_uint2(kNone32, kNone32);
+      }
+    }
   }
   for (uint64_t i = gtid; i < p.npatch; i += gthreads) {
     const uint32_t x = p.patch[3 * i];
@@ -1451,6 +1480,10 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
     if (gtid == static_cast<uint64_t>(k) && static_cast<uint32_t>(k) < p.nipatch &&
         owns(me, p.ipatch[3 * k]))
       p.dp[p.ipatch[3 * k]] = make_uint2(p.ipatch[3 * k + 1], p.ipatch[3 * k + 2]);
+  if (p.bstamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) p.bstamp[63 * gridDim.x + blockIdx.x] = gtimer();
+  }
   if (cta == 0 && threadIdx.x == 0) {
     me.ctr[kXkSlot] = xk;
     me.ctr[kLaunchSlot] = launch + 1;

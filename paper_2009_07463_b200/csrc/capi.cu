@@ -829,9 +829,9 @@ int etb_debug_block_stamps(etb_layout* h, uint64_t start, uint64_t* out, uint64_
                            uint32_t* grid, uint32_t* levels) {
   return guarded([&] {
     need(h, "etb_debug_block_stamps");
-    if (h->P) throw std::invalid_argument("etb_debug_block_stamps: single-partition kernel only");
     ETB_CUDA(cudaSetDevice(h->device));
-    const uint64_t g = static_cast<uint64_t>(h->S.grid);
+    // partitioned layouts: CTA c belongs to partition c / (grid / partitions)
+    const uint64_t g = static_cast<uint64_t>(h->P ? h->P->grid : h->S.grid);
     etb::DevBuf<unsigned long long> st(64 * g);
     ETB_CUDA(cudaMemsetAsync(st.get(), 0, 64 * g * 8, h->stream));
     run_bfs(h, start, nullptr, true, nullptr, st.get());

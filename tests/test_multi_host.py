@@ -74,3 +74,50 @@ def test_blob_exchange_gloo_world2():
         assert p.exitcode == 0
     for r in range(2):
         assert got[r] == [bytes([0]) * 8, bytes([1]) * 9]
+
+
+def _merge_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2009_07463_b200.multi import merge_owned
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, nc, nt = 200, 96, 60
+    rng = np.random.default_rng(7)
+    anchor = np.concatenate([np.sort(rng.integers(0, nc, nt - 5)), np.full(5, 0xFFFFFFFF)])
+    b = partition_bounds(nc, nt, n, anchor.astype(np.uint64), world)
+    truth = rng.integers(-2**62, 2**62, n, dtype=np.int64)
+    truth[::7] = -1  # unreached entries are all ones
+    # junk outside the owned ranges, the owner's values inside them
+    mine = np.zeros(n, bool)
+    for lo, hi in ((b[rank, 0], b[rank, 1]), (b[rank, 2], b[rank, 3]), (b[rank, 4], b[rank, 5])):
+        mine[int(lo):int(hi)] = True
+    local = torch.from_numpy(np.where(mine, truth, 999).astype(np.int64))
+    full = merge_owned(local, b[rank], dist)
+    q.put((rank, bool((full.numpy() == truth).all())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_merge_owned_result_gloo_world2():
+    """multi.merge_owned (bench.py's multi-GPU validation): each rank holds only
+    its owned slices; summing the masked slices over ranks gives every rank the
+    whole result, negative (unreached) entries included."""
+    import multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_merge_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: True, 1: True}
