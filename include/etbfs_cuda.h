@@ -215,9 +215,12 @@ int etb_layout_partition(etb_layout* L, uint32_t parts);
  * 0 = device scope, as between partitions sharing one GPU (the default of
  * etb_layout_partition). Lets the one-GPU emulation run the multi-GPU code path. */
 int etb_layout_partition_scope(etb_layout* L, int system_scope);
-/* Partition k's owned ranges: bounds[6k..6k+5] = core lo, hi, tree lo, hi,
- * isolated lo, hi (relaid ids). */
-int etb_layout_partition_bounds(const etb_layout* L, uint32_t parts, uint64_t* bounds);
+/* The partition owning every relaid vertex among `parts` (owner: n u32): core
+ * vertex v belongs to partition (v >> 8) mod parts (256-vertex blocks dealt
+ * round robin over the degree-sorted core, as the paper's SRRS), a tree vertex
+ * to its anchor's partition, component trees and isolated vertices to the
+ * last one. */
+int etb_layout_partition_owner(const etb_layout* L, uint32_t parts, uint32_t* owner);
 /* One GPU per process: rank `rank` of `world` builds its partition and exports
  * an opaque blob (etb_mp_blob_size() bytes); after all blobs are exchanged
  * (ordered by rank) etb_mp_connect opens the peers' exchange blocks over CUDA

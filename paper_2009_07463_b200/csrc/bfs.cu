@@ -57,6 +57,9 @@ constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex i
 // 7 on the small-core one (s22: 5/6/7 all -0.5..-1 us per root against 8, 7 best)
 constexpr int kBuU = 8, kBuUSmall = 7;
 constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab on long levels
+// BfsParams::td_as_bu default (env ETB_TD_AS_BU overrides; 0 = off): s26 +6%
+// harmonic-mean GTEPS (slowest roots 0.80 -> 0.62-0.68 ms), s22 neutral
+constexpr double kTdAsBuDefault = 4.0;  // measured best at s26 (3..5 equal, 6 and up: no level)
 
 // The step functions below are templates on their parameter view P: BfsParams
 // (one partition: the whole core, the whole grid) or PartView (one partition of
@@ -68,6 +71,8 @@ __device__ __forceinline__ uint32_t whi_of(const BfsParams& p) { return p.nwords
 __device__ __forceinline__ unsigned cta_of(const BfsParams&) { return blockIdx.x; }
 __device__ __forceinline__ unsigned ncta_of(const BfsParams&) { return gridDim.x; }
 __device__ __forceinline__ uint32_t seg_off(const BfsParams&, uint32_t) { return 0; }
+// bitmap word of the i-th word a bottom-up step sweeps
+__device__ __forceinline__ uint64_t word_at(const BfsParams&, uint64_t i) { return i; }
 
 struct WarpSmem {
   uint32_t cbuf[kCbuf];     // staged claims (top-down); with win: deferred misses (bottom-up)
@@ -552,27 +557,28 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
     bool any = false;
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
-      vis[k] = w0 + k < whi_of(p) ? p.visited[w0 + k] : ~0u;
+      vis[k] = w0 + k < whi_of(p) ? p.visited[word_at(p, w0 + k)] : ~0u;
       any |= vis[k] != ~0u;
     }
     if (!any) continue;
     uint32_t f[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k)
-      f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[(w0 + k) * 32 + lane];
+      f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[word_at(p, w0 + k) * 32 + lane];
     bool hit[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
-      const uint32_t v = static_cast<uint32_t>((w0 + k) * 32 + lane);
+      const uint64_t wk = word_at(p, w0 + k);
+      const uint32_t v = static_cast<uint32_t>(wk * 32 + lane);
       const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
       if (hit[k]) {
         p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), f[k]);
       }
       if (lane == 0 && m) {
-        p.visited[w0 + k] = vis[k] | m;
-        fnext[w0 + k] = m;
+        p.visited[wk] = vis[k] | m;
+        fnext[wk] = m;
         claims_acc += __popc(m);
       }
       const bool miss = f[k] != kNone32 && !hit[k];
@@ -584,7 +590,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       uint32_t av[kU], ad[kU];
 #pragma unroll
       for (int k = 0; k < kU; ++k) {
-        av[k] = static_cast<uint32_t>((w0 + k) * 32 + lane);
+        av[k] = static_cast<uint32_t>(word_at(p, w0 + k) * 32 + lane);
         ad[k] = hit[k] ? p.cmeta[av[k]].x : 0u;
       }
       bu_append<kU>(av, ad, qv_out, qp_out, lslot);
@@ -610,7 +616,8 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
   // and works through the words with unvisited vertices kBuU at a time, so
   // late levels (few unvisited left) skip full words without a round trip each.
   for (uint64_t b0 = wlo_of(p) + gw * kSweep; b0 < whi_of(p); b0 += nw * kSweep) {
-    const uint32_t mine = lane < kSweep && b0 + lane < whi_of(p) ? p.visited[b0 + lane] : ~0u;
+    const uint32_t mine =
+        lane < kSweep && b0 + lane < whi_of(p) ? p.visited[word_at(p, b0 + lane)] : ~0u;
     unsigned todo = __ballot_sync(0xffffffffu, mine != ~0u);
     while (todo) {
       uint32_t vis[kBuU], wi[kBuU];
@@ -618,7 +625,7 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
       for (int k = 0; k < kBuU; ++k) {
         const int j = todo ? __ffs(todo) - 1 : 0;
         vis[k] = todo ? __shfl_sync(0xffffffffu, mine, j) : ~0u;
-        wi[k] = static_cast<uint32_t>(b0) + j;
+        wi[k] = static_cast<uint32_t>(word_at(p, b0 + j));
         todo &= todo - 1;
       }
       uint32_t f[kBuU];
@@ -900,6 +907,22 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           bu_step<kLarge ? kBuU : kBuUSmall>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext,
                                              claims_acc, qv_in, qp_in,
                                              bu_list ? &slot[0] : nullptr);
+      } else if (p.td_as_bu > 0.0 && !(L == 1 && list_from_prologue) && L > 0 &&
+                 (double)ne > p.td_as_bu * (double)(p.nc - reached)) {
+        // a top-down level (α/β state advanced as the reference's) executed as
+        // a bottom-up sweep over the unvisited core against this frontier's
+        // bitmap: the same claims, coalesced instead of scattered; claims and
+        // scout are counted from the new frontier bitmap (scout_pass)
+        etc -= (double)scout;
+        list_valid = false;
+        defer_scout = true;
+        if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
+          bu_sweep<32>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in,
+                       qp_in, nullptr);
+        else
+          bu_step<kLarge ? kBuU : kBuUSmall>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext,
+                                             claims_acc, qv_in, qp_in, nullptr);
+        claims_acc = 0;
       } else {
         etc -= (double)scout;
         // The next frontier list is emitted only when this frontier's edge count
@@ -1080,27 +1103,29 @@ __global__ void __launch_bounds__(B, 1) et_bfs_kernel(BfsParams p) {
 }
 
 // ============================================================================
-// (5) The 1D core partition (bfs_part.cuh): partition k owns the core ids
-// [lo_k, hi_k) (Eq. 1 of the paper, proj/src/preprocess.cpp:77, word aligned)
-// and the trees anchored there. The level loop is the single-partition one,
-// run by each partition over its own work with the same step functions:
-//   bottom-up  its owned visited words (bu_step / bu_sweep on a PartView);
-//   top-down   every frontier row restricted to its owned neighbours (rows
-//              are sorted: one segment per row, seg[u]), atomic-free claims
-//              (td_step<3>), the frontier list built per level from the
-//              replicated frontier bitmap;
+// (5) The 1D core partition (bfs_part.cuh): partition k owns core words
+// (hubs) and 256-vertex blocks (the rest) dealt round robin over the degree
+// order, as the paper's SRRS (Alg. 4), and the trees anchored there. The level
+// loop is the single-partition one, run by each partition over its own work
+// with the same step functions:
+//   bottom-up  its owned visited words (bu_step / bu_sweep on a PartView whose
+//              word index maps onto the owned blocks);
+//   top-down   every frontier row's owned neighbours (the partition's top-down
+//              CSR), atomic-free claims (td_step<3>), the frontier list built
+//              per level from the replicated frontier bitmap;
 // claims touch only partition-local memory (owned visited and next-frontier
 // words). At the end of a level each partition pushes its owned next-frontier
 // words to every peer's replica — the per-level frontier-bitmap allgather,
-// fused into the kernel as coalesced stores over peer memory (NVLink) or local
-// memory (all partitions on one GPU) — counting its claims and α/β scout in the
-// same pass, and one barrier over all partitions adds the partials into every
-// partition's counters, so every partition takes the same α/β decision.
+// fused into the kernel as whole 32-byte sectors over peer memory (NVLink) or
+// local memory (all partitions on one GPU) — counting its claims and α/β scout
+// in the same pass, and one barrier over all partitions adds the partials into
+// every partition's counters, so every partition takes the same α/β decision.
 // ============================================================================
 
-// What the step functions read, for one partition: the shared core graph and
-// result array, the partition's own visited replica, its CTA group, its owned
-// words and the owned segment of every core row.
+// What the step functions read, for one partition: the core graph (bottom-up:
+// the whole replicated CSR; top-down: the partition's owned-neighbour CSR) and
+// result array, the partition's own visited replica, its CTA group and its
+// owned words.
 struct PartView {
   const uint64_t* crow;
   const uint32_t* ccol;
@@ -1109,17 +1134,22 @@ struct PartView {
   const uint2* cmeta;
   uint2* dp;
   uint32_t* visited;
-  const uint2* seg;
-  uint32_t nc, nwords, wlo, whi;
+  uint32_t nc, nwords;
+  uint32_t part, nparts;
+  uint32_t nwo;   // owned words
+  uint32_t nhub;  // of which in the hub region (one word at a time)
   unsigned cta, ncta;
   unsigned long long* wstamp;  // (ETB_WARP_STAMPS diagnostics: unused here)
   int32_t wdepth;
 };
-__device__ __forceinline__ uint64_t wlo_of(const PartView& v) { return v.wlo; }
-__device__ __forceinline__ uint32_t whi_of(const PartView& v) { return v.whi; }
+__device__ __forceinline__ uint64_t wlo_of(const PartView&) { return 0; }
+__device__ __forceinline__ uint32_t whi_of(const PartView& v) { return v.nwo; }
 __device__ __forceinline__ unsigned cta_of(const PartView& v) { return v.cta; }
 __device__ __forceinline__ unsigned ncta_of(const PartView& v) { return v.ncta; }
-__device__ __forceinline__ uint32_t seg_off(const PartView& v, uint32_t u) { return v.seg[u].x; }
+__device__ __forceinline__ uint32_t seg_off(const PartView&, uint32_t) { return 0; }
+__device__ __forceinline__ uint64_t word_at(const PartView& v, uint64_t i) {
+  return owned_word(static_cast<uint32_t>(i), v.part, v.nparts, v.nhub);
+}
 
 // Exchange-block counters (per partition): two parities of {four level slots
 // of [claims, scout, grab, -], conversion counters at [16], [17]}; [62] cross
@@ -1196,10 +1226,10 @@ __device__ void part_level_sync(const PartParams& pp, uint32_t part, unsigned pa
 }
 
 // The frontier bitmap (replica, all words) -> this partition's list of
-// frontier vertices with a non-empty owned segment and the prefix of the
-// segment lengths (as convert_step, with seg[v].y for the core degree).
-__device__ void part_convert(const PartView& v, const uint32_t* fcur, uint32_t* qv, uint64_t* qp,
-                             unsigned long long* cslot) {
+// frontier vertices with owned neighbours and the prefix of their owned-row
+// lengths (as convert_step, over the top-down CSR trow).
+__device__ void part_convert(const PartView& v, const uint64_t* trow, const uint32_t* fcur,
+                             uint32_t* qv, uint64_t* qp, unsigned long long* cslot) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)wib * v.ncta + v.cta;
   const uint64_t nw = (uint64_t)(v.ncta * blockDim.x) >> 5;
@@ -1208,7 +1238,8 @@ __device__ void part_convert(const PartView& v, const uint32_t* fcur, uint32_t* 
     const uint32_t bits = wi < v.nwords ? fcur[wi] : 0u;
     uint32_t cnt = 0, edges = 0;
     for (uint32_t b = bits; b; b &= b - 1) {
-      const uint32_t d = v.seg[static_cast<uint32_t>(wi * 32 + __ffs(b) - 1)].y;
+      const uint32_t x = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
+      const uint32_t d = static_cast<uint32_t>(trow[x + 1] - trow[x]);
       cnt += d != 0;
       edges += d;
     }
@@ -1223,7 +1254,7 @@ __device__ void part_convert(const PartView& v, const uint32_t* fcur, uint32_t* 
     uint64_t vpos = (old >> kItemShift) + vin - cnt, epos = (old & kItemMask) + ein - edges;
     for (uint32_t b = bits; b; b &= b - 1) {
       const uint32_t x = static_cast<uint32_t>(wi * 32 + __ffs(b) - 1);
-      const uint32_t d = v.seg[x].y;
+      const uint32_t d = static_cast<uint32_t>(trow[x + 1] - trow[x]);
       if (!d) continue;
       qv[vpos] = x;
       qp[vpos] = epos;
@@ -1234,9 +1265,9 @@ __device__ void part_convert(const PartView& v, const uint32_t* fcur, uint32_t* 
 }
 
 // The allgather of one level: this partition's owned next-frontier words, 32
-// per warp iteration (one coalesced 128-byte store per peer), into every
-// peer's replica of that ring slot; with kCount also the level's claims
-// (popcount) and α/β scout (Σ full degree, coalesced: lane = vertex).
+// per warp iteration (four whole 8-word blocks: four 32-byte sectors per peer),
+// into every peer's replica of that ring slot; with kCount also the level's
+// claims (popcount) and α/β scout (Σ full degree, coalesced: lane = vertex).
 template <bool kCount>
 __device__ void part_push(const PartParams& pp, uint32_t part, const PartView& v, uint32_t ring,
                           const uint32_t* fnext, unsigned long long& claims,
@@ -1244,9 +1275,9 @@ __device__ void part_push(const PartParams& pp, uint32_t part, const PartView& v
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)wib * v.ncta + v.cta;
   const uint64_t nw = (uint64_t)(v.ncta * blockDim.x) >> 5;
-  for (uint64_t w0 = v.wlo + gw * 32; w0 < v.whi; w0 += nw * 32) {
-    const uint64_t wi = w0 + lane;
-    const bool in = wi < v.whi;
+  for (uint64_t j0 = gw * 32; j0 < v.nwo; j0 += nw * 32) {
+    const bool in = j0 + lane < v.nwo;
+    const uint32_t wi = in ? static_cast<uint32_t>(word_at(v, j0 + lane)) : 0u;
     const uint32_t f = in ? __ldcg(&fnext[wi]) : 0u;
     for (uint32_t q = 0; q < pp.nparts; ++q) {
       if (q == part || !in) continue;
@@ -1260,15 +1291,24 @@ __device__ void part_push(const PartParams& pp, uint32_t part, const PartView& v
 #pragma unroll 4
         for (int j = 0; j < 32; ++j) {
           const uint32_t bits = __shfl_sync(0xffffffffu, f, j);
-          if ((bits >> lane) & 1u) scout += v.degn[(w0 + j) * 32 + lane];
+          const uint32_t w = __shfl_sync(0xffffffffu, wi, j);
+          if ((bits >> lane) & 1u) scout += v.degn[(uint64_t)w * 32 + lane];
         }
       }
     }
   }
 }
 
-__device__ __forceinline__ bool owns(const PartDev& me, uint32_t v) {
-  return (v >= me.lo && v < me.hi) || (v >= me.tlo && v < me.thi) || (v >= me.zlo && v < me.zhi);
+// Does partition `part` of G own relaid vertex x (core block, tree by anchor,
+// component trees and isolated vertices to the last partition)?
+__device__ __forceinline__ bool owns(const BfsParams& p, const PartDev& me, uint32_t part,
+                                     uint32_t G, uint32_t x) {
+  if (x < p.nc) return core_owner(x, G) == part;
+  if (x < p.nc + p.nt) {
+    const uint32_t a = p.tanchor[x - p.nc];
+    return a == kNone32 ? part == G - 1 : core_owner(a, G) == part;
+  }
+  return x >= me.zlo && x < me.zhi;
 }
 
 template <bool kLarge>
@@ -1279,12 +1319,13 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   const unsigned gsize = gridDim.x / pp.local_parts;
   const unsigned cta = blockIdx.x % gsize;
   const uint32_t part = pp.first_part + blockIdx.x / gsize;
+  const uint32_t G = pp.nparts;
   const PartDev& me = pp.parts[part];
   const uint64_t gtid = (uint64_t)cta * blockDim.x + threadIdx.x;
   const uint64_t gthreads = (uint64_t)gsize * blockDim.x;
   const bool lead = part == 0 && cta == 0 && threadIdx.x == 0;
   const bool stats = p.level_claims && lead;
-  PartView v;
+  PartView v;  // bottom-up view: the whole core CSR
   v.crow = p.crow;
   v.ccol = p.ccol;
   v.cfirst = p.cfirst;
@@ -1292,20 +1333,24 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   v.cmeta = p.cmeta;
   v.dp = p.dp;
   v.visited = me.visited;
-  v.seg = me.seg;
   v.nc = p.nc;
   v.nwords = p.nwords;
-  v.wlo = me.lo >> 5;
-  v.whi = static_cast<uint32_t>((static_cast<uint64_t>(me.hi) + 31) >> 5);
+  v.part = part;
+  v.nparts = G;
+  v.nwo = me.nwo;
+  v.nhub = me.nhub;
   v.cta = cta;
   v.ncta = gsize;
   v.wstamp = nullptr;
   v.wdepth = -1;
+  PartView vt = v;  // top-down view: the partition's owned-neighbour CSR
+  vt.crow = me.trow;
+  vt.ccol = me.tcol;
   const unsigned long long launch = me.ctr[kLaunchSlot];
   const unsigned par = static_cast<unsigned>(launch & 1u);
   unsigned long long* const ctr = me.ctr + 32 * par;
   unsigned long long xk = me.ctr[kXkSlot];  // cross barriers completed by earlier launches
-  const unsigned long long per_barrier = static_cast<unsigned long long>(pp.nparts) * gsize;
+  const unsigned long long per_barrier = static_cast<unsigned long long>(G) * gsize;
   const uint32_t start = p.start;
   const bool run_core = start != kNone32;
   if (stats) p.level_claims[256] = gtimer();
@@ -1316,17 +1361,17 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   {
     const uint32_t tail = p.nc & 31u;
     const uint32_t sw = run_core ? start >> 5 : kNone32, sb = run_core ? 1u << (start & 31) : 0u;
-    for (uint64_t i = gtid; i < p.nwords; i += gthreads) {
-      me.fb0[i] = i == sw ? sb : 0u;  // the whole replica: a bottom-up level 0 probes it
-      if (i >= v.wlo && i < v.whi) {
-        uint32_t vis = i == sw ? sb : 0u;
-        if (i == p.nwords - 1 && tail) vis |= ~0u << tail;
-        me.visited[i] = vis;
-        me.fb1[i] = 0;
-      }
+    for (uint64_t i = gtid; i < p.nwords; i += gthreads)  // a bottom-up level 0 probes it all
+      me.fb0[i] = i == sw ? sb : 0u;
+    for (uint64_t j = gtid; j < me.nwo; j += gthreads) {
+      const uint32_t i = static_cast<uint32_t>(word_at(v, j));
+      uint32_t vis = i == sw ? sb : 0u;
+      if (i == p.nwords - 1 && tail) vis |= ~0u << tail;
+      me.visited[i] = vis;
+      me.fb1[i] = 0;
     }
   }
-  if (run_core && gtid == 0 && start >= me.lo && start < me.hi)
+  if (run_core && gtid == 0 && core_owner(start, G) == part)
     p.dp[start] = make_uint2(static_cast<uint32_t>(p.base_depth), p.start_parent);
   group_sync(me.bar, gsize);
   if (stats) p.level_claims[257] = gtimer();
@@ -1343,7 +1388,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
       uint32_t* fnext = F[(L + 1) % 3];
       uint32_t* fzero = F[(L + 2) % 3];
       unsigned long long* slot = ctr + (L & 3) * 4;
-      for (uint64_t i = v.wlo + gtid; i < v.whi; i += gthreads) fzero[i] = 0;  // owned words
+      for (uint64_t j = gtid; j < me.nwo; j += gthreads) fzero[word_at(v, j)] = 0;  // owned words
       if (gtid == 0) {
         ctr[((L + 2) & 3) * 4 + 0] = 0;
         ctr[((L + 2) & 3) * 4 + 1] = 0;
@@ -1366,22 +1411,38 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         group_sync(me.bar, gsize);  // the owned next words are final
         unsigned long long none = 0;
         part_push<false>(pp, part, v, (L + 1) % 3, fnext, none, none);
+      } else if (p.td_as_bu > 0.0 && L > 0 &&
+                 (double)scout > p.td_as_bu * (double)(p.nc - reached)) {
+        // a top-down level executed as a bottom-up sweep over the owned
+        // unvisited words (as et_bfs_body; decided on the frontier's full degree
+        // sum, known to every partition before any list is built): same claims,
+        // counted with the scout by the push pass
+        etc -= (double)scout;
+        if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
+          bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
+        else
+          bu_step<kLarge ? kBuU : kBuUSmall>(v, mb, fcur, fnext, dnext, claims_acc, nullptr,
+                                             nullptr, nullptr);
+        claims_acc = 0;
+        if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
+        group_sync(me.bar, gsize);
+        part_push<true>(pp, part, v, (L + 1) % 3, fnext, claims_acc, scout_acc);
       } else {
         etc -= (double)scout;
         uint64_t nq = 0, ne = 0;
         if (L == 0) {
-          ne = me.seg[start].y;  // the start's owned row segment, no list
+          ne = me.trow[start + 1] - me.trow[start];  // the start's owned neighbours, no list
           nq = ne != 0;
         } else {
           unsigned long long* cslot = ctr + 16 + (L & 1);
-          part_convert(v, fcur, me.qv, me.qp, cslot);
+          part_convert(v, me.trow, fcur, me.qv, me.qp, cslot);
           group_sync(me.bar, gsize);
           if (threadIdx.x == 0) sm.tot[2] = ld_volatile(cslot);
           __syncthreads();
           nq = sm.tot[2] >> kItemShift;
           ne = sm.tot[2] & kItemMask;
         }
-        td_step<3, kLarge>(v, mb, sm.w[threadIdx.x >> 5].win, me.qv, me.qp, nq, ne, nullptr,
+        td_step<3, kLarge>(vt, mb, sm.w[threadIdx.x >> 5].win, me.qv, me.qp, nq, ne, nullptr,
                            nullptr, fnext, slot, dnext, scout_acc, claims_acc,
                            L == 0 ? start : kNone32);
         if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
@@ -1431,17 +1492,20 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   if (stats && p.nlevels) *p.nlevels = L;
 
   // ---- owned tree replay + owned core fill + owned patch entries ---------------
-  // (as et_bfs_body's final phase over the partition's ranges: four tree
+  // (as et_bfs_body's final phase over the partition's vertices: four tree
   // entries in flight per thread, and a warp clears the unreached vertices of
   // 32 owned visited words with coalesced 256-byte stores)
-  const uint64_t tlo = me.tlo, nto = me.thi - me.tlo;
-  for (uint64_t t0 = gtid; t0 < nto; t0 += 4 * gthreads) {
-    uint32_t a[4], td[4], ts[4], vb[4], da[4];
+  for (uint64_t t0 = gtid; t0 < me.ntrees; t0 += 4 * gthreads) {
+    uint32_t tv[4], a[4], td[4], ts[4], vb[4], da[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint64_t tv = tlo + t0 + k * gthreads;
-      const bool in = t0 + k * gthreads < nto && !(tv >= p.skip_lo && tv < p.skip_hi);
-      const uint64_t t = tv - p.nc;
+      const uint64_t i = t0 + k * gthreads;
+      tv[k] = i < me.ntrees ? me.trees[i] : kNone32;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool in = tv[k] != kNone32 && !(tv[k] >= p.skip_lo && tv[k] < p.skip_hi);
+      const uint32_t t = tv[k] - p.nc;
       a[k] = in ? p.tanchor[t] : kNone32 - 1;
       td[k] = in ? p.tdepth[t] : 0u;
       ts[k] = in ? p.tsrc[t] : 0u;
@@ -1455,30 +1519,32 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (a[k] == kNone32 - 1) continue;  // out of range or inside the start's tree
-      p.dp[tlo + t0 + k * gthreads] =
-          vb[k] ? make_uint2(da[k] + td[k], ts[k]) : make_uint2(kNone32, kNone32);
+      p.dp[tv[k]] = vb[k] ? make_uint2(da[k] + td[k], ts[k]) : make_uint2(kNone32, kNone32);
     }
   }
   {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t gw = gtid >> 5, nw = gthreads >> 5;
-    for (uint64_t w0 = v.wlo + gw * 32; w0 < v.whi; w0 += nw * 32) {
-      const uint32_t un = w0 + lane < v.whi ? ~me.visited[w0 + lane] : 0u;
+    for (uint64_t j0 = gw * 32; j0 < me.nwo; j0 += nw * 32) {
+      const bool in = j0 + lane < me.nwo;
+      const uint32_t wi = in ? static_cast<uint32_t>(word_at(v, j0 + lane)) : 0u;
+      const uint32_t un = in ? ~me.visited[wi] : 0u;
       for (unsigned m = __ballot_sync(0xffffffffu, un != 0); m; m &= m - 1) {
         const int j = __ffs(m) - 1;
+        const uint32_t w = __shfl_sync(0xffffffffu, wi, j);
         if ((__shfl_sync(0xffffffffu, un, j) >> lane) & 1u)
-          p.dp[(w0 + j) * 32 + lane] = make_uint2(kNone32, kNone32);
+          p.dp[(uint64_t)w * 32 + lane] = make_uint2(kNone32, kNone32);
       }
     }
   }
   for (uint64_t i = gtid; i < p.npatch; i += gthreads) {
     const uint32_t x = p.patch[3 * i];
-    if (owns(me, x)) p.dp[x] = make_uint2(p.patch[3 * i + 1], p.patch[3 * i + 2]);
+    if (owns(p, me, part, G, x)) p.dp[x] = make_uint2(p.patch[3 * i + 1], p.patch[3 * i + 2]);
   }
 #pragma unroll
   for (int k = 0; k < kInlinePatch; ++k)
     if (gtid == static_cast<uint64_t>(k) && static_cast<uint32_t>(k) < p.nipatch &&
-        owns(me, p.ipatch[3 * k]))
+        owns(p, me, part, G, p.ipatch[3 * k]))
       p.dp[p.ipatch[3 * k]] = make_uint2(p.ipatch[3 * k + 1], p.ipatch[3 * k + 2]);
   if (p.bstamp) {
     __syncthreads();
@@ -1616,6 +1682,8 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   // (nc/8: s26 -3.5 us per root against nc/4 — more of the large levels take
   // the list-less path; s22 unchanged)
   p.emit_limit = static_cast<double>(L.nc) / 8.0 + 1024.0;
+  p.td_as_bu = kTdAsBuDefault;
+  if (const char* e = getenv("ETB_TD_AS_BU")) p.td_as_bu = atof(e);
   p.trace = nullptr;
   p.level_claims = nullptr;
   p.bstamp = nullptr;

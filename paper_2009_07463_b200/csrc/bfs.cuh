@@ -59,6 +59,12 @@ struct BfsParams {
   uint32_t ipatch[3 * kInlinePatch];
   double alpha, beta, edges_to_check;
   double emit_limit;  // top-down levels with scout >= this skip work-item emission
+  // A level the α/β rule runs top-down is executed as a frontier-restricted
+  // bottom-up sweep when its frontier edges exceed td_as_bu x the unvisited core
+  // vertices (0 = never): the claimed set — the unvisited core vertices with a
+  // frontier neighbour — is the same, so depths, claims, scout and the α/β
+  // sequence are the reference's; only the GPU cost differs.
+  double td_as_bu;
   int top_down_only;   // CoreKernel::kTopDown
   int bottom_up_only;  // CoreKernel::kBlockSearch: bottom-up levels to fixpoint
   // stats (may be null)

@@ -10,23 +10,25 @@
 namespace etb {
 namespace {
 
-// seg[u] = {offset, length} of u's neighbours inside [lo, hi) (rows ascend).
-__global__ void seg_kernel(const uint64_t* crow, const uint32_t* ccol, uint64_t nc, uint32_t lo,
-                           uint32_t hi, uint2* seg) {
+// Top-down CSR of partition k: per core row, the neighbours it owns (rows stay
+// sorted). count pass, then (after a scan) fill pass.
+__global__ void owned_count_kernel(const uint64_t* crow, const uint32_t* ccol, uint64_t nc,
+                                   uint32_t k, uint32_t G, uint32_t* cnt) {
   for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nc;
        u += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t rb = crow[u], re = crow[u + 1];
-    uint64_t a = rb, b = re;
-    while (a < b) {
-      const uint64_t m = (a + b) >> 1;
-      if (ccol[m] < lo) a = m + 1; else b = m;
-    }
-    uint64_t c = a, d = re;
-    while (c < d) {
-      const uint64_t m = (c + d) >> 1;
-      if (ccol[m] < hi) c = m + 1; else d = m;
-    }
-    seg[u] = make_uint2(static_cast<uint32_t>(a - rb), static_cast<uint32_t>(c - a));
+    uint32_t c = 0;
+    for (uint64_t e = crow[u]; e < crow[u + 1]; ++e) c += core_owner(ccol[e], G) == k;
+    cnt[u] = c;
+  }
+}
+
+__global__ void owned_fill_kernel(const uint64_t* crow, const uint32_t* ccol, uint64_t nc,
+                                  uint32_t k, uint32_t G, const uint64_t* trow, uint32_t* tcol) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nc;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t o = trow[u];
+    for (uint64_t e = crow[u]; e < crow[u + 1]; ++e)
+      if (core_owner(ccol[e], G) == k) tcol[o++] = ccol[e];
   }
 }
 
@@ -37,50 +39,44 @@ PartState::~PartState() {
     if (m) cudaIpcCloseMemHandle(m);
 }
 
-void part_bounds(const DevLayout& L, uint32_t nparts, std::vector<PartDev>& out) {
+void part_owners(const DevLayout& L, uint32_t nparts, uint32_t* owner) {
   if (nparts < 1 || nparts > kMaxParts)
     throw std::invalid_argument("etb_layout_partition: partitions must be in [1, 16]");
-  out.assign(nparts, PartDev{});
   const uint64_t nc = L.nc, nt = L.nt;
-  // Core: V_k = [k nc / G, (k+1) nc / G) rounded down to whole 32-vertex words.
-  for (uint32_t k = 0; k < nparts; ++k) {
-    const uint64_t lo = k == 0 ? 0 : ((k * nc / nparts) & ~uint64_t{31});
-    const uint64_t hi = k + 1 == nparts ? nc : (((k + 1) * nc / nparts) & ~uint64_t{31});
-    out[k].lo = static_cast<uint32_t>(lo);
-    out[k].hi = static_cast<uint32_t>(std::max(lo, hi));
+  for (uint64_t v = 0; v < nc; ++v) owner[v] = core_owner(static_cast<uint32_t>(v), nparts);
+  for (uint64_t t = 0; t < nt; ++t) {
+    const uint32_t a = L.h_tanchor[t];
+    owner[nc + t] = a == kNone32 ? nparts - 1 : core_owner(a, nparts);
   }
-  // Trees follow their anchor (trees are laid out in anchor order); component
-  // trees and isolated vertices go to the last partition.
-  const auto& anc = L.h_tanchor;
-  uint64_t first_component = nt;
-  for (uint64_t i = 0; i < nt; ++i)
-    if (anc[i] == kNone32) {
-      first_component = i;
-      break;
-    }
-  for (uint32_t k = 0; k < nparts; ++k) {
-    auto lb = [&](uint32_t bound) {
-      return static_cast<uint64_t>(std::lower_bound(anc.begin(), anc.begin() + first_component,
-                                                    bound) - anc.begin());
-    };
-    const uint64_t t0 = k == 0 ? 0 : lb(out[k].lo);
-    const uint64_t t1 = k + 1 == nparts ? nt : lb(out[k + 1].lo);
-    out[k].tlo = static_cast<uint32_t>(nc + t0);
-    out[k].thi = static_cast<uint32_t>(nc + t1);
-    out[k].zlo = out[k].zhi = static_cast<uint32_t>(L.n);
-  }
-  out[nparts - 1].zlo = static_cast<uint32_t>(nc + nt);
+  for (uint64_t v = nc + nt; v < L.n; ++v) owner[v] = nparts - 1;
 }
 
 void part_build(const DevLayout& L, PartState& P, uint32_t nparts, uint32_t first, uint32_t local,
                 cudaStream_t s) {
+  if (nparts < 1 || nparts > kMaxParts)
+    throw std::invalid_argument("etb_layout_partition: partitions must be in [1, 16]");
   P.nparts = nparts;
   P.first = first;
   P.local = local;
-  part_bounds(L, nparts, P.h_parts);
-  const uint64_t nc = L.nc;
-  const uint64_t words = (nc + 31) / 32 + 1;
-  P.seg.alloc(local * (nc ? nc : 1));
+  const uint64_t nc = L.nc, nt = L.nt;
+  const uint32_t nw = static_cast<uint32_t>((nc + 31) / 32);
+  const uint64_t words = nw + 1;
+  P.h_parts.assign(nparts, PartDev{});
+  std::vector<std::vector<uint32_t>> trees(nparts);
+  for (uint64_t t = 0; t < nt; ++t) {
+    const uint32_t a = L.h_tanchor[t];
+    trees[a == kNone32 ? nparts - 1 : core_owner(a, nparts)].push_back(
+        static_cast<uint32_t>(nc + t));
+  }
+  for (uint32_t k = 0; k < nparts; ++k) {
+    PartDev& d = P.h_parts[k];
+    d.part = k;
+    d.nwo = owned_words(nw, k, nparts);
+    d.nhub = owned_hub_words(nw, k, nparts);
+    d.ntrees = static_cast<uint32_t>(trees[k].size());
+    d.zlo = d.zhi = static_cast<uint32_t>(L.n);
+  }
+  P.h_parts[nparts - 1].zlo = static_cast<uint32_t>(nc + nt);
   P.visited.alloc(local * words);
   P.qv.alloc(local * (nc + 1));
   P.qp.alloc(local * (nc + 1));
@@ -89,8 +85,13 @@ void part_build(const DevLayout& L, PartState& P, uint32_t nparts, uint32_t firs
   ETB_CUDA(cudaMemsetAsync(P.xblock.get(), 0, local * P.xbytes, s));
   P.bar.alloc(local);
   ETB_CUDA(cudaMemsetAsync(P.bar.get(), 0, local * 8, s));
+  P.trow.resize(local);
+  P.tcol.resize(local);
+  P.trees.resize(local);
+  DevBuf<uint32_t> cnt(nc ? nc : 1);
   for (uint32_t j = 0; j < local; ++j) {
-    PartDev& d = P.h_parts[first + j];
+    const uint32_t k = first + j;
+    PartDev& d = P.h_parts[k];
     unsigned char* xb = P.xblock.get() + j * P.xbytes;
     d.fb0 = reinterpret_cast<uint32_t*>(xb);
     d.fb1 = d.fb0 + words;
@@ -101,12 +102,37 @@ void part_build(const DevLayout& L, PartState& P, uint32_t nparts, uint32_t firs
     d.visited = P.visited.get() + j * words;
     d.qv = P.qv.get() + j * (nc + 1);
     d.qp = P.qp.get() + j * (nc + 1);
-    uint2* sg = P.seg.get() + j * (nc ? nc : 1);
-    d.seg = sg;
+    // the top-down CSR of this partition's owned neighbours
+    P.trow[j].alloc(nc + 1);
+    uint64_t ne = 0;
     if (nc) {
-      seg_kernel<<<grid_for(nc, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), nc, d.lo, d.hi, sg);
+      owned_count_kernel<<<grid_for(nc, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), nc, k,
+                                                           nparts, cnt.get());
+      ETB_LAUNCH_CHECK();
+      exclusive_scan_u32_to_u64(cnt.get(), P.trow[j].get(), nc, s);
+      uint64_t last = 0;
+      uint32_t lastc = 0;
+      ETB_CUDA(cudaMemcpyAsync(&last, P.trow[j].get() + nc - 1, 8, cudaMemcpyDeviceToHost, s));
+      ETB_CUDA(cudaMemcpyAsync(&lastc, cnt.get() + nc - 1, 4, cudaMemcpyDeviceToHost, s));
+      ETB_CUDA(cudaStreamSynchronize(s));
+      ne = last + lastc;
+    }
+    ETB_CUDA(cudaMemcpyAsync(P.trow[j].get() + nc, &ne, 8, cudaMemcpyHostToDevice, s));
+    P.tcol[j].alloc(ne ? ne : 1);
+    if (nc) {
+      owned_fill_kernel<<<grid_for(nc, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), nc, k,
+                                                          nparts, P.trow[j].get(),
+                                                          P.tcol[j].get());
       ETB_LAUNCH_CHECK();
     }
+    d.trow = P.trow[j].get();
+    d.tcol = P.tcol[j].get();
+    P.trees[j].alloc(trees[k].empty() ? 1 : trees[k].size());
+    if (!trees[k].empty())
+      ETB_CUDA(cudaMemcpyAsync(P.trees[j].get(), trees[k].data(), trees[k].size() * 4,
+                               cudaMemcpyHostToDevice, s));
+    d.trees = P.trees[j].get();
+    ETB_CUDA(cudaStreamSynchronize(s));  // the host vectors above
   }
   P.d_parts.alloc(nparts);
   ETB_CUDA(cudaMemcpyAsync(P.d_parts.get(), P.h_parts.data(), nparts * sizeof(PartDev),
@@ -115,10 +141,10 @@ void part_build(const DevLayout& L, PartState& P, uint32_t nparts, uint32_t firs
   ETB_CUDA(cudaGetDevice(&dev));
   ETB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   P.block = block_for(nc);
-  const void* k = part_kernel_for(P.block);
-  ETB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const void* kf = part_kernel_for(P.block);
+  ETB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(bfs_smem_bytes())));
-  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P.block, bfs_smem_bytes()));
+  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, P.block, bfs_smem_bytes()));
   if (per_sm < 1) throw CudaError("et_bfs_part_kernel cannot be resident");
   int grid = sms;  // one CTA per SM, as the single-partition kernel
   grid -= grid % static_cast<int>(local);  // equal block groups

@@ -205,6 +205,23 @@ __global__ void te_kernel(const uint2* dp, const uint32_t* degn, uint64_t n,
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
+// te_kernel over the vertices partition `part` of G owns (bfs_part.cuh).
+__global__ void te_owned_kernel(const uint2* dp, const uint32_t* degn, uint64_t n, uint64_t nc,
+                                uint64_t nt, const uint32_t* tanchor, uint32_t part, uint32_t G,
+                                unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t o;
+    if (i < nc) o = etb::core_owner(static_cast<uint32_t>(i), G);
+    else if (i < nc + nt) o = tanchor[i - nc] == etb::kNone32 ? G - 1 : etb::core_owner(tanchor[i - nc], G);
+    else o = G - 1;
+    if (o == part && static_cast<int32_t>(dp[i].x) >= 0) acc += degn[i];
+  }
+  for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 // Interleaved {depth, parent} -> separate arrays (either may be null).
 __global__ void split_kernel(const uint2* dp, uint64_t n, int32_t* depth, uint32_t* parent,
                              uint64_t* parent64) {
@@ -742,14 +759,10 @@ int etb_result_traversed_edges(etb_layout* h, uint64_t* te) {
     if (h->P && h->P->local < h->P->nparts && !h->S.assembled) {
       // Multi-GPU: this device holds only its partitions' results; the caller
       // sums the partial counts over ranks.
-      for (uint32_t j = 0; j < h->P->local; ++j) {
-        const etb::PartDev& d = h->P->h_parts[h->P->first + j];
-        const std::pair<uint64_t, uint64_t> rs[3] = {{d.lo, d.hi}, {d.tlo, d.thi}, {d.zlo, d.zhi}};
-        for (const auto& r : rs)
-          if (r.second > r.first)
-            te_kernel<<<etb::grid_for(r.second - r.first, 256), 256, 0, h->stream>>>(
-                h->S.dp.get() + r.first, h->L.degn.get() + r.first, r.second - r.first, acc.get());
-      }
+      for (uint32_t j = 0; j < h->P->local; ++j)
+        te_owned_kernel<<<etb::grid_for(h->L.n, 256), 256, 0, h->stream>>>(
+            h->S.dp.get(), h->L.degn.get(), h->L.n, h->L.nc, h->L.nt, h->L.tanchor.get(),
+            h->P->first + j, h->P->nparts, acc.get());
     } else {
       te_kernel<<<etb::grid_for(h->L.n, 256), 256, 0, h->stream>>>(h->S.dp.get(), h->L.degn.get(),
                                                                     h->L.n, acc.get());
@@ -915,17 +928,11 @@ int etb_layout_partition_scope(etb_layout* h, int system_scope) {
   });
 }
 
-int etb_layout_partition_bounds(const etb_layout* h, uint32_t parts, uint64_t* bounds) {
+int etb_layout_partition_owner(const etb_layout* h, uint32_t parts, uint32_t* owner) {
   return guarded([&] {
-    need(h, "etb_layout_partition_bounds");
-    need(bounds, "etb_layout_partition_bounds");
-    std::vector<etb::PartDev> b;
-    etb::part_bounds(h->L, parts, b);
-    for (uint32_t k = 0; k < parts; ++k) {
-      uint64_t* o = bounds + 6 * k;
-      o[0] = b[k].lo, o[1] = b[k].hi, o[2] = b[k].tlo, o[3] = b[k].thi, o[4] = b[k].zlo,
-      o[5] = b[k].zhi;
-    }
+    need(h, "etb_layout_partition_owner");
+    if (h->L.n) need(owner, "etb_layout_partition_owner");
+    etb::part_owners(h->L, parts, owner);
   });
 }
 

@@ -171,7 +171,7 @@ def lib() -> C.CDLL:
     sig("etb_debug_block_stamps", vp, u64, vp, u64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32))
     sig("etb_debug_warp_stamps", vp, u64, C.c_int32, vp, u64, C.POINTER(C.c_uint32))
     sig("etb_layout_partition", vp, C.c_uint32)
-    sig("etb_layout_partition_bounds", vp, C.c_uint32, vp)
+    sig("etb_layout_partition_owner", vp, C.c_uint32, vp)
     sig("etb_layout_partition_scope", vp, C.c_int)
     sig("etb_mp_blob_size")
     sig("etb_mp_export", vp, C.c_uint32, C.c_uint32, vp)
@@ -387,11 +387,11 @@ def partition(cg: "EtLayout", parts: int, system_scope: bool = False) -> None:
         _check(lib().etb_layout_partition_scope(cg.handle, 1))
 
 
-def partition_bounds(cg: "EtLayout", parts: int) -> np.ndarray:
-    """(parts, 6) u64: core lo/hi, tree lo/hi, isolated lo/hi per partition."""
-    b = np.empty(6 * parts, np.uint64)
-    _check(lib().etb_layout_partition_bounds(cg.handle, int(parts), _ptr(b)))
-    return b.reshape(parts, 6)
+def partition_owner(cg: "EtLayout", parts: int) -> np.ndarray:
+    """u32[n]: the partition owning each relaid vertex (bfs_part.cuh rule)."""
+    o = np.empty(max(cg.vertex_count, 1), np.uint32)
+    _check(lib().etb_layout_partition_owner(cg.handle, int(parts), _ptr(o)))
+    return o[: cg.vertex_count]
 
 
 def relayout_csr(g: Csr, types=None, mh: int = -1) -> EtLayout:

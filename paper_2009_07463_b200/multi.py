@@ -1,17 +1,19 @@
 """Host side of the 1D core partition.
 
-* ``partition_bounds`` restates the device partition rule (bfs_part.cu
-  ``part_bounds``): core V_k = [k·nc/G, (k+1)·nc/G) rounded down to 32-vertex
-  bitmap words (Eq. 1 of the paper; proj/src/preprocess.cpp:77); edge trees
-  follow their anchor; component trees and isolated vertices go to the last
-  partition.
+* ``partition_owner`` restates the device ownership rule (bfs_part.cuh): the
+  degree-sorted core is dealt round robin, as the paper's static round-robin
+  shuffle (SRRS, Alg. 4) balances its segments (the equal ranges of Eq. 1,
+  proj/src/preprocess.cpp:77, would give one partition every hub) — the first
+  2048 bitmap words (64K hubs) one 32-vertex word at a time, the rest in
+  256-vertex blocks; a tree vertex follows its anchor; component trees and
+  isolated vertices go to the last partition.
 * ``exchange_blobs`` / ``connect`` wire one process per GPU: each rank exports
   its partition's exchange block as a CUDA IPC blob, the blobs are all-gathered
   through torch.distributed (any backend; gloo in the CPU tests), and each rank
   opens its peers' blocks. The BFS kernels then synchronise through NVLink peer
   memory — no NCCL call on the data path.
 * ``assemble_result`` (validation only, outside any timed region): every rank
-  holds the result of the vertices it owns; the owned slices are summed over
+  holds the result of the vertices it owns; the owned entries are summed over
   ranks (disjoint supports, so the sum is the merge) and written back, so the
   device validator sees the whole tree on every rank.
 """
@@ -22,28 +24,29 @@ import ctypes as C
 import numpy as np
 
 NONE32 = 0xFFFFFFFF
+HUB_WORDS = 2048   # bitmap words dealt one at a time
+BLOCK_WORDS = 8    # the rest: 256-vertex blocks
 
 
-def partition_bounds(nc: int, nt: int, n: int, tanchor: np.ndarray, parts: int) -> np.ndarray:
-    """(parts, 6) array: core lo, hi, tree lo, hi, isolated lo, hi (relaid ids)."""
+def core_owner(v, parts):
+    w = np.asarray(v, np.uint64) >> np.uint64(5)
+    hub = w < HUB_WORDS
+    tail = (w - np.minimum(w, HUB_WORDS)) // BLOCK_WORDS
+    return np.where(hub, w % parts, tail % parts).astype(np.uint32)
+
+
+def partition_owner(nc: int, nt: int, n: int, tanchor: np.ndarray, parts: int) -> np.ndarray:
+    """The owning partition of every relaid vertex (u32[n])."""
     if parts < 1 or parts > 16:
         raise ValueError("etb_layout_partition: partitions must be in [1, 16]")
-    out = np.zeros((parts, 6), np.uint64)
-    for k in range(parts):
-        lo = 0 if k == 0 else (k * nc // parts) & ~31
-        hi = nc if k + 1 == parts else ((k + 1) * nc // parts) & ~31
-        out[k, 0], out[k, 1] = lo, max(lo, hi)
-    anc = np.asarray(tanchor, np.uint64)
-    comp = np.nonzero(anc == NONE32)[0]
-    first_component = int(comp[0]) if comp.size else nt
-    attached = anc[:first_component]
-    for k in range(parts):
-        t0 = 0 if k == 0 else int(np.searchsorted(attached, out[k, 0], side="left"))
-        t1 = nt if k + 1 == parts else int(np.searchsorted(attached, out[k + 1, 0], side="left"))
-        out[k, 2], out[k, 3] = nc + t0, nc + t1
-        out[k, 4] = out[k, 5] = n
-    out[parts - 1, 4] = nc + nt
-    return out
+    own = np.full(n, parts - 1, np.uint32)
+    own[:nc] = core_owner(np.arange(nc, dtype=np.uint64), parts)
+    anc = np.asarray(tanchor, np.uint64)[:nt]
+    attached = anc != NONE32
+    tree_own = np.full(nt, parts - 1, np.uint32)
+    tree_own[attached] = core_owner(anc[attached], parts)
+    own[nc:nc + nt] = tree_own
+    return own
 
 
 def exchange_blobs(blob: bytes, group=None) -> list[bytes]:
@@ -69,19 +72,15 @@ def connect(cg, rank: int, world: int, group=None) -> None:
     _check(L.etb_mp_connect(cg.handle, joined))
 
 
-def merge_owned(local, bounds_row, dist, group=None):
-    """The whole result from every rank's owned slices: this rank's owned ranges
-    (core, trees, isolated; bounds_row = its row of partition_bounds) of `local`
-    (a 1-D int64 tensor of interleaved {depth, parent} pairs), zero elsewhere,
-    summed over ranks. Supports are disjoint, so the sum reproduces each owner's
-    entries exactly (negative values included)."""
+def merge_owned(local, mine, dist, group=None):
+    """The whole result from every rank's owned entries: `local` (a 1-D int64
+    tensor of interleaved {depth, parent} pairs) where `mine` (a bool tensor on
+    the same device: this rank owns the vertex), zero elsewhere, summed over
+    ranks. Supports are disjoint, so the sum reproduces each owner's entries
+    exactly (negative values included)."""
     import torch
 
-    out = torch.zeros_like(local)
-    b = [int(x) for x in bounds_row]
-    for lo, hi in ((b[0], b[1]), (b[2], b[3]), (b[4], b[5])):
-        if hi > lo:
-            out[lo:hi] = local[lo:hi]
+    out = torch.where(mine, local, torch.zeros_like(local))
     dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
     return out
 
@@ -97,12 +96,13 @@ def assemble_result(cg, D) -> None:
     buffer and mark it whole (etb_result_mark_assembled)."""
     import torch
 
-    from .etbfs import _check, lib, partition_bounds
+    from .etbfs import _check, lib, partition_owner
 
     ptr = C.c_void_p()
     _check(lib().etb_result_device_ptr(cg.handle, C.byref(ptr)))
     dp = torch.as_tensor(_DeviceArray(ptr.value, cg.vertex_count), device="cuda")
-    full = merge_owned(dp, partition_bounds(cg, D.world)[D.rank], D.d)
+    mine = torch.from_numpy(partition_owner(cg, D.world) == D.rank).to(dp.device)
+    full = merge_owned(dp, mine, D.d)
     dp.copy_(full)
     torch.cuda.synchronize()
     _check(lib().etb_result_mark_assembled(cg.handle))

@@ -9,20 +9,20 @@ import oracle as O
 import paper_2009_07463_b200 as eb
 from conftest import edges_of
 from paper_2009_07463_b200 import etbfs as E
-from paper_2009_07463_b200.multi import partition_bounds
+from paper_2009_07463_b200.multi import partition_owner
 from test_gpu_parity import check_root
 
 pytestmark = pytest.mark.gpu
 
 
-def test_bounds_match_host_rule(kron16):
+def test_owner_matches_host_rule(kron16):
     cg = eb.relayout_csr(eb.generate_graph(scale=16, edgefactor=16, seed=1), mh=-1)
     _, _, ce = eb.extract_edge_tree_list(cg)
     anchor = np.where(ce == O.NO_VERTEX, np.uint64(0xFFFFFFFF), ce)
     for parts in (1, 2, 3, 8, 16):
-        want = partition_bounds(cg.core_vertex_count, cg.tree_vertex_count, cg.vertex_count,
-                                anchor, parts)
-        assert (E.partition_bounds(cg, parts) == want).all(), parts
+        want = partition_owner(cg.core_vertex_count, cg.tree_vertex_count, cg.vertex_count,
+                               anchor, parts)
+        assert (E.partition_owner(cg, parts) == want).all(), parts
 
 
 def test_partitioned_corpus_all_starts(corpus):

@@ -7,42 +7,52 @@ import socket
 import numpy as np
 import pytest
 
-from paper_2009_07463_b200.multi import exchange_blobs, partition_bounds
-
-
-def check_bounds(b, nc, nt, n):
-    parts = b.shape[0]
-    assert b[0, 0] == 0 and b[-1, 1] == nc
-    for k in range(parts):
-        assert b[k, 0] % 32 == 0
-        if k + 1 < parts:
-            assert b[k, 1] == b[k + 1, 0] and b[k, 3] == b[k + 1, 2]
-    assert b[0, 2] == nc and b[-1, 3] == nc + nt
-    assert b[-1, 4] == nc + nt and b[-1, 5] == n
-    for k in range(parts - 1):
-        assert b[k, 4] == b[k, 5] == n
+from paper_2009_07463_b200.multi import exchange_blobs, partition_owner
 
 
 @pytest.mark.parametrize("parts", [1, 2, 3, 8, 16])
-def test_partition_bounds_cover_everything(parts):
+def test_partition_owner_rule(parts):
+    """Core: 32-vertex words (the 64K hubs), then 256-vertex blocks, dealt round
+    robin; trees follow their anchor;
+    component trees and isolated vertices to the last partition. Every
+    partition gets a near-equal share of the core and of its degree mass."""
     rng = np.random.default_rng(parts)
-    nc, nt, nz = 10_000, 3_000, 500
+    nc, nt, nz = 100_000, 3_000, 500
     attached = np.sort(rng.integers(0, nc, size=nt - 40)).astype(np.uint64)
     anchor = np.concatenate([attached, np.full(40, 0xFFFFFFFF, np.uint64)])
-    b = partition_bounds(nc, nt, nc + nt + nz, anchor, parts)
-    check_bounds(b, nc, nt, nc + nt + nz)
-    # every attached tree vertex lands in the partition owning its anchor
+    n = nc + nt + nz
+    own = partition_owner(nc, nt, n, anchor, parts)
+    assert own.shape == (n,) and own.max() < parts
+    for v in (0, 31, 32, 65535):  # hub region: 32-vertex words
+        assert own[v] == (v // 32) % parts
+    for v in (65536, 65536 + 255, 65536 + 256, nc - 1):  # then 256-vertex blocks
+        assert own[v] == ((v - 65536) // 256) % parts
     for t, a in enumerate(attached):
-        k = int(np.searchsorted(b[:, 0], a, side="right") - 1)
-        assert b[k, 2] <= nc + t < b[k, 3]
+        assert own[nc + t] == own[int(a)]
+    assert (own[nc + nt - 40:] == parts - 1).all()
+    counts = np.bincount(own[:nc], minlength=parts)
+    assert counts.max() - counts.min() <= 256 + 32
 
 
-def test_partition_bounds_tiny_and_errors():
-    b = partition_bounds(5, 0, 5, np.zeros(0, np.uint64), 4)
-    check_bounds(b, 5, 0, 5)
-    assert (b[:3, 1] == 0).all()  # 5 vertices fit one word: all owned by the last part
+def test_partition_owner_balances_kronecker_degree_mass():
+    """On a Kronecker s18 degree sequence sorted descending (as relaid core ids
+    are), the round-robin ownership spreads the degree mass (the top-down work)
+    far more evenly than equal id ranges (Eq. 1) would."""
+    import oracle as O
+    from paper_2009_07463_b200.multi import core_owner
+    c = O.OracleCsr(1 << 18, O.oracle_generate(18, 16, 1))
+    deg = np.sort(c.degrees().astype(np.float64))[::-1]
+    deg = deg[deg > 0]
+    for parts, bound in ((2, 1.05), (8, 1.25)):
+        mass = np.bincount(core_owner(np.arange(len(deg)), parts), weights=deg, minlength=parts)
+        ranges = np.bincount(np.arange(len(deg)) * parts // len(deg), weights=deg, minlength=parts)
+        assert mass.max() / mass.mean() <= bound, parts
+        assert ranges.max() / ranges.mean() > 1.4, parts
+
+
+def test_partition_owner_errors():
     with pytest.raises(ValueError):
-        partition_bounds(10, 0, 10, np.zeros(0, np.uint64), 17)
+        partition_owner(10, 0, 10, np.zeros(0, np.uint64), 17)
 
 
 def _worker(rank, world, port, q):
@@ -85,18 +95,16 @@ def _merge_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    n, nc, nt = 200, 96, 60
+    n, nc, nt = 2000, 960, 600
     rng = np.random.default_rng(7)
     anchor = np.concatenate([np.sort(rng.integers(0, nc, nt - 5)), np.full(5, 0xFFFFFFFF)])
-    b = partition_bounds(nc, nt, n, anchor.astype(np.uint64), world)
+    own = partition_owner(nc, nt, n, anchor.astype(np.uint64), world)
     truth = rng.integers(-2**62, 2**62, n, dtype=np.int64)
     truth[::7] = -1  # unreached entries are all ones
-    # junk outside the owned ranges, the owner's values inside them
-    mine = np.zeros(n, bool)
-    for lo, hi in ((b[rank, 0], b[rank, 1]), (b[rank, 2], b[rank, 3]), (b[rank, 4], b[rank, 5])):
-        mine[int(lo):int(hi)] = True
+    # junk outside the owned vertices, the owner's values on them
+    mine = own == rank
     local = torch.from_numpy(np.where(mine, truth, 999).astype(np.int64))
-    full = merge_owned(local, b[rank], dist)
+    full = merge_owned(local, torch.from_numpy(mine), dist)
     q.put((rank, bool((full.numpy() == truth).all())))
     dist.barrier()
     dist.destroy_process_group()
