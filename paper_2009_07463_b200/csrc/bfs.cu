@@ -71,8 +71,10 @@ __device__ __forceinline__ uint32_t whi_of(const BfsParams& p) { return p.nwords
 __device__ __forceinline__ unsigned cta_of(const BfsParams&) { return blockIdx.x; }
 __device__ __forceinline__ unsigned ncta_of(const BfsParams&) { return gridDim.x; }
 __device__ __forceinline__ uint32_t seg_off(const BfsParams&, uint32_t) { return 0; }
-// bitmap word of the i-th word a bottom-up step sweeps
+// bitmap word of the i-th word a bottom-up step sweeps, and of the k-th word of
+// an aligned run of 8 starting at index i0 (run_word: one mapping per run)
 __device__ __forceinline__ uint64_t word_at(const BfsParams&, uint64_t i) { return i; }
+template <class P> struct IsPart { static constexpr bool value = false; };
 
 struct WarpSmem {
   uint32_t cbuf[kCbuf];     // staged claims (top-down); with win: deferred misses (bottom-up)
@@ -167,6 +169,7 @@ __device__ void flush_claims(const P& p, const uint32_t* cbuf, const int32_t* cd
     const uint32_t take = d[k] != 0;
     const uint32_t kin = warp_incl_scan(take), din = warp_incl_scan(d[k]);
     if (take) {
+      ETB_DCHECK(vpos + kin - 1 <= p.nc && v < p.nc);
       qv_out[vpos + kin - 1] = v;
       qp_out[vpos + kin - 1] = epos + din - d[k];
     }
@@ -253,6 +256,7 @@ __device__ void td_step(const P& p, uint32_t* cbuf, int32_t* win, const uint32_t
       if (single) {  // one row: its vertex and row start once for the chunk
         const uint32_t uu = root != kNone32 ? root : qv[i];
         const uint64_t base = p.crow[uu] + seg_off(p, uu) + (e0 - qi);
+        ETB_DCHECK(uu < p.nc && base + (e1 - e0) <= p.crow[uu + 1]);
 #pragma unroll
         for (int j = 0; j < kEpl; ++j) {
           const uint32_t rel = lane + 32 * j;
@@ -274,11 +278,15 @@ __device__ void td_step(const P& p, uint32_t* cbuf, int32_t* win, const uint32_t
           uint32_t col = kNone32;
           if (u[j] != kNone32) {
             const uint64_t vs = w[j] == 0 ? qi : e0 + static_cast<uint64_t>(max(win[w[j]], 0));
+          ETB_DCHECK(u[j] < p.nc && e0 + rel >= vs &&
+                     p.crow[u[j]] + seg_off(p, u[j]) + (e0 + rel - vs) < p.crow[u[j] + 1]);
             col = p.ccol[p.crow[u[j]] + seg_off(p, u[j]) + (e0 + rel - vs)];
           }
           w[j] = col;
         }
       }
+#pragma unroll
+      for (int j = 0; j < kEpl; ++j) ETB_DCHECK(w[j] == kNone32 || w[j] < p.nc);
       // With a list to emit (small frontiers) every target's {core, full}
       // degree is fetched with its visited word, off the claim's critical path;
       // without one only the claimed targets' full degree is read.
@@ -439,6 +447,7 @@ __device__ __forceinline__ void scan_rows2(const P& p, const uint32_t* fcur, uin
                                            uint32_t& pa, uint32_t& pb, bool& ha, bool& hb) {
   ha = hb = false;
   while (ea < enda || eb < endb) {
+    ETB_DCHECK(enda <= p.crow[p.nc] && endb <= p.crow[p.nc]);
     const uint32_t x0 = ea < enda ? p.ccol[ea] : kNone32;
     const uint32_t x1 = ea + 1 < enda ? p.ccol[ea + 1] : kNone32;
     const uint32_t y0 = eb < endb ? p.ccol[eb] : kNone32;
@@ -553,24 +562,36 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
   for (uint64_t w0 = wlo_of(p) + gw * kU; w0 < whi_of(p); w0 += nw * kU) {
+    // the run's words: w0 + k (one partition), or one owned-word mapping per
+    // run (partitioned: aligned runs of 8 are 8 hub words G apart or one block)
+    uint64_t wb = 0, ws = 0;
+    if constexpr (IsPart<P>::value) {
+      static_assert(kU == 8, "partition runs are aligned 8-word runs");
+      wb = word_at(p, w0);
+      ws = run_stride(p, w0);
+    }
+    auto wrd = [&](int k) -> uint64_t {
+      if constexpr (IsPart<P>::value) return wb + k * ws;
+      else return w0 + k;
+    };
     uint32_t vis[kU];
     bool any = false;
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
-      vis[k] = w0 + k < whi_of(p) ? p.visited[word_at(p, w0 + k)] : ~0u;
+      vis[k] = w0 + k < whi_of(p) ? p.visited[wrd(k)] : ~0u;
       any |= vis[k] != ~0u;
     }
     if (!any) continue;
     uint32_t f[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k)
-      f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[word_at(p, w0 + k) * 32 + lane];
+      f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[wrd(k) * 32 + lane];
     bool hit[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
-      const uint64_t wk = word_at(p, w0 + k);
+      const uint64_t wk = wrd(k);
       const uint32_t v = static_cast<uint32_t>(wk * 32 + lane);
       const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
       if (hit[k]) {
@@ -583,6 +604,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       }
       const bool miss = f[k] != kNone32 && !hit[k];
       const unsigned mm = __ballot_sync(0xffffffffu, miss);
+      ETB_DCHECK(nmiss + 32 <= kMissCap && v < p.nc);
       if (miss) mbuf[nmiss + __popc(mm & lt)] = v;
       nmiss += __popc(mm);
     }
@@ -590,7 +612,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       uint32_t av[kU], ad[kU];
 #pragma unroll
       for (int k = 0; k < kU; ++k) {
-        av[k] = static_cast<uint32_t>(word_at(p, w0 + k) * 32 + lane);
+        av[k] = static_cast<uint32_t>(wrd(k) * 32 + lane);
         ad[k] = hit[k] ? p.cmeta[av[k]].x : 0u;
       }
       bu_append<kU>(av, ad, qv_out, qp_out, lslot);
@@ -616,8 +638,13 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
   // and works through the words with unvisited vertices kBuU at a time, so
   // late levels (few unvisited left) skip full words without a round trip each.
   for (uint64_t b0 = wlo_of(p) + gw * kSweep; b0 < whi_of(p); b0 += nw * kSweep) {
-    const uint32_t mine =
-        lane < kSweep && b0 + lane < whi_of(p) ? p.visited[word_at(p, b0 + lane)] : ~0u;
+    uint32_t myw = 0, mine;
+    if constexpr (IsPart<P>::value) {
+      myw = static_cast<uint32_t>(word_at(p, b0 + lane));
+      mine = lane < kSweep && b0 + lane < whi_of(p) ? p.visited[myw] : ~0u;
+    } else {
+      mine = lane < kSweep && b0 + lane < whi_of(p) ? p.visited[b0 + lane] : ~0u;
+    }
     unsigned todo = __ballot_sync(0xffffffffu, mine != ~0u);
     while (todo) {
       uint32_t vis[kBuU], wi[kBuU];
@@ -625,7 +652,10 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
       for (int k = 0; k < kBuU; ++k) {
         const int j = todo ? __ffs(todo) - 1 : 0;
         vis[k] = todo ? __shfl_sync(0xffffffffu, mine, j) : ~0u;
-        wi[k] = static_cast<uint32_t>(word_at(p, b0 + j));
+        if constexpr (IsPart<P>::value)
+          wi[k] = __shfl_sync(0xffffffffu, myw, j);
+        else
+          wi[k] = static_cast<uint32_t>(b0) + j;
         todo &= todo - 1;
       }
       uint32_t f[kBuU];
@@ -649,7 +679,8 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
         }
         const bool miss = f[k] != kNone32 && !hit[k];
         const unsigned mm = __ballot_sync(0xffffffffu, miss);
-        if (miss) mbuf[nmiss + __popc(mm & lt)] = v;
+        ETB_DCHECK(nmiss + 32 <= kMissCap && v < p.nc);
+      if (miss) mbuf[nmiss + __popc(mm & lt)] = v;
         nmiss += __popc(mm);
       }
       if (lslot) {
@@ -737,6 +768,13 @@ __device__ unsigned long long scout_pass(const BfsParams& p, const uint32_t* f,
   claims += c;
   return s;
 }
+
+// Tree entries in flight per thread in the replay (two dependent round trips
+// each: the tree arrays, then the anchor's visited bit and depth).
+#ifndef ETB_REPLAY
+#define ETB_REPLAY 4
+#endif
+constexpr int kReplay = ETB_REPLAY;
 
 // kLarge: the 1024-thread instantiation (cores of >= 2^23 vertices), the only
 // one whose top-down levels can claim a large share of the core at once.
@@ -1031,10 +1069,10 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
   // Replay (TEET/TEOLV, et_bfs.cpp:14-32): the tree arrays and, per anchor, its
   // visited bit and depth are fetched together (two dependent round trips;
   // an unreached anchor's stale depth is simply ignored).
-  for (uint64_t t0 = tid; t0 < p.nt; t0 += 4 * nthreads) {
-    uint32_t a[4], td[4], ts[4], vis[4], da[4];
+  for (uint64_t t0 = tid; t0 < p.nt; t0 += kReplay * nthreads) {
+    uint32_t a[kReplay], td[kReplay], ts[kReplay], vis[kReplay], da[kReplay];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kReplay; ++k) {
       const uint64_t t = t0 + k * nthreads;
       const uint32_t tv = static_cast<uint32_t>(p.nc + t);
       const bool in = t < p.nt && !(tv >= p.skip_lo && tv < p.skip_hi);
@@ -1043,13 +1081,13 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
       ts[k] = in ? p.tsrc[t] : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kReplay; ++k) {
       const bool ok = a[k] < kNone32 - 1;
       vis[k] = ok ? test_bit(p.visited, a[k]) : 0u;
       da[k] = ok ? __ldcg(&p.dp[a[k]].x) : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kReplay; ++k) {
       if (a[k] == kNone32 - 1) continue;  // out of range or inside the start's tree
       p.dp[p.nc + t0 + k * nthreads] =
           vis[k] ? make_uint2(da[k] + td[k], ts[k]) : make_uint2(kNone32, kNone32);
@@ -1147,6 +1185,11 @@ __device__ __forceinline__ uint32_t whi_of(const PartView& v) { return v.nwo; }
 __device__ __forceinline__ unsigned cta_of(const PartView& v) { return v.cta; }
 __device__ __forceinline__ unsigned ncta_of(const PartView& v) { return v.ncta; }
 __device__ __forceinline__ uint32_t seg_off(const PartView&, uint32_t) { return 0; }
+template <> struct IsPart<PartView> { static constexpr bool value = true; };
+// stride of the aligned 8-word run starting at owned index i0
+__device__ __forceinline__ uint64_t run_stride(const PartView& v, uint64_t i0) {
+  return i0 < v.nhub ? v.nparts : 1;
+}
 __device__ __forceinline__ uint64_t word_at(const PartView& v, uint64_t i) {
   return owned_word(static_cast<uint32_t>(i), v.part, v.nparts, v.nhub);
 }
@@ -1283,6 +1326,7 @@ __device__ void part_push(const PartParams& pp, uint32_t part, const PartView& v
       if (q == part || !in) continue;
       const PartDev& pq = pp.parts[q];
       uint32_t* dst = ring == 0 ? pq.fb0 : (ring == 1 ? pq.fb1 : pq.fb2);
+      ETB_DCHECK(wi < v.nwords);
       dst[wi] = f;
     }
     if (kCount) {
@@ -1405,8 +1449,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
           bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
         else
-          bu_step<kLarge ? kBuU : kBuUSmall>(v, mb, fcur, fnext, dnext, claims_acc, nullptr,
-                                             nullptr, nullptr);
+          bu_step<kBuU>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
         if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
         group_sync(me.bar, gsize);  // the owned next words are final
         unsigned long long none = 0;
@@ -1421,8 +1464,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
           bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
         else
-          bu_step<kLarge ? kBuU : kBuUSmall>(v, mb, fcur, fnext, dnext, claims_acc, nullptr,
-                                             nullptr, nullptr);
+          bu_step<kBuU>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
         claims_acc = 0;
         if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
         group_sync(me.bar, gsize);

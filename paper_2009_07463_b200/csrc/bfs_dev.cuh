@@ -3,6 +3,21 @@
 
 #include "bfs.cuh"
 
+// Checked builds (-DETB_DEBUG_CHECKS, tools/build_variant.py): bounds and
+// capacity asserts on the traversal's index arithmetic, trapping on the first
+// violation (compute-sanitizer is closed on this pool; the checked library is
+// run over the GPU parity suites instead).
+#ifdef ETB_DEBUG_CHECKS
+#define ETB_DCHECK(c)   \
+  do {                  \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define ETB_DCHECK(c) \
+  do {                \
+  } while (0)
+#endif
+
 namespace etb {
 namespace dev {
 

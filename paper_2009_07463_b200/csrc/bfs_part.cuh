@@ -5,8 +5,8 @@
 // the hubs — most top-down edges — and the last partition the low-degree
 // vertices, most bottom-up misses. As the paper's static round-robin shuffle
 // (SRRS, Alg. 4) does for its NUMA segments, ownership is distributed round
-// robin over the degree order — the 64K hubs one 32-vertex word at a time,
-// the rest in 256-vertex blocks (8 bitmap words = one 32-byte sector, so the
+// robin over the degree order — the top 8K·G hubs one 32-vertex word at a
+// time, the rest in 256-vertex blocks (8 bitmap words = one 32-byte sector, so the
 // exchanged bitmap words stay whole sectors) — and the edge trees anchored in
 // them; component trees and isolated vertices go to the last partition.
 //
@@ -36,25 +36,34 @@ constexpr int kMaxParts = 16;
 // u64 counters at the start of a partition's exchange block (bfs.cu: two
 // parities of level slots, launch bookkeeping); the arrival counter follows.
 constexpr uint64_t kCtrWords = 64;
-// Ownership granularity: the first kPartHubWords bitmap words (the 64K
-// highest-degree core vertices) are dealt one word (32 vertices) at a time,
-// the rest in blocks of kPartBlockWords words (256 vertices, one 32-byte
-// sector of bitmap): at s22 the top 256-vertex block alone holds 6% of the
-// degree mass (G = 8: 1.33x the mean share) against 1.5% for the top word.
-constexpr uint32_t kPartHubWords = 2048;
+// Ownership granularity: the first kPartHubWordsPer·G bitmap words (the
+// highest-degree core vertices: 16K at G = 2, 64K at G = 8) are dealt one word
+// (32 vertices) at a time, the rest in blocks of kPartBlockWords words (256
+// vertices, one 32-byte sector of bitmap): at s22 the top 256-vertex block
+// alone holds 6% of the degree mass (G = 8: 1.33x the mean share) against 1.5%
+// for the top word. Every partition then owns a multiple of 8 hub words, so
+// an aligned run of 8 owned words is either 8 hub words G apart or one block.
+constexpr uint32_t kPartHubWordsPer = 256;
 constexpr uint32_t kPartBlockWords = 8;
+
+__host__ __device__ __forceinline__ uint32_t hub_words(uint32_t G) { return kPartHubWordsPer * G; }
 
 // Owner of core vertex v among G partitions.
 __host__ __device__ __forceinline__ uint32_t core_owner(uint32_t v, uint32_t G) {
   const uint32_t w = v >> 5;
-  return w < kPartHubWords ? w % G : ((w - kPartHubWords) / kPartBlockWords) % G;
+  return w < hub_words(G) ? w % G : ((w - hub_words(G)) / kPartBlockWords) % G;
+}
+// Hub words (the one-word-at-a-time region) owned by partition k of G.
+__host__ __device__ __forceinline__ uint32_t owned_hub_words(uint32_t nwords, uint32_t k,
+                                                             uint32_t G) {
+  const uint32_t hn = nwords < hub_words(G) ? nwords : hub_words(G);
+  return hn > k ? (hn - 1 - k) / G + 1 : 0;
 }
 // Bitmap words owned by partition k of G (nwords words in all).
 __host__ __device__ __forceinline__ uint32_t owned_words(uint32_t nwords, uint32_t k, uint32_t G) {
-  const uint32_t hn = nwords < kPartHubWords ? nwords : kPartHubWords;
-  const uint32_t hub = hn > k ? (hn - 1 - k) / G + 1 : 0;
-  if (nwords <= kPartHubWords) return hub;
-  const uint32_t tn = nwords - kPartHubWords;
+  const uint32_t hub = owned_hub_words(nwords, k, G);
+  if (nwords <= hub_words(G)) return hub;
+  const uint32_t tn = nwords - hub_words(G);
   const uint32_t nb = (tn + kPartBlockWords - 1) / kPartBlockWords;
   if (k >= nb) return hub;
   const uint32_t blocks = (nb - 1 - k) / G + 1;  // k, k + G, ... < nb
@@ -62,18 +71,12 @@ __host__ __device__ __forceinline__ uint32_t owned_words(uint32_t nwords, uint32
   const uint32_t in_last = tn - last * kPartBlockWords;
   return hub + (blocks - 1) * kPartBlockWords + (in_last < kPartBlockWords ? in_last : kPartBlockWords);
 }
-// Hub words (the one-word-at-a-time region) owned by partition k of G.
-__host__ __device__ __forceinline__ uint32_t owned_hub_words(uint32_t nwords, uint32_t k,
-                                                             uint32_t G) {
-  const uint32_t hn = nwords < kPartHubWords ? nwords : kPartHubWords;
-  return hn > k ? (hn - 1 - k) / G + 1 : 0;
-}
 // The j-th owned word of partition k of G, which owns nhub hub words.
 __host__ __device__ __forceinline__ uint32_t owned_word(uint32_t j, uint32_t k, uint32_t G,
                                                        uint32_t nhub) {
   if (j < nhub) return j * G + k;
   j -= nhub;
-  return kPartHubWords + ((j / kPartBlockWords) * G + k) * kPartBlockWords + j % kPartBlockWords;
+  return hub_words(G) + ((j / kPartBlockWords) * G + k) * kPartBlockWords + j % kPartBlockWords;
 }
 
 // Device-visible descriptor of one partition. Pointers must be valid on the

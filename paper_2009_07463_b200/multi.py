@@ -4,7 +4,7 @@
   degree-sorted core is dealt round robin, as the paper's static round-robin
   shuffle (SRRS, Alg. 4) balances its segments (the equal ranges of Eq. 1,
   proj/src/preprocess.cpp:77, would give one partition every hub) — the first
-  2048 bitmap words (64K hubs) one 32-vertex word at a time, the rest in
+  256·G bitmap words (8K·G hubs) one 32-vertex word at a time, the rest in
   256-vertex blocks; a tree vertex follows its anchor; component trees and
   isolated vertices go to the last partition.
 * ``exchange_blobs`` / ``connect`` wire one process per GPU: each rank exports
@@ -24,14 +24,15 @@ import ctypes as C
 import numpy as np
 
 NONE32 = 0xFFFFFFFF
-HUB_WORDS = 2048   # bitmap words dealt one at a time
-BLOCK_WORDS = 8    # the rest: 256-vertex blocks
+HUB_WORDS_PER = 256  # x G bitmap words dealt one at a time
+BLOCK_WORDS = 8      # the rest: 256-vertex blocks
 
 
 def core_owner(v, parts):
     w = np.asarray(v, np.uint64) >> np.uint64(5)
-    hub = w < HUB_WORDS
-    tail = (w - np.minimum(w, HUB_WORDS)) // BLOCK_WORDS
+    hw = HUB_WORDS_PER * parts
+    hub = w < hw
+    tail = (w - np.minimum(w, hw)) // BLOCK_WORDS
     return np.where(hub, w % parts, tail % parts).astype(np.uint32)
 
 

@@ -12,7 +12,7 @@ from paper_2009_07463_b200.multi import exchange_blobs, partition_owner
 
 @pytest.mark.parametrize("parts", [1, 2, 3, 8, 16])
 def test_partition_owner_rule(parts):
-    """Core: 32-vertex words (the 64K hubs), then 256-vertex blocks, dealt round
+    """Core: 32-vertex words (the 8K·G hubs), then 256-vertex blocks, dealt round
     robin; trees follow their anchor;
     component trees and isolated vertices to the last partition. Every
     partition gets a near-equal share of the core and of its degree mass."""
@@ -23,10 +23,12 @@ def test_partition_owner_rule(parts):
     n = nc + nt + nz
     own = partition_owner(nc, nt, n, anchor, parts)
     assert own.shape == (n,) and own.max() < parts
-    for v in (0, 31, 32, 65535):  # hub region: 32-vertex words
+    hub = 256 * parts * 32  # hub region: 32-vertex words dealt one at a time
+    for v in (0, 31, 32, min(hub, nc) - 1):
         assert own[v] == (v // 32) % parts
-    for v in (65536, 65536 + 255, 65536 + 256, nc - 1):  # then 256-vertex blocks
-        assert own[v] == ((v - 65536) // 256) % parts
+    for v in (hub, hub + 255, hub + 256, nc - 1):  # then 256-vertex blocks
+        if hub <= v < nc:
+            assert own[v] == ((v - hub) // 256) % parts
     for t, a in enumerate(attached):
         assert own[nc + t] == own[int(a)]
     assert (own[nc + nt - 40:] == parts - 1).all()

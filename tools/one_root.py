@@ -22,9 +22,12 @@ def main():
     ap.add_argument("--mh", type=int, default=-1)
     ap.add_argument("--index", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--parts", type=int, default=1, help="1D core partitions on this device")
     args = ap.parse_args()
     g = eb.generate_graph(scale=args.scale, edgefactor=args.edgefactor, seed=1)
     cg = eb.relayout_csr(g, mh=args.mh)
+    if args.parts > 1:
+        E.partition(cg, args.parts)
     roots = select_roots_from_degrees(g.degrees(), 64, 1)
     s = int(cg.old2new[int(roots[args.index])])
     ms, kms = E.time_roots(cg, np.full(args.reps, s, np.uint64), warmup=0, flush_l2=True)
