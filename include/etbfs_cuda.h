@@ -260,6 +260,9 @@ int etb_debug_warp_stamps(etb_layout* L, uint64_t start, int32_t depth, uint64_t
  * init end, [2 + L] level L end, [128 + L] conversion before level L end,
  * [255] replay end) and, at [192 + L], top-down level L's frontier edge count. */
 int etb_debug_phase_stamps(etb_layout* L, uint64_t* out256);
+/* Diagnostics (libraries built with -DETB_DEBUG_CHECKS; 0 otherwise): the
+ * source line of the first failed device bounds check since the last call. */
+int etb_debug_check_line(uint32_t* line);
 /* Diagnostics: median event-timed duration (us) of an empty kernel launched
  * like the traversal (same grid, block, shared memory, cooperative). */
 int etb_debug_launch_floor(etb_layout* L, int iters, double* empty_us);

@@ -57,6 +57,11 @@ constexpr int kCbuf = kTdChunk;      // staged claims of one chunk (u32 vertex i
 // 7 on the small-core one (s22: 5/6/7 all -0.5..-1 us per root against 8, 7 best)
 constexpr int kBuU = 8, kBuUSmall = 7;
 constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab on long levels
+// bu_step loads the first neighbours together with the visited words (1) or
+// after them, for the unvisited lanes only (0)
+#ifndef ETB_BU_EAGER
+#define ETB_BU_EAGER 0
+#endif
 // BfsParams::td_as_bu default (env ETB_TD_AS_BU overrides; 0 = off): s26 +6%
 // harmonic-mean GTEPS (slowest roots 0.80 -> 0.62-0.68 ms), s22 neutral
 constexpr double kTdAsBuDefault = 4.0;  // measured best at s26 (3..5 equal, 6 and up: no level)
@@ -576,6 +581,23 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
     };
     uint32_t vis[kU];
     bool any = false;
+#if ETB_BU_EAGER
+    // first neighbours loaded with the visited words, not after them (one
+    // round trip less per iteration; bu_step runs on levels where most of the
+    // core is unvisited, so few of these loads are wasted)
+    uint32_t cf[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const uint64_t x = wrd(k) * 32 + lane;
+      vis[k] = w0 + k < whi_of(p) ? p.visited[wrd(k)] : ~0u;
+      cf[k] = w0 + k < whi_of(p) && x < p.nc ? p.cfirst[x] : kNone32;
+      any |= vis[k] != ~0u;
+    }
+    if (!any) continue;
+    uint32_t f[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : cf[k];
+#else
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
       vis[k] = w0 + k < whi_of(p) ? p.visited[wrd(k)] : ~0u;
@@ -586,6 +608,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
 #pragma unroll
     for (int k = 0; k < kU; ++k)
       f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[wrd(k) * 32 + lane];
+#endif
     bool hit[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
@@ -604,7 +627,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       }
       const bool miss = f[k] != kNone32 && !hit[k];
       const unsigned mm = __ballot_sync(0xffffffffu, miss);
-      ETB_DCHECK(nmiss + 32 <= kMissCap && v < p.nc);
+      ETB_DCHECK(nmiss + 32 <= kMissCap && (!miss || v < p.nc));
       if (miss) mbuf[nmiss + __popc(mm & lt)] = v;
       nmiss += __popc(mm);
     }
@@ -679,7 +702,7 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
         }
         const bool miss = f[k] != kNone32 && !hit[k];
         const unsigned mm = __ballot_sync(0xffffffffu, miss);
-        ETB_DCHECK(nmiss + 32 <= kMissCap && v < p.nc);
+        ETB_DCHECK(nmiss + 32 <= kMissCap && (!miss || v < p.nc));
       if (miss) mbuf[nmiss + __popc(mm & lt)] = v;
         nmiss += __popc(mm);
       }
@@ -774,6 +797,7 @@ __device__ unsigned long long scout_pass(const BfsParams& p, const uint32_t* f,
 #ifndef ETB_REPLAY
 #define ETB_REPLAY 4
 #endif
+
 constexpr int kReplay = ETB_REPLAY;
 
 // kLarge: the 1024-thread instantiation (cores of >= 2^23 vertices), the only
@@ -1623,6 +1647,19 @@ const void* part_kernel_for(int block) {
 }
 
 size_t bfs_smem_bytes() { return sizeof(Smem); }
+
+// Checked builds: the source line of the first failed device check (0: none,
+// or an unchecked build); reading it clears it.
+unsigned debug_check_line() {
+#ifdef ETB_DEBUG_CHECKS
+  unsigned v = 0, z = 0;
+  ETB_CUDA(cudaMemcpyFromSymbol(&v, etb_check_line, 4));
+  ETB_CUDA(cudaMemcpyToSymbol(etb_check_line, &z, 4));
+  return v;
+#else
+  return 0;
+#endif
+}
 
 int block_for(uint64_t nc) {
   if (const char* e = getenv("ETB_BFS_BLOCK")) {

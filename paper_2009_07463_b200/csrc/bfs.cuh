@@ -112,6 +112,7 @@ void bfs_launch(const BfsParams& p, BfsState& S, cudaStream_t s);
 void bfs_prepare_start(const DevLayout& L, BfsState& S, uint64_t start, BfsParams& p,
                        cudaStream_t s);
 void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p);
+unsigned debug_check_line();  // checked builds: first failed device check's line
 
 // work.cu: the algorithmic work of the traversal whose result is dp, from its
 // depths and the direction trace of its nl levels (see work.cu): levels[4 L + k]

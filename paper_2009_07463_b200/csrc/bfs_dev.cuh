@@ -4,13 +4,15 @@
 #include "bfs.cuh"
 
 // Checked builds (-DETB_DEBUG_CHECKS, tools/build_variant.py): bounds and
-// capacity asserts on the traversal's index arithmetic, trapping on the first
-// violation (compute-sanitizer is closed on this pool; the checked library is
-// run over the GPU parity suites instead).
+// capacity asserts on the traversal's index arithmetic; the first violation's
+// source line is recorded in etb_check_line (read by etb_debug_check_line) —
+// compute-sanitizer is closed on this pool, so the checked library is run over
+// the GPU parity suites instead.
 #ifdef ETB_DEBUG_CHECKS
-#define ETB_DCHECK(c)   \
-  do {                  \
-    if (!(c)) __trap(); \
+static __device__ unsigned int etb_check_line = 0;  // per translation unit
+#define ETB_DCHECK(c)                                     \
+  do {                                                    \
+    if (!(c)) atomicCAS(&::etb_check_line, 0u, __LINE__); \
   } while (0)
 #else
 #define ETB_DCHECK(c) \

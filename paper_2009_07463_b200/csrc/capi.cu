@@ -828,6 +828,13 @@ int etb_time_roots_wall(etb_layout* h, const uint64_t* starts, uint64_t count, i
   });
 }
 
+int etb_debug_check_line(uint32_t* line) {
+  return guarded([&] {
+    need(line, "etb_debug_check_line");
+    *line = etb::debug_check_line();
+  });
+}
+
 int etb_debug_phase_stamps(etb_layout* h, uint64_t* out256) {
   return guarded([&] {
     need(h, "etb_debug_phase_stamps");
