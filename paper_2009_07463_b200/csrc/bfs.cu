@@ -1337,7 +1337,7 @@ __device__ void part_convert(const PartView& v, const uint64_t* trow, const uint
 // claims (popcount) and α/β scout (Σ full degree, coalesced: lane = vertex).
 template <bool kCount>
 __device__ void part_push(const PartParams& pp, uint32_t part, const PartView& v, uint32_t ring,
-                          const uint32_t* fnext, unsigned long long& claims,
+                          bool dense, const uint32_t* fnext, unsigned long long& claims,
                           unsigned long long& scout) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)wib * v.ncta + v.cta;
@@ -1346,8 +1346,13 @@ __device__ void part_push(const PartParams& pp, uint32_t part, const PartView& v
     const bool in = j0 + lane < v.nwo;
     const uint32_t wi = in ? static_cast<uint32_t>(word_at(v, j0 + lane)) : 0u;
     const uint32_t f = in ? __ldcg(&fnext[wi]) : 0u;
+    // Replica slots are cleared whole by their holder one level ahead (before
+    // the barrier after which peers push into them), so past level 0 only
+    // words with claims travel and sparse top-down levels push little; level
+    // 0's slot was not (a peer may reach its first push before this launch's
+    // init), so level 0 pushes every owned word.
     for (uint32_t q = 0; q < pp.nparts; ++q) {
-      if (q == part || !in) continue;
+      if (q == part || !in || (!dense && f == 0u)) continue;
       const PartDev& pq = pp.parts[q];
       uint32_t* dst = ring == 0 ? pq.fb0 : (ring == 1 ? pq.fb1 : pq.fb2);
       ETB_DCHECK(wi < v.nwords);
@@ -1432,6 +1437,8 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
     for (uint64_t i = gtid; i < p.nwords; i += gthreads)  // a bottom-up level 0 probes it all
       me.fb0[i] = i == sw ? sb : 0u;
     for (uint64_t j = gtid; j < me.nwo; j += gthreads) {
+      // owned words only: peers may push level 0's words into the others
+      // before this init is done
       const uint32_t i = static_cast<uint32_t>(word_at(v, j));
       uint32_t vis = i == sw ? sb : 0u;
       if (i == p.nwords - 1 && tail) vis |= ~0u << tail;
@@ -1456,7 +1463,9 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
       uint32_t* fnext = F[(L + 1) % 3];
       uint32_t* fzero = F[(L + 2) % 3];
       unsigned long long* slot = ctr + (L & 3) * 4;
-      for (uint64_t j = gtid; j < me.nwo; j += gthreads) fzero[word_at(v, j)] = 0;  // owned words
+      // the whole replica slot (owned words and the peers' pushed words: a
+      // peer pushes only its nonzero words into it, after the next barrier)
+      for (uint64_t i = gtid; i < p.nwords; i += gthreads) fzero[i] = 0;
       if (gtid == 0) {
         ctr[((L + 2) & 3) * 4 + 0] = 0;
         ctr[((L + 2) & 3) * 4 + 1] = 0;
@@ -1477,7 +1486,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
         group_sync(me.bar, gsize);  // the owned next words are final
         unsigned long long none = 0;
-        part_push<false>(pp, part, v, (L + 1) % 3, fnext, none, none);
+        part_push<false>(pp, part, v, (L + 1) % 3, L == 0, fnext, none, none);
       } else if (p.td_as_bu > 0.0 && L > 0 &&
                  (double)scout > p.td_as_bu * (double)(p.nc - reached)) {
         // a top-down level executed as a bottom-up sweep over the owned
@@ -1492,7 +1501,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         claims_acc = 0;
         if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
         group_sync(me.bar, gsize);
-        part_push<true>(pp, part, v, (L + 1) % 3, fnext, claims_acc, scout_acc);
+        part_push<true>(pp, part, v, (L + 1) % 3, L == 0, fnext, claims_acc, scout_acc);
       } else {
         etc -= (double)scout;
         uint64_t nq = 0, ne = 0;
@@ -1508,12 +1517,25 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
           nq = sm.tot[2] >> kItemShift;
           ne = sm.tot[2] & kItemMask;
         }
-        td_step<3, kLarge>(vt, mb, sm.w[threadIdx.x >> 5].win, me.qv, me.qp, nq, ne, nullptr,
-                           nullptr, fnext, slot, dnext, scout_acc, claims_acc,
-                           L == 0 ? start : kNone32);
+        // Levels with a small frontier claim with returning atomics, counting
+        // claims and scout as they go (most targets are unvisited: only the
+        // winners write); large ones claim atomic-free and count in the push
+        // pass (as the single-partition kernel's list-less levels).
+        const bool small = (double)scout < p.emit_limit;
+        if (small)
+          td_step<0, kLarge>(vt, mb, sm.w[threadIdx.x >> 5].win, me.qv, me.qp, nq, ne, nullptr,
+                             nullptr, fnext, slot, dnext, scout_acc, claims_acc,
+                             L == 0 ? start : kNone32);
+        else
+          td_step<3, kLarge>(vt, mb, sm.w[threadIdx.x >> 5].win, me.qv, me.qp, nq, ne, nullptr,
+                             nullptr, fnext, slot, dnext, scout_acc, claims_acc,
+                             L == 0 ? start : kNone32);
         if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
         group_sync(me.bar, gsize);
-        part_push<true>(pp, part, v, (L + 1) % 3, fnext, claims_acc, scout_acc);
+        if (small)
+          part_push<false>(pp, part, v, (L + 1) % 3, L == 0, fnext, claims_acc, scout_acc);
+        else
+          part_push<true>(pp, part, v, (L + 1) % 3, L == 0, fnext, claims_acc, scout_acc);
       }
       ++xk;
       part_level_sync(pp, part, par, sm, claims_acc, bu ? 0ull : scout_acc, (L & 3) * 4,
