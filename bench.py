@@ -441,6 +441,13 @@ def run_ours(args):
         write_report_v1(args, ctx["roots"], ctx["te"], ctx["sec"][:NROOTS], ctx["valid"],
                         p["preprocessing_s"], ctx["g"].vertex_count,
                         ctx["g"].undirected_edge_count())
+    if D.rank == 0 and D.world == 1 and args.tree_out:
+        # BenchConfig::tree_out (bench.hpp:45): the first root's tree, original ids, ETT1
+        import paper_2009_07463_b200 as eb
+        from paper_2009_07463_b200 import etbfs as E
+        E.bfs_device(ctx["cg"], int(ctx["starts"][0]))
+        _, par = E.result_original(ctx["cg"], levels=False)
+        eb.write_tree(args.tree_out, int(ctx["roots"][0]), par)
     if D.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, ctx)
     if D.world == 1 and args.emulate_partitions:
@@ -661,6 +668,8 @@ def main():
     ap.add_argument("--ref-roots-per-step", type=int, default=2)
     ap.add_argument("--report-json", default=None,
                     help="also write the reference's JSON report (schema v1, bench.cpp:301-343)")
+    ap.add_argument("--tree-out", default=None,
+                    help="write the first root's BFS tree (original ids) as an ETT1 file")
     ap.add_argument("--no-paper-mode", action="store_true",
                     help="skip the mh=0/TEOLV line at the headline scale")
     ap.add_argument("--secondary", default="22/16,24/4,28/16",

@@ -969,7 +969,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           bu_step<kLarge ? kBuU : kBuUSmall>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext,
                                              claims_acc, qv_in, qp_in,
                                              bu_list ? &slot[0] : nullptr);
-      } else if (p.td_as_bu > 0.0 && !(L == 1 && list_from_prologue) && L > 0 &&
+      } else if (p.td_as_bu > 0.0 && !p.top_down_only && !(L == 1 && list_from_prologue) && L > 0 &&
                  (double)ne > p.td_as_bu * (double)(p.nc - reached)) {
         // a top-down level (α/β state advanced as the reference's) executed as
         // a bottom-up sweep over the unvisited core against this frontier's
@@ -1487,7 +1487,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         group_sync(me.bar, gsize);  // the owned next words are final
         unsigned long long none = 0;
         part_push<false>(pp, part, v, (L + 1) % 3, L == 0, fnext, none, none);
-      } else if (p.td_as_bu > 0.0 && L > 0 &&
+      } else if (p.td_as_bu > 0.0 && !p.top_down_only && L > 0 &&
                  (double)scout > p.td_as_bu * (double)(p.nc - reached)) {
         // a top-down level executed as a bottom-up sweep over the owned
         // unvisited words (as et_bfs_body; decided on the frontier's full degree

@@ -61,9 +61,10 @@ struct BfsParams {
   double emit_limit;  // top-down levels with scout >= this skip work-item emission
   // A level the α/β rule runs top-down is executed as a frontier-restricted
   // bottom-up sweep when its frontier edges exceed td_as_bu x the unvisited core
-  // vertices (0 = never): the claimed set — the unvisited core vertices with a
-  // frontier neighbour — is the same, so depths, claims, scout and the α/β
-  // sequence are the reference's; only the GPU cost differs.
+  // vertices (0 = never; hybrid drivers only, CoreKernel::kTopDown stays
+  // top-down): the claimed set — the unvisited core vertices with a frontier
+  // neighbour — is the same, so depths, claims, scout and the α/β sequence are
+  // the reference's; only the GPU cost differs.
   double td_as_bu;
   int top_down_only;   // CoreKernel::kTopDown
   int bottom_up_only;  // CoreKernel::kBlockSearch: bottom-up levels to fixpoint
@@ -85,6 +86,7 @@ struct BfsState {
   DevBuf<uint2> dp;          // interleaved result: one 8-byte store per claim
   DevBuf<int32_t> tmp_depth;  // de-interleaved staging for host downloads
   DevBuf<uint32_t> tmp_parent;
+  DevBuf<uint64_t> tmp_parent64;
   DevBuf<char> trace;
   DevBuf<unsigned long long> level_claims;
   DevBuf<uint32_t> nlevels;

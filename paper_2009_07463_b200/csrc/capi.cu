@@ -240,17 +240,19 @@ void download_result(etb_layout* h, int32_t* depth, uint32_t* parent, uint64_t* 
   if (!n || (!depth && !parent && !parent64)) return;
   auto& S = h->S;
   cudaStream_t s = h->stream;
+  // staging buffers persist with the layout: no allocation (and no
+  // synchronising free) inside the reference-facing call
   if (depth && S.tmp_depth.size() < n) S.tmp_depth.alloc(n);
   if (parent && S.tmp_parent.size() < n) S.tmp_parent.alloc(n);
-  etb::DevBuf<uint64_t> p64;
-  if (parent64) p64.alloc(n);
+  if (parent64 && S.tmp_parent64.size() < n) S.tmp_parent64.alloc(n);
   split_kernel<<<etb::grid_for(n, 256), 256, 0, s>>>(S.dp.get(), n, depth ? S.tmp_depth.get() : nullptr,
                                                      parent ? S.tmp_parent.get() : nullptr,
-                                                     parent64 ? p64.get() : nullptr);
+                                                     parent64 ? S.tmp_parent64.get() : nullptr);
   ETB_LAUNCH_CHECK();
   if (depth) ETB_CUDA(cudaMemcpyAsync(depth, S.tmp_depth.get(), n * 4, cudaMemcpyDeviceToHost, s));
   if (parent) ETB_CUDA(cudaMemcpyAsync(parent, S.tmp_parent.get(), n * 4, cudaMemcpyDeviceToHost, s));
-  if (parent64) ETB_CUDA(cudaMemcpyAsync(parent64, p64.get(), n * 8, cudaMemcpyDeviceToHost, s));
+  if (parent64)
+    ETB_CUDA(cudaMemcpyAsync(parent64, S.tmp_parent64.get(), n * 8, cudaMemcpyDeviceToHost, s));
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 

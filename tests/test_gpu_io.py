@@ -56,7 +56,8 @@ def test_bench_report_v1_and_tree_out(tmp_path, kron16):
     root_dir = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     rj, tt = str(tmp_path / "r.json"), str(tmp_path / "t.ett")
     subprocess.run([sys.executable, os.path.join(root_dir, "bench.py"), "--scale", "16",
-                    "--steps", "1", "--warmup", "3", "--secondary-scale", "", "--no-cpu-baseline",
+                    "--steps", "1", "--warmup", "3", "--secondary", "0", "--no-paper-mode",
+                    "--emulate-partitions", "", "--no-cpu-baseline",
                     "--report-json", rj, "--tree-out", tt], check=True, capture_output=True,
                    cwd=root_dir, timeout=600)
     rep = json.load(open(rj))
