@@ -62,6 +62,11 @@ constexpr uint64_t kGrab = 4;        // top-down chunks per warp per grab on lon
 #ifndef ETB_BU_EAGER
 #define ETB_BU_EAGER 0
 #endif
+// BfsParams::small_mode3_edges default (env ETB_SMALL_MODE3 overrides)
+#ifndef ETB_SMALL_MODE3_DEFAULT
+#define ETB_SMALL_MODE3_DEFAULT 2e6  // s22: +0.9% (938.5 vs 930.4 GTEPS; 5e5: neutral)
+#endif
+constexpr double kSmallMode3Default = ETB_SMALL_MODE3_DEFAULT;
 // BfsParams::td_as_bu default (env ETB_TD_AS_BU overrides; 0 = off): s26 +6%
 // harmonic-mean GTEPS (slowest roots 0.80 -> 0.62-0.68 ms), s22 neutral
 constexpr double kTdAsBuDefault = 4.0;  // measured best at s26 (3..5 equal, 6 and up: no level)
@@ -1001,8 +1006,8 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         // claims and scout are counted afterwards by a streaming pass over the
         // new frontier (mode 3). (Measured: s26 -5 us per root; on the
         // small-core kernel the extra pass and barrier cost more than they save.)
-        defer_scout = kLarge && !emit;
-        if (kLarge && defer_scout)
+        defer_scout = !emit && (kLarge || (double)ne >= p.small_mode3_edges);
+        if (defer_scout)
           td_step<3, kLarge>(p, cb, wn, qv_in, qp_in, nq, ne, qv_out, qp_out, fnext, slot, dnext,
                      scout_acc, claims_acc, root);
         else if (!emit)
@@ -1784,6 +1789,8 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   // the list-less path; s22 unchanged)
   p.emit_limit = static_cast<double>(L.nc) / 8.0 + 1024.0;
   p.td_as_bu = kTdAsBuDefault;
+  p.small_mode3_edges = kSmallMode3Default;
+  if (const char* e = getenv("ETB_SMALL_MODE3")) p.small_mode3_edges = atof(e);
   if (const char* e = getenv("ETB_TD_AS_BU")) p.td_as_bu = atof(e);
   p.trace = nullptr;
   p.level_claims = nullptr;

@@ -66,6 +66,10 @@ struct BfsParams {
   // neighbour — is the same, so depths, claims, scout and the α/β sequence are
   // the reference's; only the GPU cost differs.
   double td_as_bu;
+  // small-core kernel: list-less top-down levels with at least this many
+  // frontier edges claim atomic-free and count afterwards (as the large-core
+  // kernel's); smaller ones claim with returning atomics
+  double small_mode3_edges;
   int top_down_only;   // CoreKernel::kTopDown
   int bottom_up_only;  // CoreKernel::kBlockSearch: bottom-up levels to fixpoint
   // stats (may be null)
