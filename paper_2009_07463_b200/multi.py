@@ -99,6 +99,10 @@ def assemble_result(cg, D) -> None:
 
     from .etbfs import _check, lib, partition_owner
 
+    # the traversal ran on the layout's own (non-blocking) stream: finish it
+    # before torch's stream reads the result, and torch's writes before the
+    # library's next calls (cudaDeviceSynchronize covers every stream)
+    torch.cuda.synchronize()
     ptr = C.c_void_p()
     _check(lib().etb_result_device_ptr(cg.handle, C.byref(ptr)))
     dp = torch.as_tensor(_DeviceArray(ptr.value, cg.vertex_count), device="cuda")
