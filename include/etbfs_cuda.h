@@ -260,6 +260,13 @@ int etb_debug_warp_stamps(etb_layout* L, uint64_t start, int32_t depth, uint64_t
  * init end, [2 + L] level L end, [128 + L] conversion before level L end,
  * [255] replay end) and, at [192 + L], top-down level L's frontier edge count. */
 int etb_debug_phase_stamps(etb_layout* L, uint64_t* out256);
+/* Diagnostics of a -DETB_MISS_CYCLES build (zeros otherwise), 320 counters per
+ * depth d: [d % 64] warp cycles in bottom-up steps, [64 + d % 64] in their
+ * deferred-miss resolution, [128 + d % 32] deferred vertices, [160 + d % 32]
+ * rows scanned past the second neighbour, [192 + d % 32] rows scanned by the
+ * whole warp, [224 + d % 32] its 32-edge rounds, [256 + d % 64] the slowest
+ * warp's miss-resolution cycles; reset != 0 clears them. */
+int etb_debug_diag(etb_layout* L, uint64_t* out320, int reset);
 /* Diagnostics (libraries built with -DETB_DEBUG_CHECKS; 0 otherwise): the
  * source line of the first failed device bounds check since the last call. */
 int etb_debug_check_line(uint32_t* line);

@@ -96,6 +96,23 @@ def build_cpp_tests() -> str:
     return out
 
 
+def build_prims_test() -> str:
+    """tests/cpp/test_prims: the preprocessing primitives (csrc/prims.cu) against
+    host std:: algorithms (links the library; internal C++ symbols)."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_prims.cu")
+    out = os.path.join(ROOT, "tests", "cpp", "bin", "test_prims")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    deps = [src, LIB] + headers()
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
+        return out
+    cmd = [NVCC, *ARCH, *FLAGS, src, "-o", out, "-L" + os.path.dirname(LIB), "-letbfs_b200",
+           "-Xlinker", "-rpath,$ORIGIN/../../../paper_2009_07463_b200/lib"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"test_prims build failed:\n{r.stderr}")
+    return out
+
+
 REF_ACCEPTANCE = "/root/reference/proj/tests/acceptance.cpp"
 ACCEPTANCE_BIN = os.path.join(ROOT, "tests", "cpp", "bin", "acceptance_ref")
 

@@ -409,6 +409,8 @@ __device__ void td_step(const P& p, uint32_t* cbuf, int32_t* win, const uint32_t
 // root at s22, -2 us at s26).
 constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (the claim buffer + the window)
 constexpr uint32_t kLaneFirst = 64;
+// csecond entries: the second core neighbour; bit 31 set when it ends the row
+constexpr uint32_t kSecondMask = 0x7FFFFFFFu;
 // bu_sweep on the large-core kernel once fewer than nc / kSweepT vertices are
 // unvisited (measured at s26: 2 best, -5 us per root; inlined — out of line its
 // call cost the rest of the kernel 3%)
@@ -483,13 +485,43 @@ __device__ __forceinline__ void scan_rows2(const P& p, const uint32_t* fcur, uin
   }
 }
 
+// Diagnostics (-DETB_MISS_CYCLES builds only): per depth d (mod 64), the warp
+// cycles spent in bottom-up steps [d] and in their miss resolution [64 + d],
+// read with etb_debug_diag.
+// [128 + d % 32] deferred vertices, [160 + ..] rows scanned past the second
+// neighbour, [192 + ..] rows scanned by the whole warp, [224 + ..] the warp's
+// 32-edge rounds on them, [256 + d] the slowest warp's miss-resolution cycles.
+constexpr int kDiag = 320;
+__device__ unsigned long long g_diag[kDiag];
+#ifdef ETB_MISS_CYCLES
+#define ETB_DIAG_BEGIN() const long long diag_c0 = clock64()
+#define ETB_DIAG_END(slot)                                                            \
+  do {                                                                                \
+    if ((threadIdx.x & 31) == 0) {                                                    \
+      const unsigned long long dc = clock64() - diag_c0;                              \
+      atomicAdd(&g_diag[(slot) & 127], dc);                                           \
+      if ((slot) >= 64) atomicMax(&g_diag[256 + ((slot) & 63)], dc);                  \
+    }                                                                                 \
+  } while (0)
+#define ETB_DIAG_COUNT(slot, n)                                                       \
+  do {                                                                                \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_diag[slot], (unsigned long long)(n));   \
+  } while (0)
+#else
+#define ETB_DIAG_BEGIN() (void)0
+#define ETB_DIAG_END(slot) (void)0
+#define ETB_DIAG_COUNT(slot, n) (void)0
+#endif
+
+// Row scans of deferred vertices whose first `skip` neighbours missed.
 template <class P>
-__device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext,
-                               uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
-                               unsigned long long& claims_acc, uint32_t* qv_out,
-                               uint64_t* qp_out, unsigned long long* lslot) {
+__device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
+                             uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
+                             unsigned long long& claims_acc, uint32_t* qv_out,
+                             uint64_t* qp_out, unsigned long long* lslot, uint32_t skip) {
   const unsigned lane = threadIdx.x & 31;
   __syncwarp();
+  ETB_DIAG_COUNT(160 + (dnext & 31), nmiss);
   uint32_t nlong = 0;
   for (uint32_t i0 = 0; i0 < nmiss; i0 += 64) {
     const uint32_t va = i0 + lane < nmiss ? mbuf[i0 + lane] : kNone32;
@@ -498,11 +530,11 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
     uint64_t rba = 0, rea = 0, rbb = 0, reb = 0;
     if (va != kNone32) rba = p.crow[va], rea = p.crow[va + 1];
     if (vb != kNone32) rbb = p.crow[vb], reb = p.crow[vb + 1];
-    const uint64_t la = min(rea, rba + 1 + kLaneFirst), lb = min(reb, rbb + 1 + kLaneFirst);
+    const uint64_t la = min(rea, rba + skip + kLaneFirst), lb = min(reb, rbb + skip + kLaneFirst);
     uint32_t pa = 0, pb = 0;
     bool ha, hb;
-    scan_rows2(p, fcur, rba + 1, va != kNone32 ? la : 0, rbb + 1, vb != kNone32 ? lb : 0, pa, pb,
-               ha, hb);
+    scan_rows2(p, fcur, rba + skip, va != kNone32 ? la : 0, rbb + skip, vb != kNone32 ? lb : 0,
+               pa, pb, ha, hb);
     const bool lnga = va != kNone32 && !ha && la < rea;
     const bool lngb = vb != kNone32 && !hb && lb < reb;
     if (ha) {
@@ -534,11 +566,13 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
     nlong += __popc(lmb);
     __syncwarp();
   }
+  ETB_DIAG_COUNT(192 + (dnext & 31), nlong);
   for (uint32_t i = 0; i < nlong; ++i) {
     const uint32_t v = mbuf[i];
-    const uint64_t rb = p.crow[v] + 1 + kLaneFirst, re = p.crow[v + 1];
+    const uint64_t rb = p.crow[v] + skip + kLaneFirst, re = p.crow[v + 1];
     uint32_t par = kNone32;
     for (uint64_t e0 = rb; e0 < re; e0 += 32) {
+      ETB_DIAG_COUNT(224 + (dnext & 31), 1);
       const uint64_t e = e0 + lane;
       const uint32_t x = e < re ? p.ccol[e] : kNone32;
       const unsigned m = __ballot_sync(0xffffffffu, x != kNone32 && test_bit(fcur, x));
@@ -561,6 +595,67 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
   __syncwarp();
 }
 
+// Deferred misses: vertices whose first (highest-degree) neighbour is not in
+// the frontier. Stage 1 probes every one's SECOND neighbour, four vertices per
+// lane, from the layout's csecond array (bit 31: it is the row's last) — one
+// gather and one probe per 128 vertices, no row-offset round trip; most core
+// rows missing their first neighbour have two entries (the ET relayout moved
+// the tree-like vertices out of the core), so this settles most of them.
+// Stage 2 (resolve_rows) scans the rest of the longer rows. (Measured against
+// a load-balanced warp scan of the rows, 128 edges per round trip, which was
+// 1.7x slower: the rows, not the edges, are the unit a round trip must cover.)
+template <class P>
+__device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext,
+                               uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
+                               unsigned long long& claims_acc, uint32_t* qv_out,
+                               uint64_t* qp_out, unsigned long long* lslot) {
+  const unsigned lane = threadIdx.x & 31, lt = (1u << lane) - 1;
+  __syncwarp();
+  ETB_DIAG_BEGIN();
+  ETB_DIAG_COUNT(128 + (dnext & 31), nmiss);
+  uint32_t nlong = 0;
+  for (uint32_t i0 = 0; i0 < nmiss; i0 += 128) {
+    uint32_t v[4], sc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = i0 + lane + 32u * k;
+      v[k] = i < nmiss ? mbuf[i] : kNone32;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sc[k] = v[k] != kNone32 ? p.csecond[v[k]] : kNone32;
+    bool h[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = sc[k] != kNone32 && test_bit(fcur, sc[k] & kSecondMask);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!h[k]) continue;
+      p.dp[v[k]] = make_uint2(static_cast<uint32_t>(dnext), sc[k] & kSecondMask);
+      atomicOr(&p.visited[v[k] >> 5], 1u << (v[k] & 31));
+      atomicOr(&fnext[v[k] >> 5], 1u << (v[k] & 31));
+      ++claims_acc;
+    }
+    if (lslot) {
+      uint32_t ad[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ad[k] = h[k] ? ((sc[k] >> 31) ? 2u : p.cmeta[v[k]].x) : 0u;
+      bu_append<4>(v, ad, qv_out, qp_out, lslot);
+    }
+    // rows with more than two entries and no hit yet go on to the row scans,
+    // compacted to the front of the buffer (slots < i0 + 128 are already read)
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool more = v[k] != kNone32 && !h[k] && sc[k] != kNone32 && !(sc[k] >> 31);
+      const unsigned m = __ballot_sync(0xffffffffu, more);
+      if (more) mbuf[nlong + __popc(m & lt)] = v[k];
+      nlong += __popc(m);
+    }
+    __syncwarp();
+  }
+  if (nlong) resolve_rows(p, fcur, fnext, mbuf, nlong, dnext, claims_acc, qv_out, qp_out, lslot, 2);
+  ETB_DIAG_END(64 + (dnext & 63));
+}
+
 template <int kU, class P>
 __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
@@ -571,6 +666,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
   const uint64_t nw = (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
+  ETB_DIAG_BEGIN();
   for (uint64_t w0 = wlo_of(p) + gw * kU; w0 < whi_of(p); w0 += nw * kU) {
     // the run's words: w0 + k (one partition), or one owned-word mapping per
     // run (partitioned: aligned runs of 8 are 8 hub words G apart or one block)
@@ -651,6 +747,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
     }
   }
   if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
+  ETB_DIAG_END(dnext & 63);
 }
 
 template <int kSweep, class P>
@@ -662,6 +759,7 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
   const uint64_t nw = (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
+  ETB_DIAG_BEGIN();
   // A warp sweeps kSweep visited words with one coalesced load (lane = word)
   // and works through the words with unvisited vertices kBuU at a time, so
   // late levels (few unvisited left) skip full words without a round trip each.
@@ -727,6 +825,7 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
     }
   }
   if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
+  ETB_DIAG_END(dnext & 63);
 }
 
 // Frontier bitmap -> frontier list (when a top-down level follows one that did
@@ -1113,7 +1212,11 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     for (int k = 0; k < kReplay; ++k) {
       const bool ok = a[k] < kNone32 - 1;
       vis[k] = ok ? test_bit(p.visited, a[k]) : 0u;
+#ifdef ETB_EXP_NO_DA  // timing experiment only (wrong depths): replay without the anchor-depth gather
+      da[k] = 0u;
+#else
       da[k] = ok ? __ldcg(&p.dp[a[k]].x) : 0u;
+#endif
     }
 #pragma unroll
     for (int k = 0; k < kReplay; ++k) {
@@ -1197,6 +1300,7 @@ struct PartView {
   const uint64_t* crow;
   const uint32_t* ccol;
   const uint32_t* cfirst;
+  const uint32_t* csecond;
   const uint32_t* degn;
   const uint2* cmeta;
   uint2* dp;
@@ -1407,6 +1511,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   v.crow = p.crow;
   v.ccol = p.ccol;
   v.cfirst = p.cfirst;
+  v.csecond = p.csecond;
   v.degn = p.degn;
   v.cmeta = p.cmeta;
   v.dp = p.dp;
@@ -1701,10 +1806,7 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   S.n = n;
   const uint64_t words = (L.nc + 31) / 32 + 1;
   S.words = words;
-  S.visited.alloc(2 * words);
-  S.fb0.alloc(2 * words);
-  S.fb1.alloc(2 * words);
-  S.fb2.alloc(2 * words);
+  S.bits.alloc(8 * words);
   const uint64_t cap = L.nc + 2;
   S.qv0.alloc(cap);
   S.qv1.alloc(cap);
@@ -1712,16 +1814,13 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   S.qp1.alloc(cap);
   S.ctr.alloc(64);
   // both halves clean: visited zero but the last word's padding bits
-  ETB_CUDA(cudaMemsetAsync(S.visited.get(), 0, 2 * words * 4, s));
-  ETB_CUDA(cudaMemsetAsync(S.fb0.get(), 0, 2 * words * 4, s));
-  ETB_CUDA(cudaMemsetAsync(S.fb1.get(), 0, 2 * words * 4, s));
-  ETB_CUDA(cudaMemsetAsync(S.fb2.get(), 0, 2 * words * 4, s));
+  ETB_CUDA(cudaMemsetAsync(S.bits.get(), 0, 8 * words * 4, s));
   ETB_CUDA(cudaMemsetAsync(S.ctr.get(), 0, 64 * 8, s));
   if (const uint32_t tail = static_cast<uint32_t>(L.nc & 31u)) {
     const uint32_t pad = ~0u << tail;
     const uint64_t last = (L.nc + 31) / 32 - 1;
     for (int h = 0; h < 2; ++h)
-      ETB_CUDA(cudaMemcpyAsync(S.visited.get() + h * words + last, &pad, 4,
+      ETB_CUDA(cudaMemcpyAsync(S.visited() + h * words + last, &pad, 4,
                                cudaMemcpyHostToDevice, s));
   }
   S.parity = 0;
@@ -1748,6 +1847,23 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S.block, sizeof(Smem)));
   if (per_sm < 1) throw CudaError("et_bfs_kernel cannot be resident");
   S.grid = sms;  // one CTA per SM (the level barrier's arrivals)
+  // L2 access-policy window over the per-root bitmap state (ETB_L2_PERSIST=1):
+  // its lines are kept in the persisting L2 carve-out, out of reach of the
+  // streamed CSR / result traffic and of the bench's L2 flush between roots.
+  if (const char* e = getenv("ETB_L2_PERSIST"); e && atoi(e) > 0) {
+    int maxp = 0;
+    ETB_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    const size_t want = std::min<size_t>(S.bits.bytes(), static_cast<size_t>(maxp));
+    ETB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    cudaStreamAttrValue a = {};
+    a.accessPolicyWindow.base_ptr = S.bits.get();
+    a.accessPolicyWindow.num_bytes = want;
+    a.accessPolicyWindow.hitRatio = 1.0f;
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ETB_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a));
+    S.l2_window = true;
+  }
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1755,6 +1871,7 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.crow = L.crow.get();
   p.ccol = L.ccol.get();
   p.cfirst = L.cfirst.get();
+  p.csecond = L.csecond.get();
   p.reachable = L.nc;
   p.degn = L.degn.get();
   p.cmeta = L.cmeta.get();
@@ -1765,14 +1882,14 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.tdepth = L.tdepth.get();
   p.nt = static_cast<uint32_t>(L.nt);
   const uint64_t cur = S.parity * S.words, nxt = (S.parity ^ 1u) * S.words;
-  p.visited = S.visited.get() + cur;
-  p.fb0 = S.fb0.get() + cur;
-  p.fb1 = S.fb1.get() + cur;
-  p.fb2 = S.fb2.get() + cur;
-  p.visited_next = S.visited.get() + nxt;
-  p.fb0_next = S.fb0.get() + nxt;
-  p.fb1_next = S.fb1.get() + nxt;
-  p.fb2_next = S.fb2.get() + nxt;
+  p.visited = S.visited() + cur;
+  p.fb0 = S.fb0() + cur;
+  p.fb1 = S.fb1() + cur;
+  p.fb2 = S.fb2() + cur;
+  p.visited_next = S.visited() + nxt;
+  p.fb0_next = S.fb0() + nxt;
+  p.fb1_next = S.fb1() + nxt;
+  p.fb2_next = S.fb2() + nxt;
   p.qv0 = S.qv0.get();
   p.qv1 = S.qv1.get();
   p.qp0 = S.qp0.get();
@@ -1910,6 +2027,15 @@ void bfs_launch(const BfsParams& p, BfsState& S, cudaStream_t s) {
   ETB_CUDA(cudaLaunchCooperativeKernel(kernel_for(S.block), dim3(S.grid), dim3(S.block), args,
                                        sizeof(Smem), s));
   S.parity ^= 1u;  // this launch cleans the other half; the next one uses it
+}
+
+void debug_diag(uint64_t* out, bool reset, cudaStream_t s) {
+  ETB_CUDA(cudaMemcpyFromSymbolAsync(out, g_diag, sizeof(g_diag), 0, cudaMemcpyDeviceToHost, s));
+  if (reset) {
+    static const unsigned long long zero[kDiag] = {};
+    ETB_CUDA(cudaMemcpyToSymbolAsync(g_diag, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s));
+  }
+  ETB_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace etb

@@ -15,6 +15,7 @@ struct BfsParams {
   const uint64_t* crow;
   const uint32_t* ccol;
   const uint32_t* cfirst;
+  const uint32_t* csecond;  // second core neighbour, bit 31: last of its row (kNone32: none)
   const uint32_t* degn;  // full degree (scout, bfs.cpp:80)
   const uint2* cmeta;    // per core vertex {core degree, full degree}
   uint64_t reachable;  // core vertices in the start's core component (set per root)
@@ -83,7 +84,13 @@ struct BfsParams {
 
 struct BfsState {
   uint64_t n = 0;
-  DevBuf<uint32_t> visited, fb0, fb1, fb2;
+  // visited / fb0 / fb1 / fb2, two halves each, in one allocation (one L2
+  // access-policy window can cover the whole per-root bitmap state)
+  DevBuf<uint32_t> bits;
+  uint32_t* visited() const { return bits.get(); }
+  uint32_t* fb0() const { return bits.get() + 2 * words; }
+  uint32_t* fb1() const { return bits.get() + 4 * words; }
+  uint32_t* fb2() const { return bits.get() + 6 * words; }
   DevBuf<uint32_t> qv0, qv1;
   DevBuf<uint64_t> qp0, qp1;
   DevBuf<unsigned long long> ctr, bar;
@@ -104,6 +111,7 @@ struct BfsState {
   int grid = 0, block = 0;
   uint32_t parity = 0;  // which half of visited / fb0 / fb1 / ctr the next launch uses
   uint64_t words = 0;   // per half
+  bool l2_window = false;  // the bitmap state has a persisting L2 access-policy window
   bool has_result = false;
   bool assembled = false;  // multi-GPU: the caller merged every rank's owned slices into dp
   uint64_t last_start = ~uint64_t{0};
@@ -112,6 +120,8 @@ struct BfsState {
 void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s);
 void empty_launch(const BfsState& S, cudaStream_t s);  // launch-cost floor (diagnostics)
 void bfs_launch(const BfsParams& p, BfsState& S, cudaStream_t s);
+// -DETB_MISS_CYCLES diagnostics: bottom-up step / miss-resolution warp cycles per depth
+void debug_diag(uint64_t* out320, bool reset, cudaStream_t s);
 // Fills depth/parent of the start's tree on the host (traverse_return_core_edge,
 // et_bfs.cpp:34-57) and returns the core vertex to start from (kNone32 if the
 // start's component is a pure tree or the start is isolated).

@@ -837,6 +837,15 @@ int etb_debug_check_line(uint32_t* line) {
   });
 }
 
+int etb_debug_diag(etb_layout* h, uint64_t* out320, int reset) {
+  return guarded([&] {
+    need(h, "etb_debug_diag");
+    need(out320, "etb_debug_diag");
+    ETB_CUDA(cudaSetDevice(h->device));
+    etb::debug_diag(out320, reset != 0, h->stream);
+  });
+}
+
 int etb_debug_phase_stamps(etb_layout* h, uint64_t* out256) {
   return guarded([&] {
     need(h, "etb_debug_phase_stamps");
@@ -1041,6 +1050,10 @@ int etb_time_roots(etb_layout* h, const uint64_t* starts, uint64_t count, int wa
       // per-root sequence (patch copy + kernel) on a stream that is fed ahead,
       // not the host's launch latency (the synchronous, wall-clock path is
       // what bench.py's e2e number measures).
+      // With the persisting L2 window on, its lines are first demoted to
+      // normal so that the flush evicts them too: every root starts cold.
+      if (flush_l2 && h->S.l2_window && !getenv("ETB_KEEP_PERSIST"))
+        ETB_CUDA(cudaCtxResetPersistingL2Cache());
       if (flush_l2) ETB_CUDA(cudaMemsetAsync(h->flush.get(), i & 0xFF, h->flush.size(), s));
       ETB_CUDA(cudaEventRecord(h->ev[0], s));
       // the pre-launch event only when kernel times are asked for: a third

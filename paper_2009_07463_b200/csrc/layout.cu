@@ -410,9 +410,11 @@ __global__ void key_cols_kernel(const uint64_t* keys, uint64_t count, uint64_t m
 }
 
 __global__ void first_nbr_kernel(const uint64_t* crow, const uint32_t* ccol, const uint32_t* degn,
-                                 uint64_t nc, uint32_t* first, uint2* meta) {
+                                 uint64_t nc, uint32_t* first, uint32_t* second, uint2* meta) {
   GRID_LOOP(i, nc) {
-    first[i] = crow[i] < crow[i + 1] ? ccol[crow[i]] : kNone32;
+    const uint64_t d = crow[i + 1] - crow[i];
+    first[i] = d ? ccol[crow[i]] : kNone32;
+    second[i] = d >= 2 ? ccol[crow[i] + 1] | (d == 2 ? 0x80000000u : 0u) : kNone32;
     meta[i] = make_uint2(static_cast<uint32_t>(crow[i + 1] - crow[i]), degn[i]);
   }
 }
@@ -722,6 +724,9 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
   L.ecore = read_u64(L.crow.get() + nc, s);
   L.ccol.alloc(L.ecore ? L.ecore : 1);
   L.cfirst.alloc(nc ? nc : 1);
+  L.csecond.alloc(nc ? nc : 1);
+  // (csecond keeps a flag in bit 31 of a core id)
+  if (nc >= (uint64_t{1} << 31)) throw std::runtime_error("relayout_csr: core of 2^31 vertices or more");
   L.cmeta.alloc(nc ? nc : 1);
   if (L.ecore) {
     // Rows sorted by one key sort of (new src << b | new dst), in buckets of
@@ -761,7 +766,8 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
   }
   if (nc) {
     first_nbr_kernel<<<grid_for(nc, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), L.degn.get(),
-                                                       nc, L.cfirst.get(), L.cmeta.get());
+                                                       nc, L.cfirst.get(), L.csecond.get(),
+                                                       L.cmeta.get());
     ETB_LAUNCH_CHECK();
   }
   core_components(L, s);

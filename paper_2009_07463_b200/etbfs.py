@@ -167,6 +167,7 @@ def lib() -> C.CDLL:
     sig("etb_result_traversed_edges", vp, P64)
     sig("etb_result_validate", vp, u64, vp)
     sig("etb_debug_phase_stamps", vp, vp)
+    sig("etb_debug_diag", vp, vp, i32)
     sig("etb_debug_launch_floor", vp, i32, C.POINTER(C.c_double))
     sig("etb_debug_check_line", C.POINTER(C.c_uint32))
     sig("etb_debug_block_stamps", vp, u64, vp, u64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32))

@@ -1,0 +1,6 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_partition.py tests/test_gpu_validate.py -x -q > gpurun_out/t_e.log 2>&1; tail -2 gpurun_out/t_e.log
+ETB_LIB=tools/variants/misscyc/libetbfs_b200.so timeout 600 python tools/root_profile.py --scale 26 --roots 8 --cold --diag > gpurun_out/diag26_e.log 2>&1
+timeout 1200 python tools/ab_env.py --scale 26 --steps 3 --repeat 2 --variants "ETB_BASE=1" "ETB_LIB=tools/variants/oldmiss/libetbfs_b200.so" > gpurun_out/ab26e.log 2>&1
+timeout 600 python tools/ab_env.py --scale 22 --steps 3 --repeat 2 --variants "ETB_BASE=1" "ETB_LIB=tools/variants/oldmiss/libetbfs_b200.so" > gpurun_out/ab22e.log 2>&1
+cat gpurun_out/ab26e.log gpurun_out/ab22e.log

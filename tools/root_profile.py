@@ -25,6 +25,9 @@ def main():
     ap.add_argument("--roots", type=int, default=64)
     ap.add_argument("--parts", type=int, default=1, help="1D core partitions on this device")
     ap.add_argument("--cold", action="store_true", help="per-level stats on a flushed L2")
+    ap.add_argument("--diag", action="store_true",
+                    help="-DETB_MISS_CYCLES build: bottom-up step / miss-resolution warp time per level")
+    ap.add_argument("--clock-ghz", type=float, default=1.965)
     args = ap.parse_args()
     g = eb.generate_graph(scale=args.scale, edgefactor=args.edgefactor, seed=1)
     cg = eb.relayout_csr(g, mh=args.mh)
@@ -42,8 +45,13 @@ def main():
             torch.cuda.synchronize()
         else:
             E.time_roots(cg, starts[i:i + 1], warmup=0, flush_l2=True)  # warms this root
+        diag = np.zeros(320, np.uint64)
+        if args.diag:
+            E._check(E.lib().etb_debug_diag(cg.handle, diag.ctypes.data, 1))
         r = eb.et_bfs(cg, int(s), stats=True, want_parent=False, want_depth=False)
         ns = r.stats.level_ns
+        if args.diag:
+            E._check(E.lib().etb_debug_diag(cg.handle, diag.ctypes.data, 1))
         import ctypes as C
         ph = np.zeros(256, np.uint64)
         E._check(E.lib().etb_debug_phase_stamps(cg.handle, ph.ctypes.data))
@@ -54,6 +62,16 @@ def main():
                "kernel_us": round(float(kms[i]) * 1e3, 1), "call_us": round(float(ms[i]) * 1e3, 1), "device_us": round(r.stats.total_ns / 1e3, 1),
                "init_us": round(ns[0] / 1e3, 1) if ns else None, "trace": r.stats.direction_trace,
                "claims": r.stats.level_claims, "level_us": dur, "td_edges": td_edges}
+        if args.diag:  # mean per warp, us at the SM clock (--clock-ghz)
+            nw = 148 * (1024 if cg.core_vertex_count >= (1 << 23) else 640) // 32
+            cyc = lambda c: round(float(c) / nw / (args.clock_ghz * 1e3), 1)
+            rec["bu_step_us"] = [cyc(diag[(L + 1) & 63]) for L in range(len(dur))]
+            rec["bu_miss_us"] = [cyc(diag[64 + ((L + 1) & 63)]) for L in range(len(dur))]
+            rec["bu_miss_max_us"] = [round(float(diag[256 + ((L + 1) & 63)]) / (args.clock_ghz * 1e3), 1)
+                                     for L in range(len(dur))]
+            d1 = lambda b: [int(diag[b + ((L + 1) & 31)]) for L in range(len(dur))]
+            rec["deferred"], rec["past_second"] = d1(128), d1(160)
+            rec["warp_rows"], rec["warp_rounds"] = d1(192), d1(224)
         out.append(rec)
         print(json.dumps(rec), flush=True)
     # Fixed cost: a start on an isolated vertex runs init + tree replay only.
