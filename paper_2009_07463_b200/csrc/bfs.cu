@@ -602,8 +602,9 @@ __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
 // rows missing their first neighbour have two entries (the ET relayout moved
 // the tree-like vertices out of the core), so this settles most of them.
 // Stage 2 (resolve_rows) scans the rest of the longer rows. (Measured against
-// a load-balanced warp scan of the rows, 128 edges per round trip, which was
-// 1.7x slower: the rows, not the edges, are the unit a round trip must cover.)
+// a load-balanced warp scan of the rows, 128 edges per round trip: 1.7x slower
+// for all misses, 1.14x for the rows past the second neighbour — its window
+// bookkeeping is ~50 shuffles per round and a round covers 32 rows, not 64.)
 template <class P>
 __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext,
                                uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
@@ -1847,13 +1848,18 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S.block, sizeof(Smem)));
   if (per_sm < 1) throw CudaError("et_bfs_kernel cannot be resident");
   S.grid = sms;  // one CTA per SM (the level barrier's arrivals)
-  // L2 access-policy window over the per-root bitmap state (ETB_L2_PERSIST=1):
-  // its lines are kept in the persisting L2 carve-out, out of reach of the
-  // streamed CSR / result traffic and of the bench's L2 flush between roots.
-  if (const char* e = getenv("ETB_L2_PERSIST"); e && atoi(e) > 0) {
-    int maxp = 0;
-    ETB_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
-    const size_t want = std::min<size_t>(S.bits.bytes(), static_cast<size_t>(maxp));
+  // L2 access-policy window over the per-root bitmap state (on by default,
+  // ETB_L2_PERSIST=0 turns it off): its lines are kept in the persisting L2
+  // carve-out, out of reach of the streamed CSR / result traffic (s26: +2.7%
+  // harmonic-mean GTEPS with every root started cold, persisting lines
+  // included — etb_time_roots demotes them before its L2 flush; s22: +-0).
+  // Only when the whole state fits half the carve-out: a window larger than
+  // the carve-out thrashed at scale 28 (2x slower per root).
+  int maxp = 0;
+  ETB_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  const char* pe = getenv("ETB_L2_PERSIST");
+  if ((!pe || atoi(pe) > 0) && S.bits.bytes() <= static_cast<size_t>(maxp) / 2) {
+    const size_t want = S.bits.bytes();
     ETB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
     cudaStreamAttrValue a = {};
     a.accessPolicyWindow.base_ptr = S.bits.get();
