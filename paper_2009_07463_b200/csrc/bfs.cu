@@ -96,6 +96,32 @@ struct Smem {
   unsigned long long red[2][kMaxWarps];
   unsigned long long tot[4];  // level totals read once per CTA after the barrier
 };
+static_assert(sizeof(Smem) % 16 == 0, "the bottom-up pipes follow Smem, 16-byte aligned");
+
+// Bottom-up runs fetched by the TMA engine (single-partition kernel, built with
+// -DETB_BU_TMA=1): per warp a two-stage ring, each stage one run's first
+// neighbours (kU x 32 u32, the contiguous cfirst slice) and the 16-byte-aligned
+// span of its visited words, completing on the stage's mbarrier; a run is
+// requested two iterations ahead, so the warp's chain per iteration is the
+// frontier probe alone. Measured against the plain loads (64 roots x 3 steps,
+// every root validated): s26 -1% (2474 vs 2502 GTEPS), s22 -0.3% — the first
+// neighbour stream is not what the bottom-up levels wait on, and the 69 KB of
+// stages come out of L1, which holds the hub words the probes hit. Off by
+// default; kept as the measured alternative.
+#ifndef ETB_BU_TMA
+#define ETB_BU_TMA 0
+#endif
+template <int kU>
+struct BuStage {
+  uint32_t cf[kU * 32];
+  uint32_t vw[12];  // kU words + up to 3 words of alignment on each side
+};
+template <int kU>
+struct BuPipe {
+  BuStage<kU> st[2];
+  uint64_t bar[2];
+};
+static_assert(sizeof(BuPipe<8>) % 16 == 0 && sizeof(BuPipe<7>) % 16 == 0, "16-byte stages");
 
 // Phase timestamps for stats (block 0 / thread 0): [256] entry, [257] after
 // init, [258 + L] after level L, [511] end of the tree replay.
@@ -657,6 +683,22 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
   ETB_DIAG_END(64 + (dnext & 63));
 }
 
+// Request run r0 (kU visited words and their first neighbours) into pipe
+// stage sg (lane 0; nothing past the sweep's end). The visited span is widened
+// to 16-byte boundaries (the bitmap allocation covers the overhang); cfirst is
+// padded to whole words at layout time.
+template <int kU>
+__device__ __forceinline__ void bu_issue(const BfsParams& p, BuPipe<kU>* pipe, int sg, uint64_t r0) {
+  if (r0 >= p.nwords) return;
+  const uint32_t nwd = static_cast<uint32_t>(min(static_cast<uint64_t>(kU), p.nwords - r0));
+  const uint32_t cf_bytes = nwd * 128u;
+  const uint64_t vlo = (r0 * 4) & ~uint64_t{15}, vhi = ((r0 + nwd) * 4 + 15) & ~uint64_t{15};
+  const uint32_t vw_bytes = static_cast<uint32_t>(vhi - vlo);
+  mbar_expect_tx(&pipe->bar[sg], cf_bytes + vw_bytes);
+  bulk_g2s(pipe->st[sg].cf, p.cfirst + r0 * 32, cf_bytes, &pipe->bar[sg]);
+  bulk_g2s(pipe->st[sg].vw, reinterpret_cast<const unsigned char*>(p.visited) + vlo, vw_bytes,
+           &pipe->bar[sg]);
+}
 template <int kU, class P>
 __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
@@ -668,7 +710,24 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
   ETB_DIAG_BEGIN();
-  for (uint64_t w0 = wlo_of(p) + gw * kU; w0 < whi_of(p); w0 += nw * kU) {
+  constexpr bool kTma = ETB_BU_TMA && !IsPart<P>::value;
+  [[maybe_unused]] BuPipe<kU>* pipe = nullptr;
+  [[maybe_unused]] const uint64_t rstep = nw * kU;
+  if constexpr (kTma) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pipe = reinterpret_cast<BuPipe<kU>*>(smem_raw + sizeof(Smem)) + wib;
+    if (lane == 0) {
+      mbar_init(&pipe->bar[0], 1);
+      mbar_init(&pipe->bar[1], 1);
+      fence_mbar_init();
+      fence_proxy_async_global();
+      bu_issue<kU>(p, pipe, 0, gw * kU);
+      bu_issue<kU>(p, pipe, 1, gw * kU + rstep);
+    }
+    __syncwarp();
+  }
+  int it = 0;
+  for (uint64_t w0 = wlo_of(p) + gw * kU; w0 < whi_of(p); w0 += nw * kU, ++it) {
     // the run's words: w0 + k (one partition), or one owned-word mapping per
     // run (partitioned: aligned runs of 8 are 8 hub words G apart or one block)
     uint64_t wb = 0, ws = 0;
@@ -683,6 +742,40 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
     };
     uint32_t vis[kU];
     bool any = false;
+    uint32_t f[kU];
+    if constexpr (kTma) {
+      const int sg = it & 1;
+      mbar_wait(&pipe->bar[sg], (it >> 1) & 1);
+      const BuStage<kU>& st = pipe->st[sg];
+      const uint32_t off = static_cast<uint32_t>(w0 & 3);  // words before w0 in the aligned span
+#pragma unroll
+      for (int k = 0; k < kU; ++k) {
+        vis[k] = w0 + k < whi_of(p) ? st.vw[off + k] : ~0u;
+        any |= vis[k] != ~0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kU; ++k) f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : st.cf[k * 32 + lane];
+#ifdef ETB_DEBUG_CHECKS
+#pragma unroll
+      for (int k = 0; k < kU; ++k) {
+        ETB_DCHECK(w0 + k >= whi_of(p) || vis[k] == __ldcg(&p.visited[w0 + k]));
+        ETB_DCHECK(w0 + k >= whi_of(p) || st.cf[k * 32 + lane] == p.cfirst[(w0 + k) * 32 + lane]);
+      }
+#endif
+      {  // every lane's stage reads have returned (their values are consumed by
+         // the warp-wide reduction) before the async proxy may overwrite the stage
+        uint32_t x = 0;
+#pragma unroll
+        for (int k = 0; k < kU; ++k) x |= f[k] ^ vis[k];
+        x = __reduce_or_sync(0xffffffffu, x);
+        if (x == 0x5a5a5a5au && lane == 33) f[0] = 0;  // (never true: keeps x live)
+      }
+      if (lane == 0) {  // refill the stage with the run two iterations ahead
+        fence_proxy_async_shared();
+        bu_issue<kU>(p, pipe, sg, w0 + 2 * rstep);
+      }
+      if (!any) continue;
+    } else {
 #if ETB_BU_EAGER
     // first neighbours loaded with the visited words, not after them (one
     // round trip less per iteration; bu_step runs on levels where most of the
@@ -696,7 +789,6 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       any |= vis[k] != ~0u;
     }
     if (!any) continue;
-    uint32_t f[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : cf[k];
 #else
@@ -706,11 +798,11 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       any |= vis[k] != ~0u;
     }
     if (!any) continue;
-    uint32_t f[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k)
       f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[wrd(k) * 32 + lane];
 #endif
+    }
     bool hit[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
@@ -745,6 +837,13 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
     if (nmiss > kMissCap - 32 * kU) {
       resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
       nmiss = 0;
+    }
+  }
+  if constexpr (kTma) {  // every requested run was consumed: retire the barriers
+    __syncwarp();
+    if (lane == 0) {
+      mbar_inval(&pipe->bar[0]);
+      mbar_inval(&pipe->bar[1]);
     }
   }
   if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
@@ -1482,6 +1581,46 @@ __device__ void part_push(const PartParams& pp, uint32_t part, const PartView& v
   }
 }
 
+// Bottom-up levels: each warp pushes the owned next-frontier words IT wrote —
+// bu_step / bu_sweep give every owned word one writer, the warp whose run
+// holds it (claims of the first probes and of the deferred misses alike) — so
+// the words are final when the warp's step returns and the push needs no
+// partition barrier. Runs: R consecutive owned indices starting at
+// (gw + i * nw) * R, gw / nw as in bu_step (CTA-major). kCount: also the
+// claimed vertices' full degrees (the scout of a top-down level run bottom-up).
+template <int R, bool kCount>
+__device__ void part_push_own(const PartParams& pp, uint32_t part, const PartView& v, uint32_t ring,
+                              bool dense, const uint32_t* fnext, unsigned long long& scout) {
+  static_assert(R == 8 || R == 32, "bu_step runs of 8 or bu_sweep runs of 32");
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)v.cta * (blockDim.x >> 5) + wib;
+  const uint64_t nw = (uint64_t)(v.ncta * blockDim.x) >> 5;
+  constexpr unsigned kRuns = 32 / R;  // runs per warp iteration
+  __syncwarp();
+  for (uint64_t i0 = 0;; i0 += kRuns) {
+    const uint64_t first = (gw + i0 * nw) * R;
+    if (first >= v.nwo) break;
+    const uint64_t j = (gw + (i0 + lane / R) * nw) * R + lane % R;
+    const bool in = j < v.nwo;
+    const uint32_t wi = in ? static_cast<uint32_t>(word_at(v, j)) : 0u;
+    const uint32_t f = in ? __ldcg(&fnext[wi]) : 0u;
+    for (uint32_t q = 0; q < pp.nparts; ++q) {
+      if (q == part || !in || (!dense && f == 0u)) continue;
+      const PartDev& pq = pp.parts[q];
+      uint32_t* dst = ring == 0 ? pq.fb0 : (ring == 1 ? pq.fb1 : pq.fb2);
+      dst[wi] = f;
+    }
+    if (kCount && __any_sync(0xffffffffu, f != 0)) {
+#pragma unroll 4
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t bits = __shfl_sync(0xffffffffu, f, k);
+        const uint32_t w = __shfl_sync(0xffffffffu, wi, k);
+        if ((bits >> lane) & 1u) scout += v.degn[(uint64_t)w * 32 + lane];
+      }
+    }
+  }
+}
+
 // Does partition `part` of G own relaid vertex x (core block, tree by anchor,
 // component trees and isolated vertices to the last partition)?
 __device__ __forceinline__ bool owns(const BfsParams& p, const PartDev& me, uint32_t part,
@@ -1588,31 +1727,27 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
       const int32_t dnext = p.base_depth + static_cast<int32_t>(L) + 1;
       unsigned long long claims_acc = 0, scout_acc = 0;
       uint32_t* mb = sm.w[threadIdx.x >> 5].cbuf;
-      if (bu) {
-        prev = awake;
-        if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
+      const bool td_bu = !bu && p.td_as_bu > 0.0 && !p.top_down_only && L > 0 &&
+                         (double)scout > p.td_as_bu * (double)(p.nc - reached);
+      if (bu || td_bu) {
+        // bottom-up, or a top-down level executed as a bottom-up sweep over the
+        // owned unvisited words (as et_bfs_body; decided on the frontier's full
+        // degree sum, known to every partition before any list is built): same
+        // claims, its scout counted by the push. No partition barrier: every
+        // warp pushes the owned words it wrote (part_push_own).
+        if (bu) prev = awake;
+        else etc -= (double)scout;
+        const uint32_t ring = (L + 1) % 3;
+        if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc) {
           bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
-        else
+          if (td_bu) part_push_own<32, true>(pp, part, v, ring, L == 0, fnext, scout_acc);
+          else part_push_own<32, false>(pp, part, v, ring, L == 0, fnext, scout_acc);
+        } else {
           bu_step<kBuU>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
+          if (td_bu) part_push_own<kBuU, true>(pp, part, v, ring, L == 0, fnext, scout_acc);
+          else part_push_own<kBuU, false>(pp, part, v, ring, L == 0, fnext, scout_acc);
+        }
         if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
-        group_sync(me.bar, gsize);  // the owned next words are final
-        unsigned long long none = 0;
-        part_push<false>(pp, part, v, (L + 1) % 3, L == 0, fnext, none, none);
-      } else if (p.td_as_bu > 0.0 && !p.top_down_only && L > 0 &&
-                 (double)scout > p.td_as_bu * (double)(p.nc - reached)) {
-        // a top-down level executed as a bottom-up sweep over the owned
-        // unvisited words (as et_bfs_body; decided on the frontier's full degree
-        // sum, known to every partition before any list is built): same claims,
-        // counted with the scout by the push pass
-        etc -= (double)scout;
-        if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
-          bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
-        else
-          bu_step<kBuU>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
-        claims_acc = 0;
-        if (p.bstamp && threadIdx.x == 0 && L < 62) p.bstamp[L * gridDim.x + blockIdx.x] = gtimer();
-        group_sync(me.bar, gsize);
-        part_push<true>(pp, part, v, (L + 1) % 3, L == 0, fnext, claims_acc, scout_acc);
       } else {
         etc -= (double)scout;
         uint64_t nq = 0, ne = 0;
@@ -1781,6 +1916,14 @@ const void* part_kernel_for(int block) {
 
 size_t bfs_smem_bytes() { return sizeof(Smem); }
 
+// The single-partition kernel's dynamic shared memory: Smem plus, with the
+// TMA-fed bottom-up step, one two-stage pipe per warp.
+size_t bfs_kernel_smem(int block) {
+  if (!ETB_BU_TMA) return sizeof(Smem);
+  const size_t pipe = block == kSmallBlock ? sizeof(BuPipe<kBuUSmall>) : sizeof(BuPipe<kBuU>);
+  return sizeof(Smem) + static_cast<size_t>(block / 32) * pipe;
+}
+
 // Checked builds: the source line of the first failed device check (0: none,
 // or an unchecked build); reading it clears it.
 unsigned debug_check_line() {
@@ -1805,7 +1948,9 @@ int block_for(uint64_t nc) {
 void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   const uint64_t n = L.n;
   S.n = n;
-  const uint64_t words = (L.nc + 31) / 32 + 1;
+  // per half: whole words + 1, rounded to 16 bytes (every half starts aligned
+  // for the bottom-up step's bulk copies)
+  const uint64_t words = ((L.nc + 31) / 32 + 1 + 3) & ~uint64_t{3};
   S.words = words;
   S.bits.alloc(8 * words);
   const uint64_t cap = L.nc + 2;
@@ -1844,8 +1989,9 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   S.block = block_for(L.nc);
   const void* k = kernel_for(S.block);
   ETB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(Smem)));
-  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S.block, sizeof(Smem)));
+                                (int)bfs_kernel_smem(S.block)));
+  ETB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S.block,
+                                                         bfs_kernel_smem(S.block)));
   if (per_sm < 1) throw CudaError("et_bfs_kernel cannot be resident");
   S.grid = sms;  // one CTA per SM (the level barrier's arrivals)
   // L2 access-policy window over the per-root bitmap state (on by default,
@@ -2031,7 +2177,7 @@ void empty_launch(const BfsState& S, cudaStream_t s) {
 void bfs_launch(const BfsParams& p, BfsState& S, cudaStream_t s) {
   void* args[] = {const_cast<BfsParams*>(&p)};
   ETB_CUDA(cudaLaunchCooperativeKernel(kernel_for(S.block), dim3(S.grid), dim3(S.block), args,
-                                       sizeof(Smem), s));
+                                       bfs_kernel_smem(S.block), s));
   S.parity ^= 1u;  // this launch cleans the other half; the next one uses it
 }
 

@@ -723,7 +723,10 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
   }
   L.ecore = read_u64(L.crow.get() + nc, s);
   L.ccol.alloc(L.ecore ? L.ecore : 1);
-  L.cfirst.alloc(nc ? nc : 1);
+  // padded to whole bitmap words (the bottom-up step copies whole words' runs
+  // with the TMA engine); the padding reads as "no neighbour"
+  L.cfirst.alloc((nc + 31) / 32 * 32 + 32);
+  ETB_CUDA(cudaMemsetAsync(L.cfirst.get(), 0xFF, L.cfirst.bytes(), s));
   L.csecond.alloc(nc ? nc : 1);
   // (csecond keeps a flag in bit 31 of a core id)
   if (nc >= (uint64_t{1} << 31)) throw std::runtime_error("relayout_csr: core of 2^31 vertices or more");

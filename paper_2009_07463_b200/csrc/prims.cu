@@ -31,14 +31,6 @@ constexpr int kTile = kT * kIpt;  // 4096 items per scan tile
 constexpr int kWarps = kT / 32;
 constexpr int kRadix = 256;
 
-struct Temp {
-  DevBuf<uint8_t> buf;
-  uint8_t* get(size_t bytes) {
-    if (buf.size() < bytes) buf.alloc(bytes + (bytes >> 3) + 256);
-    return buf.get();
-  }
-};
-
 // ---- block scan of one value per thread (exclusive, returns the block total) ----
 template <class T, class Op>
 __device__ __forceinline__ T block_excl_scan(T v, T identity, Op op, T* warp_tot, T& total) {
@@ -340,11 +332,6 @@ void radix_sort(DevBuf<uint64_t>& keys, DevBuf<uint64_t>& kalt, DevBuf<uint32_t>
     std::swap(keys, kalt);
     if (kPairs) std::swap(*vals, *valt);
   }
-}
-
-Temp& temp() {
-  static thread_local Temp t;
-  return t;
 }
 
 }  // namespace

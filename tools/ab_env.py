@@ -24,6 +24,8 @@ def child(args):
     from bench import harmonic_gteps, select_roots_from_degrees
     g = eb.generate_graph(scale=args.scale, edgefactor=args.edgefactor, seed=1)
     cg = eb.relayout_csr(g, mh=args.mh)
+    if args.parts > 1:  # the 1D core partition, G partitions emulated on this GPU
+        E.partition(cg, args.parts)
     roots = select_roots_from_degrees(g.degrees(), 64, 1)
     starts = cg.old2new[roots.astype(np.int64)]
     te = np.empty(64)
@@ -46,6 +48,7 @@ def main():
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--mh", type=int, default=-1)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--parts", type=int, default=1)
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--variants", nargs="*", default=[])
     ap.add_argument("--child", action="store_true")
@@ -60,7 +63,8 @@ def main():
                 env[k] = val
             r = subprocess.run([sys.executable, os.path.abspath(__file__), "--child",
                                 "--scale", str(args.scale), "--edgefactor", str(args.edgefactor),
-                                "--mh", str(args.mh), "--steps", str(args.steps)],
+                                "--mh", str(args.mh), "--steps", str(args.steps),
+                                "--parts", str(args.parts)],
                                env=env, capture_output=True, text=True)
             line = [x for x in r.stdout.splitlines() if x.startswith("{")]
             print(f"[{rep}] {v:40s} {line[0] if line else r.stderr[-500:]}", flush=True)
