@@ -95,7 +95,20 @@ struct Smem {
   WarpSmem w[kMaxWarps];
   unsigned long long red[2][kMaxWarps];
   unsigned long long tot[4];  // level totals read once per CTA after the barrier
+  unsigned int bu_next;       // bottom-up: the CTA's next run (reset at every grid barrier)
+  unsigned int pad[3];
 };
+__device__ __forceinline__ Smem& smem_view() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return *reinterpret_cast<Smem*>(smem_raw);
+}
+// Bottom-up steps of the single-partition kernel hand out their CTA's runs
+// (the same runs as the static warp striding) from a shared-memory counter, so
+// warps that drew cheap runs take more and the level barrier waits less on the
+// warps whose deferred misses were long.
+#ifndef ETB_BU_DYN
+#define ETB_BU_DYN 1
+#endif
 static_assert(sizeof(Smem) % 16 == 0, "the bottom-up pipes follow Smem, 16-byte aligned");
 
 // Bottom-up runs fetched by the TMA engine (single-partition kernel, built with
@@ -157,6 +170,7 @@ __device__ void grid_sync_add(unsigned long long* bar, Smem& sm, unsigned long l
       grid_arrive_wait(bar);
       for (int k = 0; k < n; ++k) sm.tot[k] = ld_volatile(&rd[k]);
     }
+    if (threadIdx.x == 0) sm.bu_next = 0;
   }
   __syncthreads();
 }
@@ -726,8 +740,19 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
     }
     __syncwarp();
   }
+  // (large-core kernel only, kU == kBuU: s26 +2.4%, s28 +1.6%; the small-core
+  // kernel's short levels lose more to the counter than they gain: s22 -1.1%)
+  constexpr bool kDyn = ETB_BU_DYN && !kTma && !IsPart<P>::value && kU == kBuU;
+  [[maybe_unused]] const uint64_t wpc = blockDim.x >> 5;
+  auto grab = [&]() -> uint64_t {  // the CTA's next run: cta*wpc + (k / wpc)*nw + k % wpc
+    unsigned k = 0;
+    if (lane == 0) k = atomicAdd(&smem_view().bu_next, 1u);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    return ((uint64_t)cta_of(p) * wpc + (uint64_t)(k / wpc) * nw + k % wpc) * kU;
+  };
   int it = 0;
-  for (uint64_t w0 = wlo_of(p) + gw * kU; w0 < whi_of(p); w0 += nw * kU, ++it) {
+  for (uint64_t w0 = kDyn ? grab() : wlo_of(p) + gw * kU; w0 < whi_of(p);
+       w0 = kDyn ? grab() : w0 + nw * kU, ++it) {
     // the run's words: w0 + k (one partition), or one owned-word mapping per
     // run (partitioned: aligned runs of 8 are 8 hub words G apart or one block)
     uint64_t wb = 0, ws = 0;
@@ -863,7 +888,16 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
   // A warp sweeps kSweep visited words with one coalesced load (lane = word)
   // and works through the words with unvisited vertices kBuU at a time, so
   // late levels (few unvisited left) skip full words without a round trip each.
-  for (uint64_t b0 = wlo_of(p) + gw * kSweep; b0 < whi_of(p); b0 += nw * kSweep) {
+  constexpr bool kDyn = ETB_BU_DYN && !IsPart<P>::value;
+  [[maybe_unused]] const uint64_t wpc = blockDim.x >> 5;
+  auto grab = [&]() -> uint64_t {  // as bu_step's: the CTA's next run of kSweep words
+    unsigned k = 0;
+    if (lane == 0) k = atomicAdd(&smem_view().bu_next, 1u);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    return ((uint64_t)cta_of(p) * wpc + (uint64_t)(k / wpc) * nw + k % wpc) * kSweep;
+  };
+  for (uint64_t b0 = kDyn ? grab() : wlo_of(p) + gw * kSweep; b0 < whi_of(p);
+       b0 = kDyn ? grab() : b0 + nw * kSweep) {
     uint32_t myw = 0, mine;
     if constexpr (IsPart<P>::value) {
       myw = static_cast<uint32_t>(word_at(p, b0 + lane));
@@ -1015,6 +1049,7 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
   const uint32_t start = p.start;
   const bool run_core = start != kNone32;
   stamp(p, 256);
+  if (threadIdx.x == 0) sm.bu_next = 0;  // (a barrier precedes every bottom-up step)
   // diagnostics: per-CTA entry (slot 62) and exit (slot 63) times
   if (p.bstamp && threadIdx.x == 0) p.bstamp[62 * gridDim.x + blockIdx.x] = gtimer();
 

@@ -1,0 +1,15 @@
+mkdir -p gpurun_out/r02b
+free -g > gpurun_out/r02b/host.txt; nproc >> gpurun_out/r02b/host.txt; nvidia-smi -q | grep -i -A2 "max clocks" >> gpurun_out/r02b/host.txt
+timeout 900 python bench.py > gpurun_out/r02b/bench_full.json 2> gpurun_out/r02b/bench_full.err; echo rc=$? >> gpurun_out/r02b/bench_full.err
+timeout 900 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --secondary "" --no-paper-mode --emulate-partitions "" > gpurun_out/r02b/benchplain.log 2>&1 && \
+timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r02b/launches_s26.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --secondary "" --no-paper-mode --emulate-partitions "" > gpurun_out/r02b/launches.log 2>&1
+for spec in "26 0 s26_root0" "26 2 s26_slowroot" "22 0 s22_root0"; do
+  set -- $spec
+  timeout 600 python tools/one_root.py --scale $1 --index $2 --reps 3 > gpurun_out/r02b/plain_$3.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:et_bfs_kernel -s 2 -c 1 -o gpurun_out/r02b/et_bfs_$3 python tools/one_root.py --scale $1 --index $2 --reps 3 > gpurun_out/r02b/ncu_$3.log 2>&1
+done
+for sc in 22 26 28; do
+timeout 900 python tools/traffic_capture.py --scale $sc --roots 16 > gpurun_out/r02b/tplain$sc.log 2>&1 && \
+timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:et_bfs_kernel --csv --log-file gpurun_out/r02b/traffic_s$sc.csv python tools/traffic_capture.py --scale $sc --roots 16 > gpurun_out/r02b/tncu$sc.log 2>&1
+done
+echo done > gpurun_out/r02b/done.txt
