@@ -558,8 +558,10 @@ template <class P>
 __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
                              uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
                              unsigned long long& claims_acc, uint32_t* qv_out,
-                             uint64_t* qp_out, unsigned long long* lslot, uint32_t skip) {
+                             uint64_t* qp_out, unsigned long long* lslot, uint32_t skip,
+                             unsigned long long* scout) {
   const unsigned lane = threadIdx.x & 31;
+  unsigned long long sc = 0;  // Σ full degree of the claims (when scout is wanted)
   __syncwarp();
   ETB_DIAG_COUNT(160 + (dnext & 31), nmiss);
   uint32_t nlong = 0;
@@ -582,12 +584,14 @@ __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
       atomicOr(&p.visited[va >> 5], 1u << (va & 31));
       atomicOr(&fnext[va >> 5], 1u << (va & 31));
       ++claims_acc;
+      if (scout) sc += p.degn[va];
     }
     if (hb) {
       p.dp[vb] = make_uint2(static_cast<uint32_t>(dnext), pb);
       atomicOr(&p.visited[vb >> 5], 1u << (vb & 31));
       atomicOr(&fnext[vb >> 5], 1u << (vb & 31));
       ++claims_acc;
+      if (scout) sc += p.degn[vb];
     }
     if (lslot) {
       const uint32_t av[2] = {va, vb};
@@ -626,6 +630,7 @@ __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
       atomicOr(&p.visited[v >> 5], 1u << (v & 31));
       atomicOr(&fnext[v >> 5], 1u << (v & 31));
       ++claims_acc;
+      if (scout) sc += p.degn[v];
     }
     if (lslot) {
       const uint32_t av[1] = {v}, ad[1] = {lane == 0 && par != kNone32 ? p.cmeta[v].x : 0u};
@@ -633,6 +638,7 @@ __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
     }
   }
   __syncwarp();
+  if (scout) *scout += sc;
 }
 
 // Deferred misses: vertices whose first (highest-degree) neighbour is not in
@@ -649,8 +655,10 @@ template <class P>
 __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext,
                                uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
                                unsigned long long& claims_acc, uint32_t* qv_out,
-                               uint64_t* qp_out, unsigned long long* lslot) {
+                               uint64_t* qp_out, unsigned long long* lslot,
+                               unsigned long long* scout) {
   const unsigned lane = threadIdx.x & 31, lt = (1u << lane) - 1;
+  unsigned long long sc2 = 0;
   __syncwarp();
   ETB_DIAG_BEGIN();
   ETB_DIAG_COUNT(128 + (dnext & 31), nmiss);
@@ -674,6 +682,7 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
       atomicOr(&p.visited[v[k] >> 5], 1u << (v[k] & 31));
       atomicOr(&fnext[v[k] >> 5], 1u << (v[k] & 31));
       ++claims_acc;
+      if (scout) sc2 += p.degn[v[k]];
     }
     if (lslot) {
       uint32_t ad[4];
@@ -693,7 +702,9 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
     }
     __syncwarp();
   }
-  if (nlong) resolve_rows(p, fcur, fnext, mbuf, nlong, dnext, claims_acc, qv_out, qp_out, lslot, 2);
+  if (nlong)
+    resolve_rows(p, fcur, fnext, mbuf, nlong, dnext, claims_acc, qv_out, qp_out, lslot, 2, scout);
+  if (scout) *scout += sc2;
   ETB_DIAG_END(64 + (dnext & 63));
 }
 
@@ -716,13 +727,15 @@ __device__ __forceinline__ void bu_issue(const BfsParams& p, BuPipe<kU>* pipe, i
 template <int kU, class P>
 __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
-                        uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot) {
+                        uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot,
+                        unsigned long long* scout = nullptr) {
   static_assert(32 * kU <= kMissCap, "one iteration's misses must fit the miss buffer");
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)cta_of(p) * (blockDim.x >> 5) + wib;
   const uint64_t nw = (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
+  unsigned long long scm = 0;  // main-pass claims' full degrees (scout wanted)
   ETB_DIAG_BEGIN();
   constexpr bool kTma = ETB_BU_TMA && !IsPart<P>::value;
   [[maybe_unused]] BuPipe<kU>* pipe = nullptr;
@@ -838,6 +851,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
       if (hit[k]) {
         p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), f[k]);
+        if (scout) scm += p.degn[v];
       }
       if (lane == 0 && m) {
         p.visited[wk] = vis[k] | m;
@@ -860,7 +874,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       bu_append<kU>(av, ad, qv_out, qp_out, lslot);
     }
     if (nmiss > kMissCap - 32 * kU) {
-      resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
+      resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
       nmiss = 0;
     }
   }
@@ -871,19 +885,22 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       mbar_inval(&pipe->bar[1]);
     }
   }
-  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
+  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
+  if (scout) *scout += scm;
   ETB_DIAG_END(dnext & 63);
 }
 
 template <int kSweep, class P>
 __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
-                        uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot) {
+                        uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot,
+                        unsigned long long* scout = nullptr) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)cta_of(p) * (blockDim.x >> 5) + wib;
   const uint64_t nw = (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   uint32_t nmiss = 0;
+  unsigned long long scm = 0;  // main-pass claims' full degrees (scout wanted)
   ETB_DIAG_BEGIN();
   // A warp sweeps kSweep visited words with one coalesced load (lane = word)
   // and works through the words with unvisited vertices kBuU at a time, so
@@ -931,6 +948,7 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
         const unsigned m = __ballot_sync(0xffffffffu, hit[k]);
         if (hit[k]) {
           p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), f[k]);
+          if (scout) scm += p.degn[v];
         }
         if (lane == 0 && m) {
           p.visited[wi[k]] = vis[k] | m;
@@ -953,12 +971,13 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
         bu_append<kBuU>(av, ad, qv_out, qp_out, lslot);
       }
       if (nmiss > kMissCap - 32 * kBuU) {
-        resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
+        resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
         nmiss = 0;
       }
     }
   }
-  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot);
+  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
+  if (scout) *scout += scm;
   ETB_DIAG_END(dnext & 63);
 }
 
@@ -1008,23 +1027,27 @@ __device__ void convert_step(const BfsParams& p, const uint32_t* fcur, uint32_t*
 // new frontier bitmap f: a warp takes 4 words per iteration, lane = vertex,
 // coalesced degree loads — a streaming pass instead of one random 32-byte
 // sector per claim, and the level's claims need no atomic return (td_step<3>).
+#ifndef ETB_SCOUT_W
+#define ETB_SCOUT_W 16  // (s26: 16 +0.5% against 4, 8 equal)
+#endif
 __device__ unsigned long long scout_pass(const BfsParams& p, const uint32_t* f,
                                          unsigned long long& claims) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long s = 0, c = 0;
-  for (uint64_t w0 = gw * 4; w0 < p.nwords; w0 += nw * 4) {
-    uint32_t d[4];
+  constexpr int W = ETB_SCOUT_W;  // words per warp iteration: W bitmap loads, then W degree loads
+  for (uint64_t w0 = gw * W; w0 < p.nwords; w0 += nw * W) {
+    uint32_t bits[W], d[W];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t wi = w0 + k;
-      const uint32_t bits = wi < p.nwords ? __ldcg(&f[wi]) : 0u;
-      c += (bits >> lane) & 1u;
-      d[k] = ((bits >> lane) & 1u) ? p.degn[wi * 32 + lane] : 0u;
+    for (int k = 0; k < W; ++k) bits[k] = w0 + k < p.nwords ? __ldcg(&f[w0 + k]) : 0u;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      c += (bits[k] >> lane) & 1u;
+      d[k] = ((bits[k] >> lane) & 1u) ? p.degn[(w0 + k) * 32 + lane] : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) s += d[k];
+    for (int k = 0; k < W; ++k) s += d[k];
   }
   claims += c;
   return s;
@@ -1216,14 +1239,19 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         // scout are counted from the new frontier bitmap (scout_pass)
         etc -= (double)scout;
         list_valid = false;
-        defer_scout = true;
+        // Small-core kernel: the level's scout is summed by the step itself,
+        // one degree load per claim (s22 +1.2%); large-core kernel: claims and
+        // scout counted afterwards by scout_pass (the in-step sums cost its
+        // register-bound bottom-up code spills: s26 -1.2%).
+        defer_scout = kLarge;
         if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc)
           bu_sweep<32>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in,
                        qp_in, nullptr);
         else
           bu_step<kLarge ? kBuU : kBuUSmall>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext,
-                                             claims_acc, qv_in, qp_in, nullptr);
-        claims_acc = 0;
+                                             claims_acc, qv_in, qp_in, nullptr,
+                                             kLarge ? nullptr : &scout_acc);
+        if (kLarge) claims_acc = 0;
       } else {
         etc -= (double)scout;
         // The next frontier list is emitted only when this frontier's edge count
