@@ -109,6 +109,12 @@ __device__ __forceinline__ Smem& smem_view() {
 #ifndef ETB_BU_DYN
 #define ETB_BU_DYN 1
 #endif
+// The partitioned kernel's bottom-up steps likewise (its CTA group's runs of
+// owned words); the owned words are then pushed after a partition barrier, as
+// a warp no longer knows which runs it wrote.
+#ifndef ETB_PART_DYN
+#define ETB_PART_DYN 1
+#endif
 static_assert(sizeof(Smem) % 16 == 0, "the bottom-up pipes follow Smem, 16-byte aligned");
 
 // Bottom-up runs fetched by the TMA engine (single-partition kernel, built with
@@ -755,7 +761,9 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
   }
   // (large-core kernel only, kU == kBuU: s26 +2.4%, s28 +1.6%; the small-core
   // kernel's short levels lose more to the counter than they gain: s22 -1.1%)
-  constexpr bool kDyn = ETB_BU_DYN && !kTma && !IsPart<P>::value && kU == kBuU;
+  // (partitioned kernel: p.dyn, set on the large-core instantiation only)
+  bool kDyn = ETB_BU_DYN && !kTma && kU == kBuU;
+  if constexpr (IsPart<P>::value) kDyn = kDyn && p.dyn;
   [[maybe_unused]] const uint64_t wpc = blockDim.x >> 5;
   auto grab = [&]() -> uint64_t {  // the CTA's next run: cta*wpc + (k / wpc)*nw + k % wpc
     unsigned k = 0;
@@ -905,7 +913,8 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
   // A warp sweeps kSweep visited words with one coalesced load (lane = word)
   // and works through the words with unvisited vertices kBuU at a time, so
   // late levels (few unvisited left) skip full words without a round trip each.
-  constexpr bool kDyn = ETB_BU_DYN && !IsPart<P>::value;
+  bool kDyn = ETB_BU_DYN;
+  if constexpr (IsPart<P>::value) kDyn = kDyn && p.dyn;
   [[maybe_unused]] const uint64_t wpc = blockDim.x >> 5;
   auto grab = [&]() -> uint64_t {  // as bu_step's: the CTA's next run of kSweep words
     unsigned k = 0;
@@ -1475,6 +1484,7 @@ struct PartView {
   unsigned cta, ncta;
   unsigned long long* wstamp;  // (ETB_WARP_STAMPS diagnostics: unused here)
   int32_t wdepth;
+  bool dyn;  // bottom-up runs from the CTA's counter (large-core kernel)
 };
 __device__ __forceinline__ uint64_t wlo_of(const PartView&) { return 0; }
 __device__ __forceinline__ uint32_t whi_of(const PartView& v) { return v.nwo; }
@@ -1512,6 +1522,7 @@ __device__ __forceinline__ void group_sync(unsigned long long* bar, unsigned n) 
     const long long t0 = clock64();
     while (ld_acquire(bar) < target)
       if (clock64() - t0 > 40000000000ll) __trap();
+    smem_view().bu_next = 0;
   }
   __syncthreads();
 }
@@ -1559,6 +1570,7 @@ __device__ void part_level_sync(const PartParams& pp, uint32_t part, unsigned pa
       while ((sys ? ld_acquire_sys(me_arrive) : ld_acquire(me_arrive)) < target)
         if (clock64() - t0 > 40000000000ll) __trap();
       for (int k = 0; k < n; ++k) sm.tot[k] = ld_volatile(&rd[k]);
+      sm.bu_next = 0;
     }
   }
   __syncthreads();
@@ -1729,6 +1741,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   v.ncta = gsize;
   v.wstamp = nullptr;
   v.wdepth = -1;
+  v.dyn = ETB_PART_DYN && kLarge;  // (s26 G = 2 +1.3%; s22 G = 8 -6%: the barrier it needs)
   PartView vt = v;  // top-down view: the partition's owned-neighbour CSR
   vt.crow = me.trow;
   vt.ccol = me.tcol;
@@ -1741,6 +1754,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   const bool run_core = start != kNone32;
   if (stats) p.level_claims[256] = gtimer();
   if (p.bstamp && threadIdx.x == 0) p.bstamp[62 * gridDim.x + blockIdx.x] = gtimer();
+  if (threadIdx.x == 0) sm.bu_next = 0;
 
   // ---- init: this partition's own memory only (no cross barrier) -------------
   if (gtid < 18) me.ctr[32 * (par ^ 1u) + gtid] = 0;
@@ -1801,12 +1815,22 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         if (bu) prev = awake;
         else etc -= (double)scout;
         const uint32_t ring = (L + 1) % 3;
-        if (kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc) {
-          bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
+        const bool sweep = kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc;
+        if (sweep) bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
+        else bu_step<kBuU>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
+        if (v.dyn) {
+          group_sync(me.bar, gsize);  // the owned next words are final
+          unsigned long long none = 0;
+          if (td_bu) {
+            claims_acc = 0;  // recounted from the pushed words, with the scout
+            part_push<true>(pp, part, v, ring, L == 0, fnext, claims_acc, scout_acc);
+          } else {
+            part_push<false>(pp, part, v, ring, L == 0, fnext, none, none);
+          }
+        } else if (sweep) {
           if (td_bu) part_push_own<32, true>(pp, part, v, ring, L == 0, fnext, scout_acc);
           else part_push_own<32, false>(pp, part, v, ring, L == 0, fnext, scout_acc);
         } else {
-          bu_step<kBuU>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
           if (td_bu) part_push_own<kBuU, true>(pp, part, v, ring, L == 0, fnext, scout_acc);
           else part_push_own<kBuU, false>(pp, part, v, ring, L == 0, fnext, scout_acc);
         }
