@@ -109,9 +109,8 @@ __device__ __forceinline__ Smem& smem_view() {
 #ifndef ETB_BU_DYN
 #define ETB_BU_DYN 1
 #endif
-// The partitioned kernel's bottom-up steps likewise (its CTA group's runs of
-// owned words); the owned words are then pushed after a partition barrier, as
-// a warp no longer knows which runs it wrote.
+// The partitioned kernel's bottom-up steps likewise (its CTA's runs of owned
+// words); the CTA's warps then push the CTA's runs after a CTA barrier.
 #ifndef ETB_PART_DYN
 #define ETB_PART_DYN 1
 #endif
@@ -1741,7 +1740,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   v.ncta = gsize;
   v.wstamp = nullptr;
   v.wdepth = -1;
-  v.dyn = ETB_PART_DYN && kLarge;  // (s26 G = 2 +1.3%; s22 G = 8 -6%: the barrier it needs)
+  v.dyn = ETB_PART_DYN && kLarge;
   PartView vt = v;  // top-down view: the partition's owned-neighbour CSR
   vt.crow = me.trow;
   vt.ccol = me.tcol;
@@ -1818,16 +1817,11 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
         const bool sweep = kLarge && (double)(p.nc - reached) * kSweepT < (double)p.nc;
         if (sweep) bu_sweep<32>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
         else bu_step<kBuU>(v, mb, fcur, fnext, dnext, claims_acc, nullptr, nullptr, nullptr);
-        if (v.dyn) {
-          group_sync(me.bar, gsize);  // the owned next words are final
-          unsigned long long none = 0;
-          if (td_bu) {
-            claims_acc = 0;  // recounted from the pushed words, with the scout
-            part_push<true>(pp, part, v, ring, L == 0, fnext, claims_acc, scout_acc);
-          } else {
-            part_push<false>(pp, part, v, ring, L == 0, fnext, none, none);
-          }
-        } else if (sweep) {
+        // With the CTA's run counter (v.dyn) the CTA's warps shared its runs:
+        // once the CTA is through (a CTA barrier), each warp pushes its static
+        // share of them — the same run set, final words.
+        if (v.dyn) __syncthreads();
+        if (sweep) {
           if (td_bu) part_push_own<32, true>(pp, part, v, ring, L == 0, fnext, scout_acc);
           else part_push_own<32, false>(pp, part, v, ring, L == 0, fnext, scout_acc);
         } else {
