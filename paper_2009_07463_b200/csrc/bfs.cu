@@ -2087,7 +2087,10 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   const char* pe = getenv("ETB_L2_PERSIST");
   if ((!pe || atoi(pe) > 0) && S.bits.bytes() <= static_cast<size_t>(maxp) / 2) {
     const size_t want = S.bits.bytes();
-    ETB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    // the carve-out is per device: never shrink it under another layout's window
+    size_t cur = 0;
+    ETB_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+    if (cur < want) ETB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
     cudaStreamAttrValue a = {};
     a.accessPolicyWindow.base_ptr = S.bits.get();
     a.accessPolicyWindow.num_bytes = want;
