@@ -453,13 +453,19 @@ __device__ void td_step(const P& p, uint32_t* cbuf, int32_t* win, const uint32_t
 // trips; measured against lane-only scans up to 1024 neighbours: -0.5 us per
 // root at s22, -2 us at s26).
 constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (the claim buffer + the window)
-constexpr uint32_t kLaneFirst = 64;
+#ifndef ETB_LANE_FIRST
+#define ETB_LANE_FIRST 64
+#endif
+constexpr uint32_t kLaneFirst = ETB_LANE_FIRST;
 // csecond entries: the second core neighbour; bit 31 set when it ends the row
 constexpr uint32_t kSecondMask = 0x7FFFFFFFu;
 // bu_sweep on the large-core kernel once fewer than nc / kSweepT vertices are
 // unvisited (measured at s26: 2 best, -5 us per root; inlined — out of line its
 // call cost the rest of the kernel 3%)
-constexpr double kSweepT = 2.0;
+#ifndef ETB_SWEEP_T
+#define ETB_SWEEP_T 2.0
+#endif
+constexpr double kSweepT = ETB_SWEEP_T;
 
 // Bottom-up list emission (a level predicted to hand over to top-down): the
 // warp appends its claims, up to K per lane, to the next frontier list with one
