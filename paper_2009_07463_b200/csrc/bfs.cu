@@ -453,6 +453,11 @@ __device__ void td_step(const P& p, uint32_t* cbuf, int32_t* win, const uint32_t
 // trips; measured against lane-only scans up to 1024 neighbours: -0.5 us per
 // root at s22, -2 us at s26).
 constexpr int kMissCap = 2 * kCbuf;  // u32 entries per warp (the claim buffer + the window)
+// deferred misses are resolved once more than this many are pending (or the buffer is full)
+#ifndef ETB_MISS_FLUSH
+#define ETB_MISS_FLUSH 1024
+#endif
+constexpr int kMissFlush = ETB_MISS_FLUSH;
 #ifndef ETB_LANE_FIRST
 #define ETB_LANE_FIRST 64
 #endif
@@ -886,7 +891,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       }
       bu_append<kU>(av, ad, qv_out, qp_out, lslot);
     }
-    if (nmiss > kMissCap - 32 * kU) {
+    if (nmiss > min(kMissCap - 32 * kU, kMissFlush)) {
       resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
       nmiss = 0;
     }
@@ -984,7 +989,7 @@ __device__ __forceinline__ void bu_sweep(const P& p, uint32_t* mbuf, const uint3
         }
         bu_append<kBuU>(av, ad, qv_out, qp_out, lslot);
       }
-      if (nmiss > kMissCap - 32 * kBuU) {
+      if (nmiss > min(kMissCap - 32 * kBuU, kMissFlush)) {
         resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
         nmiss = 0;
       }
@@ -1135,7 +1140,13 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
     const uint32_t d0 = static_cast<uint32_t>(ne);
     // (Small-core kernel only: in the large-core instantiation the extra code
     // costs more in register allocation elsewhere than the 3 us it saves.)
-    if (!kLarge && !bu && !p.bottom_up_only && d0 > 0 && d0 <= blockDim.x && d0 + 1 < p.nc) {
+// (the fused first level on the large-core kernel: s26 -2.3%, s28 -1.3% — its
+// code makes the large-core kernel spill)
+#ifndef ETB_LARGE_PROLOGUE
+#define ETB_LARGE_PROLOGUE 0
+#endif
+    if ((!kLarge || ETB_LARGE_PROLOGUE) && !bu && !p.bottom_up_only && d0 > 0 &&
+        d0 <= blockDim.x && d0 + 1 < p.nc) {
       const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
       const uint64_t rs = p.crow[start];
       uint32_t w = kNone32;
