@@ -109,6 +109,7 @@ def ref() -> C.CDLL:
         _sig(L.ref_csr_n, u64, vp)
         _sig(L.ref_csr_copy, None, vp, vp, vp)
         _sig(L.ref_csr_free, None, vp)
+        _sig(L.ref_csr_alloc, vp, u64, u64, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp))
         _sig(L.ref_classify, C.c_int, vp, i64, U8P)
         _sig(L.ref_peak_height, i64, vp)
         _sig(L.ref_prepare, vp, vp, i64)

@@ -191,6 +191,26 @@ void* ref_build_csr(uint64_t n, const uint64_t* pairs, uint64_t count, uint64_t*
     return nullptr;
   }
 }
+// An empty reference CsrGraph of n vertices and nnz directed edges whose arrays
+// the caller fills in place (e.g. a device CSR downloaded straight into them:
+// no second host copy of a scale-28 column array).
+void* ref_csr_alloc(uint64_t n, uint64_t nnz, uint64_t** row_offsets, uint64_t** cols,
+                    uint64_t** degrees) {
+  try {
+    auto* g = new CsrGraph;
+    g->vertex_count = n;
+    g->row_offsets.resize(n + 1);
+    g->col_indices.resize(nnz);
+    g->degrees.resize(n);
+    *row_offsets = g->row_offsets.data();
+    *cols = g->col_indices.data();
+    *degrees = g->degrees.data();
+    return g;
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
 uint64_t ref_csr_nnz(void* h) { return static_cast<CsrGraph*>(h)->col_indices.size(); }
 uint64_t ref_csr_n(void* h) { return static_cast<CsrGraph*>(h)->vertex_count; }
 void ref_csr_copy(void* h, uint64_t* row_offsets, uint64_t* cols) {
