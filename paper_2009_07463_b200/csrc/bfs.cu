@@ -463,6 +463,10 @@ constexpr int kMissFlush = ETB_MISS_FLUSH;
 #endif
 constexpr uint32_t kLaneFirst = ETB_LANE_FIRST;
 // csecond entries: the second core neighbour; bit 31 set when it ends the row
+// (cthird: the third and fourth, likewise; ETB_MISS_THIRD = 0 skips that stage)
+#ifndef ETB_MISS_THIRD
+#define ETB_MISS_THIRD 1
+#endif
 constexpr uint32_t kSecondMask = 0x7FFFFFFFu;
 // bu_sweep on the large-core kernel once fewer than nc / kSweepT vertices are
 // unvisited (measured at s26: 2 best, -5 us per root; inlined — out of line its
@@ -718,8 +722,61 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
     }
     __syncwarp();
   }
+#if ETB_MISS_THIRD
+  // Stage 2: the rows past their second neighbour probe the third and fourth
+  // (cthird, one 8-byte gather), four rows per lane; rows of five or more
+  // entries with no hit yet go on to the row scans.
+  uint32_t nl2 = 0;
+  for (uint32_t i0 = 0; i0 < nlong; i0 += 128) {
+    uint32_t v[4];
+    uint2 t3[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = i0 + lane + 32u * k;
+      v[k] = i < nlong ? mbuf[i] : kNone32;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t3[k] = v[k] != kNone32 ? p.cthird[v[k]] : make_uint2(kNone32, kNone32);
+    bool h3[4], h4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      h3[k] = t3[k].x != kNone32 && test_bit(fcur, t3[k].x & kSecondMask);
+      h4[k] = t3[k].y != kNone32 && test_bit(fcur, t3[k].y & kSecondMask);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!h3[k] && !h4[k]) continue;
+      const uint32_t par = (h3[k] ? t3[k].x : t3[k].y) & kSecondMask;
+      p.dp[v[k]] = make_uint2(static_cast<uint32_t>(dnext), par);
+      atomicOr(&p.visited[v[k] >> 5], 1u << (v[k] & 31));
+      atomicOr(&fnext[v[k] >> 5], 1u << (v[k] & 31));
+      ++claims_acc;
+      if (scout) sc2 += p.degn[v[k]];
+    }
+    if (lslot) {
+      uint32_t ad[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ad[k] = (h3[k] || h4[k]) ? p.cmeta[v[k]].x : 0u;
+      bu_append<4>(v, ad, qv_out, qp_out, lslot);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // five or more entries: the fourth exists and is not flagged as the last
+      const bool more = v[k] != kNone32 && !h3[k] && !h4[k] && t3[k].y != kNone32 &&
+                        !(t3[k].y >> 31);
+      const unsigned mk = __ballot_sync(0xffffffffu, more);
+      if (more) mbuf[nl2 + __popc(mk & lt)] = v[k];
+      nl2 += __popc(mk);
+    }
+    __syncwarp();
+  }
+  if (nl2)
+    resolve_rows(p, fcur, fnext, mbuf, nl2, dnext, claims_acc, qv_out, qp_out, lslot, 4, scout);
+#else
   if (nlong)
     resolve_rows(p, fcur, fnext, mbuf, nlong, dnext, claims_acc, qv_out, qp_out, lslot, 2, scout);
+#endif
   if (scout) *scout += sc2;
   ETB_DIAG_END(64 + (dnext & 63));
 }
@@ -1489,6 +1546,7 @@ struct PartView {
   const uint32_t* ccol;
   const uint32_t* cfirst;
   const uint32_t* csecond;
+  const uint2* cthird;
   const uint32_t* degn;
   const uint2* cmeta;
   uint2* dp;
@@ -1743,6 +1801,7 @@ __device__ __forceinline__ void et_bfs_part_body(const PartParams& pp) {
   v.ccol = p.ccol;
   v.cfirst = p.cfirst;
   v.csecond = p.csecond;
+  v.cthird = p.cthird;
   v.degn = p.degn;
   v.cmeta = p.cmeta;
   v.dp = p.dp;
@@ -2125,6 +2184,7 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.ccol = L.ccol.get();
   p.cfirst = L.cfirst.get();
   p.csecond = L.csecond.get();
+  p.cthird = L.cthird.get();
   p.reachable = L.nc;
   p.degn = L.degn.get();
   p.cmeta = L.cmeta.get();

@@ -16,6 +16,7 @@ struct BfsParams {
   const uint32_t* ccol;
   const uint32_t* cfirst;
   const uint32_t* csecond;  // second core neighbour, bit 31: last of its row (kNone32: none)
+  const uint2* cthird;      // {third, fourth} core neighbours, same flags
   const uint32_t* degn;  // full degree (scout, bfs.cpp:80)
   const uint2* cmeta;    // per core vertex {core degree, full degree}
   uint64_t reachable;  // core vertices in the start's core component (set per root)

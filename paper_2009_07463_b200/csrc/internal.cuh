@@ -56,6 +56,7 @@ struct DevLayout {
   DevBuf<uint32_t> ccol;   // ecore
   DevBuf<uint32_t> cfirst; // nc: first (highest-degree) core neighbour or kNone32
   DevBuf<uint32_t> csecond; // nc: second core neighbour | bit 31 if it ends the row, or kNone32
+  DevBuf<uint2> cthird;     // nc: {third, fourth} core neighbours, same flags
   DevBuf<uint2> cmeta;     // nc: {core degree, full degree} — one load per claim
   // connected components of the core graph: per core vertex, the size of its
   // component (host copy; a traversal ends once the start's component is

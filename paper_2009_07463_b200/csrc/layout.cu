@@ -410,11 +410,15 @@ __global__ void key_cols_kernel(const uint64_t* keys, uint64_t count, uint64_t m
 }
 
 __global__ void first_nbr_kernel(const uint64_t* crow, const uint32_t* ccol, const uint32_t* degn,
-                                 uint64_t nc, uint32_t* first, uint32_t* second, uint2* meta) {
+                                 uint64_t nc, uint32_t* first, uint32_t* second, uint2* third,
+                                 uint2* meta) {
   GRID_LOOP(i, nc) {
     const uint64_t d = crow[i + 1] - crow[i];
     first[i] = d ? ccol[crow[i]] : kNone32;
     second[i] = d >= 2 ? ccol[crow[i] + 1] | (d == 2 ? 0x80000000u : 0u) : kNone32;
+    // third and fourth neighbours, bit 31 on the row's last one (kNone32: none)
+    third[i] = make_uint2(d >= 3 ? ccol[crow[i] + 2] | (d == 3 ? 0x80000000u : 0u) : kNone32,
+                          d >= 4 ? ccol[crow[i] + 3] | (d == 4 ? 0x80000000u : 0u) : kNone32);
     meta[i] = make_uint2(static_cast<uint32_t>(crow[i + 1] - crow[i]), degn[i]);
   }
 }
@@ -728,6 +732,7 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
   L.cfirst.alloc((nc + 31) / 32 * 32 + 32);
   ETB_CUDA(cudaMemsetAsync(L.cfirst.get(), 0xFF, L.cfirst.bytes(), s));
   L.csecond.alloc(nc ? nc : 1);
+  L.cthird.alloc(nc ? nc : 1);
   // (csecond keeps a flag in bit 31 of a core id)
   if (nc >= (uint64_t{1} << 31)) throw std::runtime_error("relayout_csr: core of 2^31 vertices or more");
   L.cmeta.alloc(nc ? nc : 1);
@@ -770,7 +775,7 @@ void build_layout(const DevGraph& g, const uint8_t* type, int64_t mh, DevLayout&
   if (nc) {
     first_nbr_kernel<<<grid_for(nc, 256), 256, 0, s>>>(L.crow.get(), L.ccol.get(), L.degn.get(),
                                                        nc, L.cfirst.get(), L.csecond.get(),
-                                                       L.cmeta.get());
+                                                       L.cthird.get(), L.cmeta.get());
     ETB_LAUNCH_CHECK();
   }
   core_components(L, s);
