@@ -2102,6 +2102,28 @@ int block_for(uint64_t nc) {
   return nc < (uint64_t{1} << 23) ? kSmallBlock : 1024;
 }
 
+// Persisting L2 access-policy window over [base, base + bytes) on stream s
+// (see bfs_state_init); false when off (ETB_L2_PERSIST=0) or too large.
+bool set_l2_window(cudaStream_t s, void* base, size_t bytes) {
+  int dev = 0, maxp = 0;
+  ETB_CUDA(cudaGetDevice(&dev));
+  ETB_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  const char* pe = getenv("ETB_L2_PERSIST");
+  if ((pe && atoi(pe) <= 0) || bytes > static_cast<size_t>(maxp) / 2) return false;
+  // the carve-out is per device: never shrink it under another layout's window
+  size_t cur = 0;
+  ETB_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  if (cur < bytes) ETB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+  cudaStreamAttrValue a = {};
+  a.accessPolicyWindow.base_ptr = base;
+  a.accessPolicyWindow.num_bytes = bytes;
+  a.accessPolicyWindow.hitRatio = 1.0f;
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  ETB_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a));
+  return true;
+}
+
 void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   const uint64_t n = L.n;
   S.n = n;
@@ -2158,24 +2180,7 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   // included — etb_time_roots demotes them before its L2 flush; s22: +-0).
   // Only when the whole state fits half the carve-out: a window larger than
   // the carve-out thrashed at scale 28 (2x slower per root).
-  int maxp = 0;
-  ETB_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
-  const char* pe = getenv("ETB_L2_PERSIST");
-  if ((!pe || atoi(pe) > 0) && S.bits.bytes() <= static_cast<size_t>(maxp) / 2) {
-    const size_t want = S.bits.bytes();
-    // the carve-out is per device: never shrink it under another layout's window
-    size_t cur = 0;
-    ETB_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-    if (cur < want) ETB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-    cudaStreamAttrValue a = {};
-    a.accessPolicyWindow.base_ptr = S.bits.get();
-    a.accessPolicyWindow.num_bytes = want;
-    a.accessPolicyWindow.hitRatio = 1.0f;
-    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    ETB_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a));
-    S.l2_window = true;
-  }
+  S.l2_window = set_l2_window(s, S.bits.get(), S.bits.bytes());
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 

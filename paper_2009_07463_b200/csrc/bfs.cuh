@@ -119,6 +119,8 @@ struct BfsState {
 };
 
 void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s);
+// persisting L2 window over one allocation on a stream (false: off / too large)
+bool set_l2_window(cudaStream_t s, void* base, size_t bytes);
 void empty_launch(const BfsState& S, cudaStream_t s);  // launch-cost floor (diagnostics)
 void bfs_launch(const BfsParams& p, BfsState& S, cudaStream_t s);
 // -DETB_MISS_CYCLES diagnostics: bottom-up step / miss-resolution warp cycles per depth

@@ -77,10 +77,12 @@ void part_build(const DevLayout& L, PartState& P, uint32_t nparts, uint32_t firs
     d.zlo = d.zhi = static_cast<uint32_t>(L.n);
   }
   P.h_parts[nparts - 1].zlo = static_cast<uint32_t>(nc + nt);
-  P.visited.alloc(local * words);
   P.qv.alloc(local * (nc + 1));
   P.qp.alloc(local * (nc + 1));
-  P.xbytes = ((3 * words * 4 + 255) / 256) * 256 + (kCtrWords + 32) * 8;
+  // per local partition: fb0 | fb1 | fb2 | visited replica | counters — the
+  // frontier replicas and counters are what peers write (the IPC export); the
+  // whole state sits under the stream's persisting L2 window
+  P.xbytes = ((4 * words * 4 + 255) / 256) * 256 + (kCtrWords + 32) * 8;
   P.xblock.alloc(local * P.xbytes);
   ETB_CUDA(cudaMemsetAsync(P.xblock.get(), 0, local * P.xbytes, s));
   P.bar.alloc(local);
@@ -96,10 +98,10 @@ void part_build(const DevLayout& L, PartState& P, uint32_t nparts, uint32_t firs
     d.fb0 = reinterpret_cast<uint32_t*>(xb);
     d.fb1 = d.fb0 + words;
     d.fb2 = d.fb1 + words;
-    d.ctr = reinterpret_cast<unsigned long long*>(xb + ((3 * words * 4 + 255) / 256) * 256);
+    d.ctr = reinterpret_cast<unsigned long long*>(xb + ((4 * words * 4 + 255) / 256) * 256);
     d.arrive = d.ctr + kCtrWords;
     d.bar = P.bar.get() + j;
-    d.visited = P.visited.get() + j * words;
+    d.visited = d.fb2 + words;
     d.qv = P.qv.get() + j * (nc + 1);
     d.qp = P.qp.get() + j * (nc + 1);
     // the top-down CSR of this partition's owned neighbours
@@ -149,6 +151,7 @@ void part_build(const DevLayout& L, PartState& P, uint32_t nparts, uint32_t firs
   int grid = sms;  // one CTA per SM, as the single-partition kernel
   grid -= grid % static_cast<int>(local);  // equal block groups
   P.grid = grid;
+  set_l2_window(s, P.xblock.get(), local * P.xbytes);
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 
