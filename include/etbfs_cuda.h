@@ -181,7 +181,11 @@ void etb_layout_free(etb_layout* L);
 int etb_bfs_device(etb_layout* L, uint64_t start, const etb_bfs_options* opts,
                    etb_bfs_stats* stats);
 /* et_bfs with host outputs (the reference-facing call): depth (n i32, -1 unreached)
- * and/or parent (n u64, ETB_NO_VERTEX unreached), relaid ids. */
+ * and/or parent (n u64, ETB_NO_VERTEX unreached), relaid ids. Every host-output
+ * call copies only the live prefix [0, core + tree) of the relaid id space over
+ * PCIe; the isolated vertices that close it are unreached in every result (but
+ * for an isolated start), so their range of the host arrays is filled by host
+ * threads while the DMA runs. The arrays come back complete either way. */
 int etb_bfs(etb_layout* L, uint64_t start, const etb_bfs_options* opts, int32_t* depth_out,
             uint64_t* parent_out, etb_bfs_stats* stats);
 /* et_bfs with compact host outputs: parent (n u32, UINT32_MAX unreached) and/or

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <unistd.h>
@@ -234,25 +235,71 @@ __global__ void split_kernel(const uint2* dp, uint64_t n, int32_t* depth, uint32
   }
 }
 
+// 0xFF fill of a host range by up to 8 threads (the calling one included): the
+// unreached marker of every output type is all ones (-1 / UINT32_MAX /
+// ETB_NO_VERTEX). One thread fills ~10-15 GB/s, a device->host DMA moves 55.
+void host_fill_ones(void* dst, size_t bytes) {
+  constexpr size_t kPerThread = size_t{4} << 20;
+  unsigned hw = std::thread::hardware_concurrency();
+  size_t want = std::min<size_t>({size_t{8}, hw ? hw : 1, bytes / kPerThread});
+  if (want <= 1) {
+    std::memset(dst, 0xFF, bytes);
+    return;
+  }
+  const size_t part = ((bytes / want) + 63) & ~size_t{63};
+  std::vector<std::thread> th;
+  th.reserve(want - 1);
+  char* p = static_cast<char*>(dst);
+  for (size_t t = 1; t < want; ++t) {
+    const size_t lo = std::min(bytes, t * part), hi = std::min(bytes, (t + 1) * part);
+    if (hi > lo) th.emplace_back([p, lo, hi] { std::memset(p + lo, 0xFF, hi - lo); });
+  }
+  std::memset(p, 0xFF, std::min(bytes, part));
+  for (auto& t : th) t.join();
+}
+
 // Split the last result on the device and copy the requested parts to host.
+// Only the live prefix [0, nc + nt) of the relaid id space crosses PCIe: the
+// isolated vertices that close it (layout.cu) are unreached in every result
+// unless one of them is the start, so the host fills their range itself while
+// the DMA of the prefix runs (half of n at Graph500 scales 26-28).
 void download_result(etb_layout* h, int32_t* depth, uint32_t* parent, uint64_t* parent64) {
   const uint64_t n = h->L.n;
   if (!n || (!depth && !parent && !parent64)) return;
   auto& S = h->S;
   cudaStream_t s = h->stream;
-  // staging buffers persist with the layout: no allocation (and no
-  // synchronising free) inside the reference-facing call
-  if (depth && S.tmp_depth.size() < n) S.tmp_depth.alloc(n);
-  if (parent && S.tmp_parent.size() < n) S.tmp_parent.alloc(n);
-  if (parent64 && S.tmp_parent64.size() < n) S.tmp_parent64.alloc(n);
-  split_kernel<<<etb::grid_for(n, 256), 256, 0, s>>>(S.dp.get(), n, depth ? S.tmp_depth.get() : nullptr,
-                                                     parent ? S.tmp_parent.get() : nullptr,
-                                                     parent64 ? S.tmp_parent64.get() : nullptr);
-  ETB_LAUNCH_CHECK();
-  if (depth) ETB_CUDA(cudaMemcpyAsync(depth, S.tmp_depth.get(), n * 4, cudaMemcpyDeviceToHost, s));
-  if (parent) ETB_CUDA(cudaMemcpyAsync(parent, S.tmp_parent.get(), n * 4, cudaMemcpyDeviceToHost, s));
-  if (parent64)
-    ETB_CUDA(cudaMemcpyAsync(parent64, S.tmp_parent64.get(), n * 8, cudaMemcpyDeviceToHost, s));
+  // a partitioned layout's result may have been assembled by the caller
+  // through etb_result_device_ptr: copy it whole
+  const uint64_t live = h->P ? n : std::min<uint64_t>(n, h->L.nc + h->L.nt);
+  if (live) {
+    // staging buffers persist with the layout: no allocation (and no
+    // synchronising free) inside the reference-facing call
+    if (depth && S.tmp_depth.size() < live) S.tmp_depth.alloc(live);
+    if (parent && S.tmp_parent.size() < live) S.tmp_parent.alloc(live);
+    if (parent64 && S.tmp_parent64.size() < live) S.tmp_parent64.alloc(live);
+    split_kernel<<<etb::grid_for(live, 256), 256, 0, s>>>(
+        S.dp.get(), live, depth ? S.tmp_depth.get() : nullptr,
+        parent ? S.tmp_parent.get() : nullptr, parent64 ? S.tmp_parent64.get() : nullptr);
+    ETB_LAUNCH_CHECK();
+    if (depth)
+      ETB_CUDA(cudaMemcpyAsync(depth, S.tmp_depth.get(), live * 4, cudaMemcpyDeviceToHost, s));
+    if (parent)
+      ETB_CUDA(cudaMemcpyAsync(parent, S.tmp_parent.get(), live * 4, cudaMemcpyDeviceToHost, s));
+    if (parent64)
+      ETB_CUDA(cudaMemcpyAsync(parent64, S.tmp_parent64.get(), live * 8, cudaMemcpyDeviceToHost, s));
+  }
+  if (live < n) {
+    const uint64_t tail = n - live;
+    if (depth) host_fill_ones(depth + live, tail * 4);
+    if (parent) host_fill_ones(parent + live, tail * 4);
+    if (parent64) host_fill_ones(parent64 + live, tail * 8);
+    const uint64_t st = S.last_start;  // an isolated start is its own depth-0 root
+    if (st >= live && st < n) {
+      if (depth) depth[st] = 0;
+      if (parent) parent[st] = static_cast<uint32_t>(st);
+      if (parent64) parent64[st] = st;
+    }
+  }
   ETB_CUDA(cudaStreamSynchronize(s));
 }
 
