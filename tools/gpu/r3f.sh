@@ -1,0 +1,5 @@
+mkdir -p gpurun_out/r3f
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r3f/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/r3f/pytest_gpu.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r3f/smoke.log 2>&1; echo rc=$? >> gpurun_out/r3f/smoke.log
+timeout 1200 python bench.py > gpurun_out/r3f/bench.json 2> gpurun_out/r3f/bench.err; echo rc=$? >> gpurun_out/r3f/bench.err
+echo done > gpurun_out/r3f/done.txt
