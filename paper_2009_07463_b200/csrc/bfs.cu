@@ -70,6 +70,13 @@ constexpr double kSmallMode3Default = ETB_SMALL_MODE3_DEFAULT;
 // BfsParams::td_as_bu default (env ETB_TD_AS_BU overrides; 0 = off): s26 +6%
 // harmonic-mean GTEPS (slowest roots 0.80 -> 0.62-0.68 ms), s22 neutral
 constexpr double kTdAsBuDefault = 4.0;  // measured best at s26 (3..5 equal, 6 and up: no level)
+// BfsParams::split_ratio / split_bound = nc / div defaults (env ETB_SPLIT_RATIO,
+// ETB_SPLIT_DIV override)
+#ifndef ETB_SPLIT_RATIO_DEFAULT
+#define ETB_SPLIT_RATIO_DEFAULT 0.0
+#endif
+constexpr double kSplitRatioDefault = ETB_SPLIT_RATIO_DEFAULT;
+constexpr double kSplitDivDefault = 1024.0;
 
 // The step functions below are templates on their parameter view P: BfsParams
 // (one partition: the whole core, the whole grid) or PartView (one partition of
@@ -96,7 +103,8 @@ struct Smem {
   unsigned long long red[2][kMaxWarps];
   unsigned long long tot[4];  // level totals read once per CTA after the barrier
   unsigned int bu_next;       // bottom-up: the CTA's next run (reset at every grid barrier)
-  unsigned int pad[3];
+  unsigned int bu_bound;      // bounded bottom-up steps: neighbours >= this end a row
+  unsigned int pad[2];
 };
 __device__ __forceinline__ Smem& smem_view() {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -513,17 +521,34 @@ __device__ __forceinline__ void bu_append(const uint32_t (&v)[K], const uint32_t
 // its own early exit: a lane resolves two deferred vertices per pass (half
 // the passes: s22 -1.3 us, s26 -14 us per root; a generic K-row version and
 // four rows spilled).
-template <class P>
+// kBound: neighbours >= bound end the row (ta / tb report it).
+template <bool kBound = false, class P>
 __device__ __forceinline__ void scan_rows2(const P& p, const uint32_t* fcur, uint64_t ea,
                                            uint64_t enda, uint64_t eb, uint64_t endb,
-                                           uint32_t& pa, uint32_t& pb, bool& ha, bool& hb) {
+                                           uint32_t& pa, uint32_t& pb, bool& ha, bool& hb,
+                                           uint32_t bound = kNone32, bool* ta = nullptr,
+                                           bool* tb = nullptr) {
   ha = hb = false;
   while (ea < enda || eb < endb) {
     ETB_DCHECK(enda <= p.crow[p.nc] && endb <= p.crow[p.nc]);
-    const uint32_t x0 = ea < enda ? p.ccol[ea] : kNone32;
-    const uint32_t x1 = ea + 1 < enda ? p.ccol[ea + 1] : kNone32;
-    const uint32_t y0 = eb < endb ? p.ccol[eb] : kNone32;
-    const uint32_t y1 = eb + 1 < endb ? p.ccol[eb + 1] : kNone32;
+    uint32_t x0 = ea < enda ? p.ccol[ea] : kNone32;
+    uint32_t x1 = ea + 1 < enda ? p.ccol[ea + 1] : kNone32;
+    uint32_t y0 = eb < endb ? p.ccol[eb] : kNone32;
+    uint32_t y1 = eb + 1 < endb ? p.ccol[eb + 1] : kNone32;
+    if (kBound) {  // rows ascend: the first neighbour past the bound ends the scan
+      if (ea < enda && (x0 >= bound || x1 >= bound)) {
+        if (x0 >= bound) x0 = kNone32;
+        x1 = kNone32;
+        *ta = true;
+        enda = ea + 2;  // this pair is the row's last
+      }
+      if (eb < endb && (y0 >= bound || y1 >= bound)) {
+        if (y0 >= bound) y0 = kNone32;
+        y1 = kNone32;
+        *tb = true;
+        endb = eb + 2;
+      }
+    }
     const bool bx0 = x0 != kNone32 && test_bit(fcur, x0);
     const bool bx1 = x1 != kNone32 && test_bit(fcur, x1);
     const bool by0 = y0 != kNone32 && test_bit(fcur, y0);
@@ -574,7 +599,8 @@ __device__ unsigned long long g_diag[kDiag];
 #endif
 
 // Row scans of deferred vertices whose first `skip` neighbours missed.
-template <class P>
+// (kBound: a row ends at its first neighbour >= the CTA's bu_bound.)
+template <bool kBound = false, class P>
 __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
                              uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
                              unsigned long long& claims_acc, uint32_t* qv_out,
@@ -582,6 +608,7 @@ __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
                              unsigned long long* scout) {
   const unsigned lane = threadIdx.x & 31;
   unsigned long long sc = 0;  // Σ full degree of the claims (when scout is wanted)
+  [[maybe_unused]] const uint32_t bound = kBound ? smem_view().bu_bound : kNone32;
   __syncwarp();
   ETB_DIAG_COUNT(160 + (dnext & 31), nmiss);
   uint32_t nlong = 0;
@@ -595,10 +622,11 @@ __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
     const uint64_t la = min(rea, rba + skip + kLaneFirst), lb = min(reb, rbb + skip + kLaneFirst);
     uint32_t pa = 0, pb = 0;
     bool ha, hb;
-    scan_rows2(p, fcur, rba + skip, va != kNone32 ? la : 0, rbb + skip, vb != kNone32 ? lb : 0,
-               pa, pb, ha, hb);
-    const bool lnga = va != kNone32 && !ha && la < rea;
-    const bool lngb = vb != kNone32 && !hb && lb < reb;
+    bool ta = false, tb = false;
+    scan_rows2<kBound>(p, fcur, rba + skip, va != kNone32 ? la : 0, rbb + skip,
+                       vb != kNone32 ? lb : 0, pa, pb, ha, hb, bound, &ta, &tb);
+    const bool lnga = va != kNone32 && !ha && !ta && la < rea;
+    const bool lngb = vb != kNone32 && !hb && !tb && lb < reb;
     if (ha) {
       p.dp[va] = make_uint2(static_cast<uint32_t>(dnext), pa);
       atomicOr(&p.visited[va >> 5], 1u << (va & 31));
@@ -638,12 +666,15 @@ __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
     for (uint64_t e0 = rb; e0 < re; e0 += 32) {
       ETB_DIAG_COUNT(224 + (dnext & 31), 1);
       const uint64_t e = e0 + lane;
-      const uint32_t x = e < re ? p.ccol[e] : kNone32;
+      uint32_t x = e < re ? p.ccol[e] : kNone32;
+      const unsigned over = kBound ? __ballot_sync(0xffffffffu, e < re && x >= bound) : 0u;
+      if (kBound && x >= bound) x = kNone32;
       const unsigned m = __ballot_sync(0xffffffffu, x != kNone32 && test_bit(fcur, x));
       if (m) {
         par = __shfl_sync(0xffffffffu, x, __ffs(m) - 1);
         break;
       }
+      if (over) break;
     }
     if (lane == 0 && par != kNone32) {
       p.dp[v] = make_uint2(static_cast<uint32_t>(dnext), par);
@@ -671,7 +702,7 @@ __device__ void resolve_rows(const P& p, const uint32_t* fcur, uint32_t* fnext,
 // a load-balanced warp scan of the rows, 128 edges per round trip: 1.7x slower
 // for all misses, 1.14x for the rows past the second neighbour — its window
 // bookkeeping is ~50 shuffles per round and a round covers 32 rows, not 64.)
-template <class P>
+template <bool kBound = false, class P>
 __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext,
                                uint32_t* mbuf, uint32_t nmiss, int32_t dnext,
                                unsigned long long& claims_acc, uint32_t* qv_out,
@@ -679,6 +710,7 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
                                unsigned long long* scout) {
   const unsigned lane = threadIdx.x & 31, lt = (1u << lane) - 1;
   unsigned long long sc2 = 0;
+  [[maybe_unused]] const uint32_t bound = kBound ? smem_view().bu_bound : kNone32;
   __syncwarp();
   ETB_DIAG_BEGIN();
   ETB_DIAG_COUNT(128 + (dnext & 31), nmiss);
@@ -692,6 +724,11 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) sc[k] = v[k] != kNone32 ? p.csecond[v[k]] : kNone32;
+    if (kBound) {  // a second neighbour past the bound: the row has ended
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (sc[k] != kNone32 && (sc[k] & kSecondMask) >= bound) sc[k] = kNone32;
+    }
     bool h[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) h[k] = sc[k] != kNone32 && test_bit(fcur, sc[k] & kSecondMask);
@@ -737,6 +774,13 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) t3[k] = v[k] != kNone32 ? p.cthird[v[k]] : make_uint2(kNone32, kNone32);
+    if (kBound) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (t3[k].x != kNone32 && (t3[k].x & kSecondMask) >= bound) t3[k] = make_uint2(kNone32, kNone32);
+        else if (t3[k].y != kNone32 && (t3[k].y & kSecondMask) >= bound) t3[k].y = kNone32;
+      }
+    }
     bool h3[4], h4[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -772,10 +816,12 @@ __device__ void resolve_misses(const P& p, const uint32_t* fcur, uint32_t* fnext
     __syncwarp();
   }
   if (nl2)
-    resolve_rows(p, fcur, fnext, mbuf, nl2, dnext, claims_acc, qv_out, qp_out, lslot, 4, scout);
+    resolve_rows<kBound>(p, fcur, fnext, mbuf, nl2, dnext, claims_acc, qv_out, qp_out, lslot, 4,
+                         scout);
 #else
   if (nlong)
-    resolve_rows(p, fcur, fnext, mbuf, nlong, dnext, claims_acc, qv_out, qp_out, lslot, 2, scout);
+    resolve_rows<kBound>(p, fcur, fnext, mbuf, nlong, dnext, claims_acc, qv_out, qp_out, lslot, 2,
+                         scout);
 #endif
   if (scout) *scout += sc2;
   ETB_DIAG_END(64 + (dnext & 63));
@@ -797,7 +843,7 @@ __device__ __forceinline__ void bu_issue(const BfsParams& p, BuPipe<kU>* pipe, i
   bulk_g2s(pipe->st[sg].vw, reinterpret_cast<const unsigned char*>(p.visited) + vlo, vw_bytes,
            &pipe->bar[sg]);
 }
-template <int kU, class P>
+template <int kU, bool kBound = false, class P>
 __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
                         uint32_t* fnext, int32_t dnext, unsigned long long& claims_acc,
                         uint32_t* qv_out, uint64_t* qp_out, unsigned long long* lslot,
@@ -916,6 +962,12 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       f[k] = ((vis[k] >> lane) & 1u) ? kNone32 : p.cfirst[wrd(k) * 32 + lane];
 #endif
     }
+    if (kBound) {  // no neighbour under the bound: nothing to probe, not a miss
+      const uint32_t bound = smem_view().bu_bound;
+#pragma unroll
+      for (int k = 0; k < kU; ++k)
+        if (f[k] >= bound) f[k] = kNone32;
+    }
     bool hit[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) hit[k] = f[k] != kNone32 && test_bit(fcur, f[k]);
@@ -949,7 +1001,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       bu_append<kU>(av, ad, qv_out, qp_out, lslot);
     }
     if (nmiss > min(kMissCap - 32 * kU, kMissFlush)) {
-      resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
+      resolve_misses<kBound>(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
       nmiss = 0;
     }
   }
@@ -960,7 +1012,7 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
       mbar_inval(&pipe->bar[1]);
     }
   }
-  if (nmiss) resolve_misses(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
+  if (nmiss) resolve_misses<kBound>(p, fcur, fnext, mbuf, nmiss, dnext, claims_acc, qv_out, qp_out, lslot, scout);
   if (scout) *scout += scm;
   ETB_DIAG_END(dnext & 63);
 }
@@ -1313,6 +1365,58 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
           bu_step<kLarge ? kBuU : kBuUSmall>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext,
                                              claims_acc, qv_in, qp_in,
                                              bu_list ? &slot[0] : nullptr);
+      } else if (kLarge && p.split_ratio > 0.0 && !p.top_down_only && L > 0 &&
+                 !((double)scout < p.emit_limit) &&
+                 (double)ne >= p.split_ratio * (double)(p.nc - reached)) {
+        // A big list-less top-down level executed split: the frontier's hubs
+        // (ids < split_bound, most of its edges) bottom-up over the unvisited
+        // core with every row scan ended at the bound — the rows of the
+        // vertices with no hub neighbour in the frontier end within their
+        // first few entries instead of being scanned whole — and the other
+        // frontier vertices top-down from a filtered list. A vertex is claimed
+        // iff it has a frontier neighbour on either side: the reference's
+        // claims; claims and scout are counted from the new frontier bitmap.
+        etc -= (double)scout;
+        list_valid = false;
+        defer_scout = true;
+        if (threadIdx.x == 0) sm.bu_bound = p.split_bound;
+        {  // the frontier vertices past the bound, appended to the free list
+          const unsigned lane = threadIdx.x & 31, lt = (1u << lane) - 1;
+          const uint64_t gwp = tid >> 5, nwp = nthreads >> 5;
+          for (uint64_t i0 = gwp * 32; i0 < nq; i0 += nwp * 32) {
+            const uint64_t i = i0 + lane;
+            uint32_t v = 0, d = 0;
+            if (i < nq) {
+              v = qv_in[i];
+              if (v >= p.split_bound)
+                d = static_cast<uint32_t>((i + 1 < nq ? qp_in[i + 1] : ne) - qp_in[i]);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, d != 0);
+            if (!m) continue;
+            const uint32_t din = warp_incl_scan(d);
+            const uint32_t dtot = __shfl_sync(0xffffffffu, din, 31);
+            unsigned long long old = 0;
+            if (lane == 0)
+              old = atomicAdd(&slot[0],
+                              (static_cast<unsigned long long>(__popc(m)) << kItemShift) | dtot);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (d != 0) {
+              const uint64_t pos = (old >> kItemShift) + __popc(m & lt);
+              qv_out[pos] = v;
+              qp_out[pos] = (old & kItemMask) + din - d;
+            }
+          }
+        }
+        __syncthreads();  // bu_bound
+        bu_step<kBuU, true>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in,
+                            qp_in, nullptr);
+        grid_sync_add(p.bar, sm, 0, nullptr, 0, nullptr, slot, 1);
+        const unsigned long long tail = sm.tot[0];
+        td_step<3, kLarge>(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_out,
+                           qp_out, tail >> kItemShift, tail & kItemMask, qv_in, qp_in, fnext, slot,
+                           dnext, scout_acc, claims_acc, kNone32);
+        claims_acc = 0;
+        scout_acc = 0;
       } else if (p.td_as_bu > 0.0 && !p.top_down_only && !(L == 1 && list_from_prologue) && L > 0 &&
                  (double)ne > p.td_as_bu * (double)(p.nc - reached)) {
         // a top-down level (α/β state advanced as the reference's) executed as
@@ -2227,6 +2331,11 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   p.small_mode3_edges = kSmallMode3Default;
   if (const char* e = getenv("ETB_SMALL_MODE3")) p.small_mode3_edges = atof(e);
   if (const char* e = getenv("ETB_TD_AS_BU")) p.td_as_bu = atof(e);
+  p.split_ratio = kSplitRatioDefault;
+  double split_div = kSplitDivDefault;
+  if (const char* e = getenv("ETB_SPLIT_RATIO")) p.split_ratio = atof(e);
+  if (const char* e = getenv("ETB_SPLIT_DIV")) split_div = std::max(1.0, atof(e));
+  p.split_bound = static_cast<uint32_t>(std::max(32.0, static_cast<double>(L.nc) / split_div));
   p.trace = nullptr;
   p.level_claims = nullptr;
   p.bstamp = nullptr;

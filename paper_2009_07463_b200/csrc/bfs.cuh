@@ -68,6 +68,13 @@ struct BfsParams {
   // neighbour — is the same, so depths, claims, scout and the α/β sequence are
   // the reference's; only the GPU cost differs.
   double td_as_bu;
+  // Large-core kernel: a list-less top-down level whose frontier edges reach
+  // split_ratio x the unvisited core vertices (0 = never) is executed split:
+  // the frontier's hubs (relaid ids < split_bound) bottom-up, every row scan
+  // ending at the first neighbour >= split_bound, the other frontier vertices
+  // top-down from a filtered list. Same claimed set, depths and α/β sequence.
+  double split_ratio;
+  uint32_t split_bound;
   // small-core kernel: list-less top-down levels with at least this many
   // frontier edges claim atomic-free and count afterwards (as the large-core
   // kernel's); smaller ones claim with returning atomics
