@@ -73,10 +73,10 @@ constexpr double kTdAsBuDefault = 4.0;  // measured best at s26 (3..5 equal, 6 a
 // BfsParams::split_ratio / split_bound = nc / div defaults (env ETB_SPLIT_RATIO,
 // ETB_SPLIT_DIV override)
 #ifndef ETB_SPLIT_RATIO_DEFAULT
-#define ETB_SPLIT_RATIO_DEFAULT 0.0
+#define ETB_SPLIT_RATIO_DEFAULT 2.0  // s26 +3.8%, s28 +7.7% (1 / 1.5 / 2.5 / 3: +2.2 / 2.8 / 2.9 / 2.4% at s26)
 #endif
 constexpr double kSplitRatioDefault = ETB_SPLIT_RATIO_DEFAULT;
-constexpr double kSplitDivDefault = 1024.0;
+constexpr double kSplitDivDefault = 1024.0;  // (s26, ratio 2: 512 -0.6%, 2048 -1.1%; ratio 1.5: 256 -0.6%, 4096 -1.2%)
 
 // The step functions below are templates on their parameter view P: BfsParams
 // (one partition: the whole core, the whole grid) or PartView (one partition of
@@ -150,7 +150,8 @@ struct BuPipe {
 static_assert(sizeof(BuPipe<8>) % 16 == 0 && sizeof(BuPipe<7>) % 16 == 0, "16-byte stages");
 
 // Phase timestamps for stats (block 0 / thread 0): [256] entry, [257] after
-// init, [258 + L] after level L, [511] end of the tree replay.
+// init, [258 + L] after level L, [320 + L] end of a split level's bottom-up
+// half, [384 + L] end of a bitmap -> list conversion, [511] end of the tree replay.
 __device__ __forceinline__ void stamp(const BfsParams& p, uint32_t slot) {
   if (p.level_claims && blockIdx.x == 0 && threadIdx.x == 0 && slot < 512)
     p.level_claims[slot] = gtimer();
@@ -1411,7 +1412,9 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
         bu_step<kBuU, true>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in,
                             qp_in, nullptr);
         grid_sync_add(p.bar, sm, 0, nullptr, 0, nullptr, slot, 1);
+        stamp(p, 320 + L);  // diagnostics: end of the split level's bottom-up half
         const unsigned long long tail = sm.tot[0];
+        if (p.level_claims && tid == 0 && L < 64) p.level_claims[448 + L] = tail & kItemMask;
         td_step<3, kLarge>(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_out,
                            qp_out, tail >> kItemShift, tail & kItemMask, qv_in, qp_in, fnext, slot,
                            dnext, scout_acc, claims_acc, kNone32);

@@ -58,10 +58,15 @@ def main():
         td_edges = [int(ph[192 + L]) if r.stats.direction_trace[L:L + 1] == "t" else None
                     for L in range(len(r.stats.direction_trace))]
         dur = [round((ns[j + 1] - ns[j]) / 1e3, 1) for j in range(len(ns) - 1)]
+        # split levels: time of the bottom-up half (stamp 320 + L) since the level's start
+        split_bu = {L: round((int(ph[64 + L]) - int(ph[0]) - ns[L]) / 1e3, 1)
+                    for L in range(min(len(ns) - 1, 60))
+                    if ph[64 + L] and ns[L] < int(ph[64 + L]) - int(ph[0]) <= ns[L + 1]}  # (not a stale stamp)
         rec = {"root": int(roots[i]), "start": int(s), "type": int(cg.vertex_type[int(s)]),
                "kernel_us": round(float(kms[i]) * 1e3, 1), "call_us": round(float(ms[i]) * 1e3, 1), "device_us": round(r.stats.total_ns / 1e3, 1),
                "init_us": round(ns[0] / 1e3, 1) if ns else None, "trace": r.stats.direction_trace,
-               "claims": r.stats.level_claims, "level_us": dur, "td_edges": td_edges}
+               "claims": r.stats.level_claims, "level_us": dur, "td_edges": td_edges,
+               "split_bu_us": split_bu}
         if args.diag:  # mean per warp, us at the SM clock (--clock-ghz)
             nw = 148 * (1024 if cg.core_vertex_count >= (1 << 23) else 640) // 32
             cyc = lambda c: round(float(c) / nw / (args.clock_ghz * 1e3), 1)
