@@ -57,3 +57,34 @@ def test_extreme_shapes(large_kernel, name, n, pairs):
         check_root(cg, oc, root)
         E.bfs_device(cg, int(cg.old2new[root]))
         assert E.result_validate(cg, int(cg.old2new[root]))["passed"], (name, root)
+
+
+@pytest.mark.parametrize("ratio,div", [("0.05", "4"), ("0.05", "64"), ("0.5", "1000000"), ("2", "1024"),
+                                       ("0", "1024")])
+def test_split_levels_s16(large_kernel, monkeypatch, kron16, ratio, div):
+    """Split top-down levels (frontier hubs bottom-up with rows ended at an id
+    bound, the other frontier vertices top-down from a filtered list) forced onto
+    nearly every list-less level (a tiny ratio) with bounds from a quarter of the
+    core down to the 32-vertex floor, at the default and switched off: depths
+    against the oracle, parents valid, the reference's direction traces and
+    traversed-edge counts."""
+    monkeypatch.setenv("ETB_SPLIT_RATIO", ratio)
+    monkeypatch.setenv("ETB_SPLIT_DIV", div)
+    k = kron16
+    csr = eb.generate_graph(scale=16, edgefactor=16, seed=1)
+    ocsr = O.OracleCsr(1 << 16, O.oracle_generate(16, 16, 1))
+    for mh in (-1, 0):
+        cg = eb.relayout_csr(csr, mh=mh)
+        traces = k["layout"][str(mh)]["traces"]
+        for i, root in enumerate(k["roots"][:32]):
+            r = check_root(cg, ocsr, int(root))
+            assert r.stats.direction_trace == traces[i], (mh, root, ratio, div)
+            s = int(cg.old2new[int(root)])
+            E.bfs_device(cg, s)
+            assert E.result_validate(cg, s)["passed"], (mh, root)
+            assert E.result_traversed_edges(cg) == k["traversed_edges"][i]
+        # the split path was taken: its bottom-up half leaves a phase stamp
+        ph = np.zeros(256, np.uint64)
+        E._check(E.lib().etb_debug_phase_stamps(cg.handle, ph.ctypes.data))
+        if float(ratio) == 0.05:
+            assert ph[64:128].any(), "no level ran split"
