@@ -2264,6 +2264,7 @@ void bfs_state_init(const DevLayout& L, BfsState& S, cudaStream_t s) {
   ETB_CUDA(cudaMemsetAsync(S.dp.get(), 0xFF, (n ? n : 1) * 8, s));
   S.trace.alloc(256);
   S.level_claims.alloc(512);
+  ETB_CUDA(cudaMemsetAsync(S.level_claims.get(), 0, 512 * 8, s));  // stamps read as "not taken"
   S.nlevels.alloc(1);
   const uint64_t pcap = std::max<uint64_t>(L.max_tree, 1) + 2;
   S.patch.alloc(3 * pcap);

@@ -88,3 +88,5 @@ def test_split_levels_s16(large_kernel, monkeypatch, kron16, ratio, div):
         E._check(E.lib().etb_debug_phase_stamps(cg.handle, ph.ctypes.data))
         if float(ratio) == 0.05:
             assert ph[64:128].any(), "no level ran split"
+        if float(ratio) == 0:
+            assert not ph[64:128].any()
