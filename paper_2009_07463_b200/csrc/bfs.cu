@@ -76,6 +76,12 @@ constexpr double kTdAsBuDefault = 4.0;  // measured best at s26 (3..5 equal, 6 a
 #define ETB_SPLIT_RATIO_DEFAULT 2.0  // s26 +3.8%, s28 +7.7% (1 / 1.5 / 2.5 / 3: +2.2 / 2.8 / 2.9 / 2.4% at s26)
 #endif
 constexpr double kSplitRatioDefault = ETB_SPLIT_RATIO_DEFAULT;
+constexpr uint32_t kSplitAuto = 0xFFFFu;  // split_tdw: chosen per level from the tail's edges
+constexpr unsigned long long kSplitShortTail = 1ull << 25;
+#ifndef ETB_SPLIT_TDW_DEFAULT
+#define ETB_SPLIT_TDW_DEFAULT kSplitAuto
+#endif
+constexpr uint32_t kSplitTdwDefault = ETB_SPLIT_TDW_DEFAULT;
 constexpr double kSplitDivDefault = 1024.0;  // (s26, ratio 2: 512 -0.6%, 2048 -1.1%; ratio 1.5: 256 -0.6%, 4096 -1.2%)
 
 // The step functions below are templates on their parameter view P: BfsParams
@@ -264,10 +270,13 @@ __device__ void td_step(const P& p, uint32_t* cbuf, int32_t* win, const uint32_t
                         const uint64_t* qp, uint64_t nq, uint64_t ne, uint32_t* qv_out,
                         uint64_t* qp_out, uint32_t* fnext, unsigned long long* slot,
                         int32_t dnext, unsigned long long& scout_acc,
-                        unsigned long long& claims_acc, uint32_t root) {
+                        unsigned long long& claims_acc, uint32_t root, unsigned tdw = 0) {
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // tdw != 0: only the CTA's first tdw warps take part (a split level's
+  // top-down half; the others are already in its bottom-up half)
+  if (tdw && wib >= tdw) return;
   const uint64_t gw = (uint64_t)wib * ncta_of(p) + cta_of(p);  // CTA-minor: spread over SMs
-  const uint64_t nw = (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
+  const uint64_t nw = tdw ? (uint64_t)ncta_of(p) * tdw : (uint64_t)(ncta_of(p) * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1;
   const uint64_t nu = (ne + kTdChunk - 1) / kTdChunk;
   for (uint64_t g0 = gw, gn = 1; g0 < nu;) {
@@ -982,8 +991,13 @@ __device__ void bu_step(const P& p, uint32_t* mbuf, const uint32_t* fcur,
         if (scout) scm += p.degn[v];
       }
       if (lane == 0 && m) {
-        p.visited[wk] = vis[k] | m;
-        fnext[wk] = m;
+        if (kBound) {  // the split level's top-down half may be claiming in this word
+          atomicOr(&p.visited[wk], m);
+          atomicOr(&fnext[wk], m);
+        } else {
+          p.visited[wk] = vis[k] | m;
+          fnext[wk] = m;
+        }
         claims_acc += __popc(m);
       }
       const bool miss = f[k] != kNone32 && !hit[k];
@@ -1408,16 +1422,48 @@ __device__ __forceinline__ void et_bfs_body(const BfsParams& p) {
             }
           }
         }
-        __syncthreads();  // bu_bound
-        bu_step<kBuU, true>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc, qv_in,
-                            qp_in, nullptr);
-        grid_sync_add(p.bar, sm, 0, nullptr, 0, nullptr, slot, 1);
-        stamp(p, 320 + L);  // diagnostics: end of the split level's bottom-up half
-        const unsigned long long tail = sm.tot[0];
-        if (p.level_claims && tid == 0 && L < 64) p.level_claims[448 + L] = tail & kItemMask;
-        td_step<3, kLarge>(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_out,
-                           qp_out, tail >> kItemShift, tail & kItemMask, qv_in, qp_in, fnext, slot,
-                           dnext, scout_acc, claims_acc, kNone32);
+        if (p.split_tdw) {
+          // Both halves at once: after the (short) filter pass and its barrier the
+          // CTA's first split_tdw warps run the top-down half, a latency-bound
+          // few chunks per warp, then join the others in the bottom-up half
+          // (its runs are handed out dynamically; its word updates are atomic
+          // in the bounded form, the other half may be claiming in the same word).
+          grid_sync_add(p.bar, sm, 0, nullptr, 0, nullptr, slot, 1);
+          stamp(p, 320 + L);  // diagnostics: a split level (here: its filter pass's end)
+          const unsigned long long tail = sm.tot[0];
+          if (p.level_claims && tid == 0 && L < 64) p.level_claims[448 + L] = tail & kItemMask;
+          // kSplitAuto: a short top-down half (a few latency-bound chunks per
+          // warp) runs beside the bottom-up half on half the warps; a long one
+          // follows it, so that its probes find the hubs' claims already made
+          // (s26, tails of 6-22M edges: 16 warps +1.8%, after +0.6%; s28, 4x
+          // the tails: 16 warps -1.3%, after +0.5%)
+          const uint32_t tdw = p.split_tdw != kSplitAuto ? p.split_tdw
+                               : (tail & kItemMask) < kSplitShortTail ? 16u : 64u;
+          if (tdw <= 32)
+            td_step<3, kLarge>(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_out,
+                               qp_out, tail >> kItemShift, tail & kItemMask, qv_in, qp_in, fnext,
+                               slot, dnext, scout_acc, claims_acc, kNone32, tdw);
+          bu_step<kBuU, true>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc,
+                              qv_in, qp_in, nullptr);
+          // split_tdw > 32: every warp goes from the CTA's last bottom-up run
+          // straight to the top-down chunks (no barrier between the halves; the
+          // top-down probes then find most targets already claimed)
+          if (tdw > 32)
+            td_step<3, kLarge>(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_out,
+                               qp_out, tail >> kItemShift, tail & kItemMask, qv_in, qp_in, fnext,
+                               slot, dnext, scout_acc, claims_acc, kNone32);
+        } else {
+          __syncthreads();  // bu_bound
+          bu_step<kBuU, true>(p, sm.w[threadIdx.x >> 5].cbuf, fcur, fnext, dnext, claims_acc,
+                              qv_in, qp_in, nullptr);
+          grid_sync_add(p.bar, sm, 0, nullptr, 0, nullptr, slot, 1);
+          stamp(p, 320 + L);  // diagnostics: end of the split level's bottom-up half
+          const unsigned long long tail = sm.tot[0];
+          if (p.level_claims && tid == 0 && L < 64) p.level_claims[448 + L] = tail & kItemMask;
+          td_step<3, kLarge>(p, sm.w[threadIdx.x >> 5].cbuf, sm.w[threadIdx.x >> 5].win, qv_out,
+                             qp_out, tail >> kItemShift, tail & kItemMask, qv_in, qp_in, fnext,
+                             slot, dnext, scout_acc, claims_acc, kNone32);
+        }
         claims_acc = 0;
         scout_acc = 0;
       } else if (p.td_as_bu > 0.0 && !p.top_down_only && !(L == 1 && list_from_prologue) && L > 0 &&
@@ -2340,6 +2386,8 @@ void bfs_fill_params(const DevLayout& L, BfsState& S, BfsParams& p) {
   if (const char* e = getenv("ETB_SPLIT_RATIO")) p.split_ratio = atof(e);
   if (const char* e = getenv("ETB_SPLIT_DIV")) split_div = std::max(1.0, atof(e));
   p.split_bound = static_cast<uint32_t>(std::max(32.0, static_cast<double>(L.nc) / split_div));
+  p.split_tdw = kSplitTdwDefault;
+  if (const char* e = getenv("ETB_SPLIT_TDW")) p.split_tdw = static_cast<uint32_t>(atoi(e));
   p.trace = nullptr;
   p.level_claims = nullptr;
   p.bstamp = nullptr;

@@ -75,6 +75,11 @@ struct BfsParams {
   // top-down from a filtered list. Same claimed set, depths and α/β sequence.
   double split_ratio;
   uint32_t split_bound;
+  // The split level's halves: 0 = bottom-up, grid barrier, top-down; 1..32 = that
+  // many warps per CTA run the top-down half first, beside the others' bottom-up
+  // runs, then join them; 33.. = every warp goes from the bottom-up runs straight
+  // to the top-down chunks; 0xFFFF = 16 or the latter by the tail's edge count
+  uint32_t split_tdw;
   // small-core kernel: list-less top-down levels with at least this many
   // frontier edges claim atomic-free and count afterwards (as the large-core
   // kernel's); smaller ones claim with returning atomics
